@@ -1,0 +1,1380 @@
+// rt3d.cu — librt3d.so: the B200 RT3D path behind include/rt3d.h.
+//
+// One persistent cooperative kernel runs a whole frame (init + PALM
+// iterations, reconstruct.hpp:457-489): every data-dependent decision of the
+// reference (backtracking accept/reject, reconstruct.hpp:274-292; the stop
+// rule, :475-477; prune counts) is taken on the device between grid
+// barriers, so a frame is one launch with no host round trip.  The same
+// device phases serve the fine-grained operators (nll, gradients, init,
+// palm_step) through the program switch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rt3d.h"
+#include "rt3d_frame.cuh"
+
+using namespace rt3d;
+
+static_assert(sizeof(StepDiagDev) == sizeof(rt3d_step_diag), "diag layout");
+static_assert(sizeof(rt3d_point) == 64, "point layout");
+
+// ===========================================================================
+// device: persistent frame kernel
+// ===========================================================================
+namespace rt3d {
+
+template <int KIND>
+__device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc, int rc, int bc,
+                          int sc, int op, int it) {
+    while (!ld_cg(&F.ctl->done)) {
+        SweepCtx X;
+        X.alpha = ld_cg(&F.ctl->alpha);
+        X.cfloor = 1e-3 * ld_cg(&F.ctl->cmax) + 1e-30;
+        X.tc = tc;
+        X.rc = rc;
+        X.bc = bc;
+        X.sc = sc;
+        X.apply_floor = 0;
+        tree_sweep<KIND>(F, sm, X, op, it);
+        grid.sync();
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
+    __shared__ Smem sm;
+    cg::grid_group grid = cg::this_grid();
+    if (threadIdx.x == 0 && !F.irf_of_pix) sm.irf0 = F.irfs[0];
+    __syncthreads();
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const int prog = F.cfg.program;
+    if (leader) F.ctl->t_start = globaltimer();
+
+    int tc = F.tc0, rc = F.rc0, bc = F.bc0, sc = F.sc0;
+    if (prog == PROG_RECON || prog == PROG_INIT || prog == PROG_BASELINE || prog == PROG_PEAKS) {
+        phase_init_peaks(F, sm);
+        grid.sync();
+        if (prog == PROG_PEAKS) return;
+        const bool baseline = prog == PROG_BASELINE;
+        const int s2 = F.s * F.s;
+        scan_stage_a(F, sm, [&](uint32_t p) {
+            uint32_t nv = F.nval[p];
+            return baseline ? (nv > 0 ? 1u : 0u) : nv * (uint32_t)s2;
+        });
+        grid.sync();
+        phase_spawn(F, sm, baseline);
+        grid.sync();
+        tc = rc = bc = sc = 0;
+        if (prog != PROG_RECON) {
+            if (leader) {
+                F.ctl->tc_end = tc;
+                F.ctl->rc_end = rc;
+                F.ctl->bc_end = bc;
+                F.ctl->sc_end = sc;
+                F.ctl->t_end = globaltimer();
+            }
+            return;
+        }
+    }
+    if (leader) F.ctl->t_init = globaltimer();
+
+    SweepCtx X0;
+    X0.alpha = 0.0;
+    X0.cfloor = 0.0;
+    X0.tc = tc;
+    X0.rc = rc;
+    X0.bc = bc;
+    X0.sc = sc;
+    X0.apply_floor = 0;
+
+    if (prog == PROG_NLL) {
+        tree_sweep<K_NLL>(F, sm, X0, OP_RESULT, 0);
+        return;
+    }
+    if (prog == PROG_GRADS) {
+        tree_sweep<K_GRAD_T>(F, sm, X0, OP_RESULT, 0);
+        grid.sync();
+        tree_sweep<K_GRAD_R>(F, sm, X0, OP_RESULT, 0);
+        grid.sync();
+        tree_sweep<K_GRAD_B>(F, sm, X0, OP_RESULT, 0);
+        return;
+    }
+
+    // ---- PALM iterations (reconstruct.hpp:300-435, 466-478) ----
+    tree_sweep<K_GRAD_T>(F, sm, X0, OP_GRAD_T_FIRST, 0);
+    grid.sync();
+    const uint32_t nth = gridDim.x * kBlock;
+    const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
+    for (int it = 0; it < F.cfg.max_iters; ++it) {
+        const uint32_t P = ld_cg(&F.ctl->P);
+        if (leader) {
+            StepDiagDev& d = F.diag[it];
+            d.nll_before = ld_cg(&F.ctl->nll_cur);
+            d.points_before = P;
+            if (P == 0) {
+                d.blk[0].nll_after_grad = d.blk[0].nll_after_denoise = d.nll_before;
+                d.blk[1].nll_after_grad = d.blk[1].nll_after_denoise = d.nll_before;
+            }
+        }
+        if (P > 0) {
+            // depth block: safeguarded step, APSS, pin
+            cand_loop<K_CAND_T>(F, sm, grid, tc, rc, bc, sc, OP_CAND_T, it);
+            if (ld_cg(&F.ctl->accept)) tc ^= 1;
+            phase_apss(F, tc, sc, P);
+            grid.sync();
+            tc ^= 1;
+            SweepCtx X = X0;
+            X.tc = tc;
+            X.rc = rc;
+            X.bc = bc;
+            X.sc = sc;
+            tree_sweep<K_GRAD_R>(F, sm, X, OP_GRAD_R, it);
+            grid.sync();
+            // intensity block: safeguarded step, kNN filter, prune
+            cand_loop<K_CAND_R>(F, sm, grid, tc, rc, bc, sc, OP_CAND_R, it);
+            if (ld_cg(&F.ctl->accept)) rc ^= 1;
+            phase_knn(F, tc, rc, sc, P);
+            grid.sync();
+            rc ^= 1;
+            phase_prune_a(F, sm, rc, sc);
+            grid.sync();
+            phase_prune_b(F, sm, tc, rc, sc);
+            grid.sync();
+            tc ^= 1;
+            rc ^= 1;
+            sc ^= 1;
+            X.tc = tc;
+            X.rc = rc;
+            X.sc = sc;
+            tree_sweep<K_GRAD_B>(F, sm, X, OP_GRAD_B_PRUNED, it);
+            grid.sync();
+        } else {
+            tree_sweep<K_GRAD_B>(F, sm, X0, OP_GRAD_B_EMPTY, it);
+            grid.sync();
+        }
+        // background block: safeguarded step, FFT low-pass, floor
+        cand_loop<K_CAND_B>(F, sm, grid, tc, rc, bc, sc, OP_CAND_B, it);
+        if (ld_cg(&F.ctl->accept)) bc ^= 1;
+        if (F.cfg.bg_mode == 1) {
+            const int nr = F.rows, nc = F.cols;
+            double* re = F.fft_re;
+            double* im = F.fft_im;
+            double* re2 = F.fft_re + F.npix;
+            double* im2 = F.fft_im + F.npix;
+            fft_stage1(F.b[bc], re, im, nr, nc, gtid, nth);
+            grid.sync();
+            fft_stage2(re, im, re2, im2, nr, nc, F.cfg.cutoff, gtid, nth);
+            grid.sync();
+            fft_stage3(re2, im2, re, im, nr, nc, gtid, nth);
+            grid.sync();
+            fft_stage4(re, im, F.b[bc], nr, nc, 1, gtid, nth);
+            grid.sync();
+        }
+        SweepCtx X = X0;
+        X.tc = tc;
+        X.rc = rc;
+        X.bc = bc;
+        X.sc = sc;
+        X.apply_floor = 1;
+        tree_sweep<K_GRAD_T>(F, sm, X, OP_GRAD_T_END, it);
+        grid.sync();
+        X0 = X;
+        X0.apply_floor = 0;
+        if (ld_cg(&F.ctl->stop)) break;
+    }
+    if (leader) {
+        F.ctl->tc_end = tc;
+        F.ctl->rc_end = rc;
+        F.ctl->bc_end = bc;
+        F.ctl->sc_end = sc;
+        F.ctl->t_end = globaltimer();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Operators on arbitrary clouds (denoise.hpp:159-248): neighbour sets by
+// brute force in ascending index order (identical to SpatialIndex::query's
+// sorted ball, spatial_index.hpp:31-47).
+// ---------------------------------------------------------------------------
+struct CloudSoA {
+    const double* x;
+    const double* y;
+    const double* z;
+    const double* r;
+    uint32_t n;
+};
+
+template <typename Fn>
+__device__ __forceinline__ void for_each_brute(const CloudSoA& c, const Pos& q, double r2, Fn fn) {
+    for (uint32_t m = 0; m < c.n; ++m) {
+        Pos o{c.x[m], c.y[m], c.z[m]};
+        const double dx = o.x - q.x, dy = o.y - q.y, dz = o.z - q.z;
+        const double d2 = dx * dx + dy * dy + dz * dz;
+        if (d2 <= r2) fn(m, o, d2);
+    }
+}
+
+__global__ void apss_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA idx, double R,
+                                    int min_nbrs, double eps, rt3d_point* out) {
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    rt3d_point p = in[k];
+    Pos q{p.x, p.y, p.z};
+    uint8_t fl = p.flags & (uint8_t)~(1u | 4u);
+    Pos o;
+    auto each = [&](double r2, auto fn) { for_each_brute(idx, q, r2, fn); };
+    if (apss_point(each, q, R, min_nbrs, eps, fl, o)) {
+        p.x = o.x;
+        p.y = o.y;
+        p.z = o.z;
+    }
+    p.flags = fl;
+    out[k] = p;
+}
+
+__global__ void knn_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA idx, int kk,
+                                   double radius, rt3d_point* out) {
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    rt3d_point p = in[k];
+    Pos q{p.x, p.y, p.z};
+    auto each = [&](double r2, auto fn) { for_each_brute(idx, q, r2, fn); };
+    p.intensity = knn_mean(each, kk, radius * radius, p.intensity,
+                           [&](uint32_t m) { return idx.r[m]; });
+    out[k] = p;
+}
+
+__global__ void split_cloud_kernel(const rt3d_point* in, uint32_t n, double* x, double* y,
+                                   double* z, double* r) {
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    x[k] = in[k].x;
+    y[k] = in[k].y;
+    z[k] = in[k].z;
+    r[k] = in[k].intensity;
+}
+
+// prune on an arbitrary cloud: keep flags + per-block counts, then scatter
+__global__ void prune_count_kernel(const rt3d_point* in, uint32_t n, double rmin, uint32_t* bcnt) {
+    __shared__ unsigned int c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n && in[k].intensity >= rmin) atomicAdd(&c, 1u);
+    __syncthreads();
+    if (threadIdx.x == 0) bcnt[blockIdx.x] = c;
+}
+
+__global__ void prune_scatter_kernel(const rt3d_point* in, uint32_t n, double rmin,
+                                     const uint32_t* bcnt, rt3d_point* out, uint32_t* total) {
+    __shared__ unsigned int base;
+    __shared__ unsigned int keep[kBlock];
+    if (threadIdx.x == 0) {
+        unsigned int s = 0;
+        for (uint32_t b = 0; b < blockIdx.x; ++b) s += bcnt[b];
+        base = s;
+        if (blockIdx.x == gridDim.x - 1) *total = s + bcnt[blockIdx.x];
+    }
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    keep[threadIdx.x] = (k < n && in[k].intensity >= rmin) ? 1u : 0u;
+    __syncthreads();
+    if (keep[threadIdx.x]) {
+        unsigned int o = base;
+        for (unsigned int q = 0; q < threadIdx.x; ++q) o += keep[q];
+        out[o] = in[k];
+    }
+}
+
+__global__ void fft_kernel(const double* img, double* out, double* re, double* im, double* re2,
+                           double* im2, int nr, int nc, double cutoff, int clamp_nonneg) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t nth = gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    fft_stage1(img, re, im, nr, nc, gtid, nth);
+    grid.sync();
+    fft_stage2(re, im, re2, im2, nr, nc, cutoff, gtid, nth);
+    grid.sync();
+    fft_stage3(re2, im2, re, im, nr, nc, gtid, nth);
+    grid.sync();
+    fft_stage4(re, im, out, nr, nc, clamp_nonneg, gtid, nth);
+}
+
+// SoA state -> AoS rt3d_point (cloud order), positions per world_from_lidar
+// (sensor.hpp:200-203) or the baseline's coarse-centre placement
+// (eval.hpp:116-118).
+__global__ void gather_points_kernel(Frame F, uint32_t P, int tc, int rc, int sc, int baseline,
+                                     rt3d_point* out) {
+    uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= P) return;
+    rt3d_point q;
+    const uint32_t p = F.pix[sc][n];
+    const int i = (int)(p / F.cols), j = (int)(p % F.cols);
+    q.i = i;
+    q.j = j;
+    q.fi = F.fi[sc][n];
+    q.fj = F.fj[sc][n];
+    q.t = F.t[tc][n];
+    q.intensity = F.r[rc][n];
+    q.flags = F.fl[sc][n];
+    for (int k = 0; k < 7; ++k) q.pad_[k] = 0;
+    if (baseline) {
+        const double coarse_pitch = F.pitch * F.s;
+        q.x = (i + 0.5) * coarse_pitch;
+        q.y = (j + 0.5) * coarse_pitch;
+    } else {
+        q.x = (q.fi + 0.5) * F.pitch;
+        q.y = (q.fj + 0.5) * F.pitch;
+    }
+    q.z = q.t * F.bres;
+    out[n] = q;
+}
+
+}  // namespace rt3d
+
+// ===========================================================================
+// host
+// ===========================================================================
+namespace {
+
+thread_local std::string g_err;
+
+rt3d_status fail(rt3d_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(RT3D_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                            \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max<size_t>(bytes, 256);
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct rt3d_session {
+    int device = 0;
+    int nsm = 0;
+    cudaStream_t stream = nullptr;
+    int grid_frame = 0;  // cooperative grid of frame_kernel
+    int grid_fft = 0;
+    // sensor
+    bool have_sensor = false;
+    int rows = 0, cols = 0, bins = 0, s = 1;
+    double pitch = 1, bres = 1;
+    bool per_pixel_irf = false;
+    DevBuf irfs, irf_tab, irf_of_pix, gain, dead;
+    // cube
+    bool have_cube = false;
+    int c_rows = 0, c_cols = 0, c_bins = 0;
+    uint64_t n_events = 0;
+    DevBuf off, ev;
+    // state
+    DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
+    size_t pcap = 0;
+    DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot;
+    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im;
+    DevBuf ctl, diag, trace, outpts, misc;
+    Ctl* h_ctl = nullptr;  // pinned staging
+    // state description
+    bool have_state = false;
+    bool baseline_state = false;
+    bool state_pinned = true;
+    uint32_t P = 0;
+    int tc = 0, rc = 0, bc = 0, sc = 0;
+    std::vector<uint32_t> perm;  // device order -> caller's cloud order (nll/grads API)
+    // last reconstruct report
+    int iterations = 0;
+    int report_iters_cap = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+rt3d_status check_session(rt3d_session* s) {
+    if (!s) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session");
+    return RT3D_OK;
+}
+
+int tree_depth(uint32_t npix) {
+    int G = 0;
+    while (((uint64_t)npix + (1ull << G) - 1) >> G > 32) ++G;
+    return G;
+}
+
+rt3d_status ensure_state(rt3d_session* s, size_t pcap, size_t npix) {
+    size_t pc = std::max<size_t>(pcap, 1);
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(s->t[k].ensure(pc * 8));
+        CUDA_TRY(s->r[k].ensure(pc * 8));
+        CUDA_TRY(s->pix[k].ensure(pc * 4));
+        CUDA_TRY(s->fi[k].ensure(pc * 4));
+        CUDA_TRY(s->fj[k].ensure(pc * 4));
+        CUDA_TRY(s->fl[k].ensure(pc));
+        CUDA_TRY(s->b[k].ensure(npix * 8));
+        CUDA_TRY(s->bo[k].ensure((npix + 1) * 4));
+    }
+    CUDA_TRY(s->gt.ensure(pc * 8));
+    CUDA_TRY(s->ct.ensure(pc * 8));
+    CUDA_TRY(s->gr.ensure(pc * 8));
+    CUDA_TRY(s->cr.ensure(pc * 8));
+    CUDA_TRY(s->oog.ensure(pc));
+    CUDA_TRY(s->gb.ensure(npix * 8));
+    CUDA_TRY(s->cb.ensure(npix * 8));
+    s->pcap = std::max(s->pcap, pc);
+    return RT3D_OK;
+}
+
+rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters) {
+    if (!s->have_sensor) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no sensor set");
+    if (!s->have_cube) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no cube set");
+    if (s->rows != s->c_rows || s->cols != s->c_cols || s->bins != s->c_bins)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "likelihood: state/cube dimension mismatch");
+    std::memset(&F, 0, sizeof F);
+    const uint32_t npix = (uint32_t)s->rows * (uint32_t)s->cols;
+    F.rows = s->rows;
+    F.cols = s->cols;
+    F.bins = s->bins;
+    F.s = s->s;
+    F.frows = s->rows * s->s;
+    F.fcols = s->cols * s->s;
+    F.pitch = s->pitch;
+    F.bres = s->bres;
+    F.tlim = (double)s->bins * (1.0 - 1e-12);  // reconstruct.hpp:331
+    F.irfs = s->irfs.as<IrfDev>();
+    F.irf_of_pix = s->per_pixel_irf ? s->irf_of_pix.as<uint32_t>() : nullptr;
+    F.gain = s->gain.as<double>();
+    F.dead = s->dead.as<uint8_t>();
+    F.npix = npix;
+    F.off = s->off.as<uint32_t>();
+    F.ev = s->ev.as<uint2>();
+    F.G = tree_depth(npix);
+    F.Gb = std::max(0, F.G - 3);
+    F.wpb = 1 << (F.G - F.Gb);
+    F.nbn = 1u << F.Gb;
+    // scratch
+    CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 8));
+    CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
+    CUDA_TRY(s->bmax.ensure((size_t)s->grid_frame * 8));
+    CUDA_TRY(s->cnt.ensure((size_t)npix * 4));
+    CUDA_TRY(s->btot.ensure((size_t)s->grid_frame * 4));
+    const size_t nslot = (size_t)npix * std::max(cfg.K, 1);
+    CUDA_TRY(s->pk_t.ensure(nslot * 8));
+    CUDA_TRY(s->pk_resp.ensure(nslot * 8));
+    CUDA_TRY(s->pk_mass.ensure(nslot * 8));
+    CUDA_TRY(s->pk_int.ensure(nslot * 8));
+    CUDA_TRY(s->npk.ensure((size_t)npix * 4));
+    CUDA_TRY(s->nval.ensure((size_t)npix * 4));
+    if (cfg.bg_mode == 1) {
+        CUDA_TRY(s->fft_re.ensure((size_t)npix * 16));
+        CUDA_TRY(s->fft_im.ensure((size_t)npix * 16));
+    }
+    CUDA_TRY(s->ctl.ensure(sizeof(Ctl)));
+    CUDA_TRY(s->diag.ensure(sizeof(StepDiagDev) * std::max(max_iters, 1)));
+    CUDA_TRY(s->trace.ensure(8 * (std::max(max_iters, 1) + 1)));
+    for (int k = 0; k < 2; ++k) {
+        F.t[k] = s->t[k].as<double>();
+        F.r[k] = s->r[k].as<double>();
+        F.b[k] = s->b[k].as<double>();
+        F.pix[k] = s->pix[k].as<uint32_t>();
+        F.fi[k] = s->fi[k].as<int32_t>();
+        F.fj[k] = s->fj[k].as<int32_t>();
+        F.fl[k] = s->fl[k].as<uint8_t>();
+        F.bo[k] = s->bo[k].as<uint32_t>();
+    }
+    F.gt = s->gt.as<double>();
+    F.ct = s->ct.as<double>();
+    F.gr = s->gr.as<double>();
+    F.cr = s->cr.as<double>();
+    F.gb = s->gb.as<double>();
+    F.cb = s->cb.as<double>();
+    F.oog = s->oog.as<uint8_t>();
+    F.lam = s->lam.as<double>();
+    F.blk = s->blk.as<double>();
+    F.bmax = s->bmax.as<double>();
+    F.cnt = s->cnt.as<uint32_t>();
+    F.btot = s->btot.as<uint32_t>();
+    F.pk_t = s->pk_t.as<double>();
+    F.pk_resp = s->pk_resp.as<double>();
+    F.pk_mass = s->pk_mass.as<double>();
+    F.pk_int = s->pk_int.as<double>();
+    F.npk = s->npk.as<uint32_t>();
+    F.nval = s->nval.as<uint32_t>();
+    F.fft_re = s->fft_re.as<double>();
+    F.fft_im = s->fft_im.as<double>();
+    F.ctl = s->ctl.as<Ctl>();
+    F.diag = s->diag.as<StepDiagDev>();
+    F.trace = s->trace.as<double>();
+    F.cfg = cfg;
+    F.cfg.max_iters = max_iters;
+    F.tc0 = s->tc;
+    F.rc0 = s->rc;
+    F.bc0 = s->bc;
+    F.sc0 = s->sc;
+    return RT3D_OK;
+}
+
+rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
+    Ctl* h = s->h_ctl;
+    std::memset(h, 0, sizeof(Ctl));
+    h->P = P_init;
+    CUDA_TRY(cudaMemcpyAsync(F.ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemsetAsync(F.diag, 0, sizeof(StepDiagDev) * std::max(F.cfg.max_iters, 1),
+                             s->stream));
+    void* args[] = {&F};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)frame_kernel, dim3(s->grid_frame),
+                                         dim3(kBlock), args, 0, s->stream));
+    return RT3D_OK;
+}
+
+rt3d_status read_ctl(rt3d_session* s) {
+    CUDA_TRY(cudaMemcpyAsync(s->h_ctl, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+Cfg cfg_from(const rt3d_recon_config* c, int program) {
+    Cfg g;
+    std::memset(&g, 0, sizeof g);
+    g.program = program;
+    g.max_iters = c->max_iters;
+    g.stop_tol = c->stop_tol;
+    g.step_auto[0] = c->step_t_auto != 0;
+    g.step_auto[1] = c->step_r_auto != 0;
+    g.step_auto[2] = c->step_b_auto != 0;
+    g.step[0] = c->step_t;
+    g.step[1] = c->step_r;
+    g.step[2] = c->step_b;
+    g.beta = c->backtrack_beta;
+    g.R = c->apss.kernel_radius;
+    g.eps = c->apss.sphere_degeneracy_eps;
+    g.min_nbrs = c->apss.min_neighbors;
+    g.knn_k = c->knn_k;
+    g.r_min = c->r_min;
+    g.bg_mode = c->background_mode;
+    g.cutoff = c->fft_cutoff;
+    g.K = c->init.max_returns;
+    g.sep = c->init.min_separation;
+    g.thr = c->init.peak_threshold;
+    return g;
+}
+
+// ReconConfig::validate (reconstruct.hpp:68-77) + ApssParams/InitParams
+rt3d_status validate_cfg(const rt3d_recon_config* c) {
+    if (!c) return fail(RT3D_ERR_INVALID_ARGUMENT, "null config");
+    if (c->max_iters < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "ReconConfig: max_iters >= 1");
+    if (c->stop_tol < 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "ReconConfig: stop_tol >= 0");
+    if (c->backtrack_beta <= 0.0 || c->backtrack_beta >= 1.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ReconConfig: backtrack_beta in (0,1)");
+    if (c->knn_k < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "ReconConfig: knn_k >= 1");
+    if (c->r_min < 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "ReconConfig: r_min >= 0");
+    if (c->apss.kernel_radius <= 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: kernel_radius must be positive");
+    if (c->apss.min_neighbors < 4)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: min_neighbors must be >= 4");
+    if (c->apss.sphere_degeneracy_eps < 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: sphere_degeneracy_eps must be >= 0");
+    if (c->init.max_returns < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "InitParams: max_returns >= 1");
+    if (c->init.min_separation < 1)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "InitParams: min_separation >= 1");
+    if (c->init.peak_threshold < 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "InitParams: peak_threshold >= 0");
+    if (c->init.max_returns > kMaxReturns)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: max_returns > %d not supported on device",
+                    kMaxReturns);
+    if (c->background_mode == 1 && (c->fft_cutoff <= 0.0 || c->fft_cutoff > 1.0))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "fft_lowpass_filter: cutoff must be in (0, 1]");
+    return RT3D_OK;
+}
+
+rt3d_status require_device(rt3d_session* s) {
+    rt3d_status st = check_session(s);
+    if (st) return st;
+    CUDA_TRY(cudaSetDevice(s->device));
+    return RT3D_OK;
+}
+
+// window half-width for the pinned neighbourhood search
+int window_w(double R, double pitch) { return (int)std::floor(R / pitch) + 1; }
+
+}  // namespace
+
+namespace {
+template <typename T>
+rt3d_status copy_per_point(rt3d_session* s, T* out, const void* dev) {
+    if (!out || !s->P) return RT3D_OK;
+    if (s->perm.empty()) {
+        CUDA_TRY(cudaMemcpyAsync(out, dev, sizeof(T) * s->P, cudaMemcpyDeviceToHost, s->stream));
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+        return RT3D_OK;
+    }
+    std::vector<T> tmp(s->P);
+    CUDA_TRY(cudaMemcpyAsync(tmp.data(), dev, sizeof(T) * s->P, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    for (size_t k = 0; k < s->P; ++k) out[s->perm[k]] = tmp[k];
+    return RT3D_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int rt3d_abi_version(void) { return RT3D_ABI_VERSION; }
+const char* rt3d_last_error(void) { return g_err.c_str(); }
+
+int rt3d_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+rt3d_status rt3d_session_create(int device, rt3d_session** out) {
+    if (!out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null out");
+    *out = nullptr;
+    int n = rt3d_device_count();
+    if (n <= 0) return fail(RT3D_ERR_NO_DEVICE, "rt3d: no CUDA device (there is no CPU fallback)");
+    if (device < 0 || device >= n) return fail(RT3D_ERR_INVALID_ARGUMENT, "bad device %d", device);
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(RT3D_ERR_NO_DEVICE, "rt3d: built for sm_100a, device is sm_%d%d", prop.major,
+                    prop.minor);
+    rt3d_session* s = new rt3d_session();
+    s->device = device;
+    s->nsm = prop.multiProcessorCount;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel, kBlock, 0));
+    if (per_sm < 1) {
+        delete s;
+        return fail(RT3D_ERR_CUDA, "rt3d: frame kernel does not fit on an SM");
+    }
+    const char* env = getenv("RT3D_BLOCKS_PER_SM");
+    int want = env ? atoi(env) : 1;
+    if (want < 1) want = 1;
+    s->grid_frame = s->nsm * std::min(per_sm, want);
+    int per_sm_fft = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock, 0));
+    s->grid_fft = s->nsm * std::max(1, per_sm_fft);
+    CUDA_TRY(cudaMallocHost(&s->h_ctl, sizeof(Ctl)));
+    CUDA_TRY(cudaEventCreate(&s->ev0));
+    CUDA_TRY(cudaEventCreate(&s->ev1));
+    *out = s;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_session_destroy(rt3d_session* s) {
+    if (!s) return RT3D_OK;
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->stream);
+    DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
+                      &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk,
+                      &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
+                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->ctl, &s->diag,
+                      &s->trace, &s->outpts, &s->misc};
+    for (DevBuf* b : bufs) b->release();
+    for (int k = 0; k < 2; ++k) {
+        s->t[k].release();
+        s->r[k].release();
+        s->b[k].release();
+        s->pix[k].release();
+        s->fi[k].release();
+        s->fj[k].release();
+        s->fl[k].release();
+        s->bo[k].release();
+    }
+    if (s->h_ctl) cudaFreeHost(s->h_ctl);
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->stream) cudaStreamDestroy(s->stream);
+    delete s;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_session_synchronize(rt3d_session* s) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+// --- IRF tables (sensor.hpp:26-41, 63, reconstruct.hpp:126-127) ------------
+static rt3d_status irf_check(const rt3d_irf& f) {
+    if (f.dtau <= 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "Irf: dtau must be positive");
+    if (f.n_samples < 2 || !f.samples) return fail(RT3D_ERR_INVALID_ARGUMENT, "Irf: need >= 2 samples");
+    for (uint64_t k = 0; k < f.n_samples; ++k)
+        if (f.samples[k] < 0.0 || !std::isfinite(f.samples[k]))
+            return fail(RT3D_ERR_INVALID_ARGUMENT, "Irf: samples must be finite and >= 0");
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* v) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!v) return fail(RT3D_ERR_INVALID_ARGUMENT, "null sensor");
+    if (v->n_rows <= 0 || v->n_cols <= 0 || v->n_bins <= 0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "SensorModel: dimensions must be positive");
+    if (v->superres < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "SensorModel: superres must be >= 1");
+    if (v->pixel_pitch <= 0.0 || v->bin_resolution <= 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "SensorModel: pitch/bin resolution must be positive");
+    if (!v->gain || !v->dead) return fail(RT3D_ERR_INVALID_ARGUMENT, "SensorModel: gain/dead required");
+    const size_t npix = (size_t)v->n_rows * v->n_cols;
+    if (npix >= (1ull << 31)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: too many pixels");
+    const size_t nirf = v->irf_per_pixel ? npix : 1;
+    std::vector<IrfDev> descs(nirf);
+    size_t total = 0;
+    for (size_t k = 0; k < nirf; ++k) {
+        const rt3d_irf& f = v->irf_per_pixel ? v->irf_per_pixel[k] : v->irf_shared;
+        if ((st = irf_check(f))) return st;
+        total += 2 * f.n_samples;
+    }
+    if (!v->irf_per_pixel && (st = irf_check(v->irf_shared))) return st;
+    std::vector<double> tab(total);
+    size_t o = 0;
+    std::vector<size_t> offs(nirf);
+    for (size_t k = 0; k < nirf; ++k) {
+        const rt3d_irf& f = v->irf_per_pixel ? v->irf_per_pixel[k] : v->irf_shared;
+        offs[k] = o;
+        double hmax = 0.0;
+        for (uint64_t q = 0; q < f.n_samples; ++q) {
+            tab[o + q] = f.samples[q];
+            hmax = std::max(hmax, f.samples[q]);
+        }
+        for (uint64_t q = 0; q + 1 < f.n_samples; ++q)
+            tab[o + f.n_samples + q] = (f.samples[q + 1] - f.samples[q]) / f.dtau;
+        IrfDev& d = descs[k];
+        d.tau_min = f.tau_min;
+        d.dtau = f.dtau;
+        d.tau_max = f.tau_min + f.dtau * (double)(f.n_samples - 1);
+        d.h_max = hmax;
+        d.n = (uint32_t)f.n_samples;
+        o += 2 * f.n_samples;
+    }
+    CUDA_TRY(s->irf_tab.ensure(total * 8));
+    CUDA_TRY(s->irfs.ensure(nirf * sizeof(IrfDev)));
+    for (size_t k = 0; k < nirf; ++k) {
+        descs[k].s = s->irf_tab.as<double>() + offs[k];
+        descs[k].d = s->irf_tab.as<double>() + offs[k] + descs[k].n;
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->irf_tab.p, tab.data(), total * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->irfs.p, descs.data(), nirf * sizeof(IrfDev), cudaMemcpyHostToDevice,
+                             s->stream));
+    if (v->irf_per_pixel) {
+        std::vector<uint32_t> idx(npix);
+        for (size_t p = 0; p < npix; ++p) idx[p] = (uint32_t)p;
+        CUDA_TRY(s->irf_of_pix.ensure(npix * 4));
+        CUDA_TRY(cudaMemcpyAsync(s->irf_of_pix.p, idx.data(), npix * 4, cudaMemcpyHostToDevice, s->stream));
+    }
+    CUDA_TRY(s->gain.ensure(npix * 8));
+    CUDA_TRY(s->dead.ensure(npix));
+    CUDA_TRY(cudaMemcpyAsync(s->gain.p, v->gain, npix * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->dead.p, v->dead, npix, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->have_sensor = true;
+    s->per_pixel_irf = v->irf_per_pixel != nullptr;
+    s->rows = v->n_rows;
+    s->cols = v->n_cols;
+    s->bins = v->n_bins;
+    s->s = v->superres;
+    s->pitch = v->pixel_pitch;
+    s->bres = v->bin_resolution;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!c) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube");
+    // PhotonCube::validate, cube.hpp:84-112
+    if (c->n_rows <= 0 || c->n_cols <= 0 || c->n_bins <= 0)
+        return fail(RT3D_ERR_FORMAT, "cube: non-positive dimensions");
+    const size_t npix = (size_t)c->n_rows * c->n_cols;
+    if (!c->offsets || c->offsets[0] != 0 || c->offsets[npix] != c->n_events)
+        return fail(RT3D_ERR_FORMAT, "cube: bad offset table");
+    if (c->n_events >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: >= 2^32 events");
+    std::vector<uint32_t> off32(npix + 1);
+    for (size_t p = 0; p < npix; ++p) {
+        if (c->offsets[p] > c->offsets[p + 1])
+            return fail(RT3D_ERR_FORMAT, "cube: negative event range at pixel %zu", p);
+        uint32_t prev = 0;
+        bool first = true;
+        for (uint64_t k = c->offsets[p]; k < c->offsets[p + 1]; ++k) {
+            const rt3d_event& e = c->events[k];
+            if (e.bin >= (uint32_t)c->n_bins)
+                return fail(RT3D_ERR_FORMAT, "cube: bin out of range at pixel %zu", p);
+            if (e.count < 1) return fail(RT3D_ERR_FORMAT, "cube: zero count at pixel %zu", p);
+            if (!first && e.bin <= prev)
+                return fail(RT3D_ERR_FORMAT, "cube: bins not strictly increasing at pixel %zu", p);
+            prev = e.bin;
+            first = false;
+        }
+        off32[p] = (uint32_t)c->offsets[p];
+    }
+    off32[npix] = (uint32_t)c->offsets[npix];
+    CUDA_TRY(s->off.ensure((npix + 1) * 4));
+    CUDA_TRY(s->ev.ensure(std::max<uint64_t>(c->n_events, 1) * 8));
+    CUDA_TRY(cudaMemcpyAsync(s->off.p, off32.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+    if (c->n_events)
+        CUDA_TRY(cudaMemcpyAsync(s->ev.p, c->events, c->n_events * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->have_cube = true;
+    s->c_rows = c->n_rows;
+    s->c_cols = c->n_cols;
+    s->c_bins = c->n_bins;
+    s->n_events = c->n_events;
+    return RT3D_OK;
+}
+
+static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = validate_cfg(cfg))) return st;
+    Cfg g = cfg_from(cfg, program);
+    const size_t npix = (size_t)s->rows * s->cols;
+    const size_t pcap = program == PROG_BASELINE
+                            ? npix
+                            : (size_t)cfg->init.max_returns * s->s * s->s * npix;
+    if ((st = ensure_state(s, pcap, npix))) return st;
+    g.W = window_w(cfg->apss.kernel_radius, s->pitch);
+    g.set_oog_flags = 1;
+    s->tc = s->rc = s->bc = s->sc = 0;
+    Frame F;
+    if ((st = build_frame(s, F, g, program == PROG_RECON ? cfg->max_iters : 1))) return st;
+    CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+    if ((st = launch_frame(s, F, 0))) return st;
+    CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+    s->have_state = true;
+    s->baseline_state = program == PROG_BASELINE;
+    s->state_pinned = true;
+    s->perm.clear();
+    s->iterations = -1;  // resolved lazily (report / state queries)
+    s->report_iters_cap = program == PROG_RECON ? cfg->max_iters : 0;
+    return RT3D_OK;
+}
+
+static rt3d_status resolve_state(rt3d_session* s) {
+    if (!s->have_state) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no state in session");
+    if (s->iterations != -1) return RT3D_OK;
+    rt3d_status st = read_ctl(s);
+    if (st) return st;
+    const Ctl& c = *s->h_ctl;
+    s->P = c.P;
+    s->tc = c.tc_end;
+    s->rc = c.rc_end;
+    s->bc = c.bc_end;
+    s->sc = c.sc_end;
+    s->iterations = c.iterations;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
+    return run_init_like(s, cfg, PROG_RECON);
+}
+
+rt3d_status rt3d_init_matched_filter(rt3d_session* s, const rt3d_init_params* p) {
+    if (!p) return fail(RT3D_ERR_INVALID_ARGUMENT, "null params");
+    rt3d_recon_config c;
+    std::memset(&c, 0, sizeof c);
+    c.max_iters = 1;
+    c.knn_k = 1;
+    c.backtrack_beta = 0.5;
+    c.apss.kernel_radius = 1.0;
+    c.apss.min_neighbors = 6;
+    c.init = *p;
+    return run_init_like(s, &c, PROG_INIT);
+}
+
+rt3d_status rt3d_baseline_xcorr(rt3d_session* s) {
+    rt3d_recon_config c;
+    std::memset(&c, 0, sizeof c);
+    c.max_iters = 1;
+    c.knn_k = 1;
+    c.backtrack_beta = 0.5;
+    c.apss.kernel_radius = 1.0;
+    c.apss.min_neighbors = 6;
+    c.init.max_returns = 1;
+    c.init.peak_threshold = 0.0;
+    c.init.min_separation = 1;
+    return run_init_like(s, &c, PROG_BASELINE);
+}
+
+rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null out");
+    if ((st = resolve_state(s))) return st;
+    if ((st = read_ctl(s))) return st;
+    const Ctl& c = *s->h_ctl;
+    std::memset(out, 0, sizeof *out);
+    out->iterations = c.iterations;
+    out->points = c.P;
+    out->init_nll = c.init_nll;
+    out->final_nll = c.prev;
+    out->init_seconds = c.t_init > c.t_start ? (c.t_init - c.t_start) * 1e-9 : 0.0;
+    out->iterate_seconds = c.t_end > c.t_init ? (c.t_end - c.t_init) * 1e-9 : 0.0;
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, s->ev0, s->ev1) == cudaSuccess) out->total_seconds = ms * 1e-3;
+    else cudaGetLastError();
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_report_copy(rt3d_session* s, double* trace, rt3d_step_diag* steps) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = resolve_state(s))) return st;
+    const int it = s->iterations;
+    if (trace)
+        CUDA_TRY(cudaMemcpyAsync(trace, s->trace.p, 8 * (it + 1), cudaMemcpyDeviceToHost, s->stream));
+    if (steps && it > 0)
+        CUDA_TRY(cudaMemcpyAsync(steps, s->diag.p, sizeof(rt3d_step_diag) * it,
+                                 cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_state_size(rt3d_session* s, uint64_t* n) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = resolve_state(s))) return st;
+    if (n) *n = s->P;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_state_copy(rt3d_session* s, rt3d_point* pts, double* background) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = resolve_state(s))) return st;
+    const size_t npix = (size_t)s->rows * s->cols;
+    if (pts && s->P) {
+        Frame F;
+        Cfg g;
+        std::memset(&g, 0, sizeof g);
+        if ((st = build_frame(s, F, g, 1))) return st;
+        CUDA_TRY(s->outpts.ensure((size_t)s->P * sizeof(rt3d_point)));
+        gather_points_kernel<<<(s->P + 255) / 256, 256, 0, s->stream>>>(
+            F, s->P, s->tc, s->rc, s->sc, s->baseline_state ? 1 : 0, s->outpts.as<rt3d_point>());
+        CUDA_TRY(cudaGetLastError());
+        if (s->perm.empty()) {
+            CUDA_TRY(cudaMemcpyAsync(pts, s->outpts.p, (size_t)s->P * sizeof(rt3d_point),
+                                     cudaMemcpyDeviceToHost, s->stream));
+        } else {
+            std::vector<rt3d_point> tmp(s->P);
+            CUDA_TRY(cudaMemcpyAsync(tmp.data(), s->outpts.p, (size_t)s->P * sizeof(rt3d_point),
+                                     cudaMemcpyDeviceToHost, s->stream));
+            CUDA_TRY(cudaStreamSynchronize(s->stream));
+            for (size_t k = 0; k < s->P; ++k) pts[s->perm[k]] = tmp[k];
+        }
+    }
+    if (background)
+        CUDA_TRY(cudaMemcpyAsync(background, s->b[s->bc].p, npix * 8, cudaMemcpyDeviceToHost,
+                                 s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_state_upload(rt3d_session* s, const rt3d_state_view* v) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!v) return fail(RT3D_ERR_INVALID_ARGUMENT, "null state");
+    if (!s->have_sensor) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no sensor set");
+    const size_t npix = (size_t)s->rows * s->cols;
+    const size_t n = v->n_points;
+    if (n >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: too many points");
+    if (!v->background) return fail(RT3D_ERR_INVALID_ARGUMENT, "null background");
+    // SceneState::refresh semantics (likelihood.hpp:38-55): stable counting
+    // sort of the cloud by home pixel.
+    std::vector<uint32_t> counts(npix, 0);
+    for (size_t k = 0; k < n; ++k) {
+        const rt3d_point& p = v->points[k];
+        if (p.i < 0 || p.i >= s->rows || p.j < 0 || p.j >= s->cols)
+            return fail(RT3D_ERR_INVALID_ARGUMENT, "SceneState: point home pixel out of bounds");
+        ++counts[(size_t)p.i * s->cols + p.j];
+    }
+    std::vector<uint32_t> bo(npix + 1, 0);
+    for (size_t p = 0; p < npix; ++p) bo[p + 1] = bo[p] + counts[p];
+    std::vector<uint32_t> order(n);
+    {
+        std::vector<uint32_t> cur(bo.begin(), bo.end() - 1);
+        for (size_t k = 0; k < n; ++k) {
+            const rt3d_point& p = v->points[k];
+            order[cur[(size_t)p.i * s->cols + p.j]++] = (uint32_t)k;
+        }
+    }
+    bool identity = true;
+    for (size_t k = 0; k < n && identity; ++k) identity = order[k] == k;
+    bool pinned = true;
+    std::vector<double> t(n), r(n);
+    std::vector<uint32_t> pix(n);
+    std::vector<int32_t> fi(n), fj(n);
+    std::vector<uint8_t> fl(n);
+    for (size_t k = 0; k < n; ++k) {
+        const rt3d_point& p = v->points[order[k]];
+        t[k] = p.t;
+        r[k] = p.intensity;
+        pix[k] = (uint32_t)((size_t)p.i * s->cols + p.j);
+        fi[k] = p.fi;
+        fj[k] = p.fj;
+        fl[k] = p.flags;
+        pinned = pinned && p.x == (p.fi + 0.5) * s->pitch && p.y == (p.fj + 0.5) * s->pitch &&
+                 p.fi >= 0 && p.fj >= 0 && p.fi / s->s == p.i && p.fj / s->s == p.j;
+    }
+    if ((st = ensure_state(s, n, npix))) return st;
+    s->tc = s->rc = s->bc = s->sc = 0;
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(s->t[0].p, t.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+        CUDA_TRY(cudaMemcpyAsync(s->r[0].p, r.data(), n * 8, cudaMemcpyHostToDevice, s->stream));
+        CUDA_TRY(cudaMemcpyAsync(s->pix[0].p, pix.data(), n * 4, cudaMemcpyHostToDevice, s->stream));
+        CUDA_TRY(cudaMemcpyAsync(s->fi[0].p, fi.data(), n * 4, cudaMemcpyHostToDevice, s->stream));
+        CUDA_TRY(cudaMemcpyAsync(s->fj[0].p, fj.data(), n * 4, cudaMemcpyHostToDevice, s->stream));
+        CUDA_TRY(cudaMemcpyAsync(s->fl[0].p, fl.data(), n, cudaMemcpyHostToDevice, s->stream));
+    }
+    CUDA_TRY(cudaMemcpyAsync(s->bo[0].p, bo.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->b[0].p, v->background, npix * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->have_state = true;
+    s->baseline_state = false;
+    s->state_pinned = pinned;
+    s->P = (uint32_t)n;
+    s->iterations = 0;
+    s->perm.clear();
+    if (!identity) s->perm = order;
+    return RT3D_OK;
+}
+
+static rt3d_status run_sweeps(rt3d_session* s, int program) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = resolve_state(s))) return st;
+    Cfg g;
+    std::memset(&g, 0, sizeof g);
+    g.program = program;
+    g.max_iters = 1;
+    Frame F;
+    if ((st = build_frame(s, F, g, 1))) return st;
+    if ((st = launch_frame(s, F, s->P))) return st;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_nll(rt3d_session* s, double* out) {
+    rt3d_status st = run_sweeps(s, PROG_NLL);
+    if (st) return st;
+    if ((st = read_ctl(s))) return st;
+    if (out) *out = s->h_ctl->result;
+    return RT3D_OK;
+}
+
+static rt3d_status run_grads(rt3d_session* s) { return run_sweeps(s, PROG_GRADS); }
+
+rt3d_status rt3d_grad_depth(rt3d_session* s, double* value, uint8_t* oog) {
+    rt3d_status st = run_grads(s);
+    if (st) return st;
+    if ((st = copy_per_point(s, value, s->gt.p))) return st;
+    return copy_per_point(s, oog, s->oog.p);
+}
+
+rt3d_status rt3d_grad_intensity(rt3d_session* s, double* out) {
+    rt3d_status st = run_grads(s);
+    if (st) return st;
+    return copy_per_point(s, out, s->gr.p);
+}
+
+rt3d_status rt3d_grad_background(rt3d_session* s, double* out) {
+    rt3d_status st = run_grads(s);
+    if (st) return st;
+    if (out) {
+        CUDA_TRY(cudaMemcpyAsync(out, s->gb.p, (size_t)s->rows * s->cols * 8,
+                                 cudaMemcpyDeviceToHost, s->stream));
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_block_curvatures(rt3d_session* s, double* depth, double* intensity,
+                                  double* background) {
+    rt3d_status st = run_grads(s);
+    if (st) return st;
+    if ((st = copy_per_point(s, depth, s->ct.p))) return st;
+    if ((st = copy_per_point(s, intensity, s->cr.p))) return st;
+    if (background) {
+        CUDA_TRY(cudaMemcpyAsync(background, s->cb.p, (size_t)s->rows * s->cols * 8,
+                                 cudaMemcpyDeviceToHost, s->stream));
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_palm_step(rt3d_session* s, const rt3d_recon_config* cfg, rt3d_step_diag* diag) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = validate_cfg(cfg))) return st;
+    if ((st = resolve_state(s))) return st;
+    if (!s->perm.empty())
+        return fail(RT3D_ERR_UNSUPPORTED,
+                    "rt3d: palm_step needs a pixel-ordered cloud (cloud order == bucket order)");
+    if (!s->state_pinned || s->baseline_state)
+        return fail(RT3D_ERR_UNSUPPORTED,
+                    "rt3d: palm_step needs points at their fine-pixel centres (world_from_lidar)");
+    Cfg g = cfg_from(cfg, PROG_PALM);
+    g.W = window_w(cfg->apss.kernel_radius, s->pitch);
+    g.set_oog_flags = 1;
+    if (cfg->background_mode == 1 && (s->rows < 2 || s->cols < 2))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "fft_lowpass_filter: image must be at least 2x2");
+    Frame F;
+    if ((st = build_frame(s, F, g, 1))) return st;
+    if ((st = launch_frame(s, F, s->P))) return st;
+    s->iterations = -1;
+    if ((st = resolve_state(s))) return st;
+    if (diag) {
+        CUDA_TRY(cudaMemcpyAsync(diag, s->diag.p, sizeof(rt3d_step_diag), cudaMemcpyDeviceToHost,
+                                 s->stream));
+        CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    s->iterations = 0;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_matched_filter_peaks(rt3d_session* s, const rt3d_event* events, uint64_t n,
+                                      const rt3d_irf* irf, int32_t n_bins, int32_t k,
+                                      double threshold, int32_t min_sep, rt3d_peak* out,
+                                      int32_t* n_out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!irf || !out || !n_out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null argument");
+    if (k > kMaxReturns) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: k > %d", kMaxReturns);
+    *n_out = 0;
+    if (n == 0 || k < 1) return RT3D_OK;
+    // a 1x1 sensor + cube holding the pixel; the session's own sensor/cube
+    // are replaced (documented in rt3d.h usage of this test entry point)
+    double gain = 1.0;
+    uint8_t dead = 0;
+    rt3d_sensor sv;
+    std::memset(&sv, 0, sizeof sv);
+    sv.n_rows = sv.n_cols = 1;
+    sv.n_bins = n_bins;
+    sv.superres = 1;
+    sv.pixel_pitch = sv.bin_resolution = 1.0;
+    sv.irf_shared = *irf;
+    sv.gain = &gain;
+    sv.dead = &dead;
+    if ((st = rt3d_set_sensor(s, &sv))) return st;
+    uint64_t offs[2] = {0, n};
+    rt3d_cube cv;
+    std::memset(&cv, 0, sizeof cv);
+    cv.n_rows = cv.n_cols = 1;
+    cv.n_bins = n_bins;
+    cv.offsets = offs;
+    cv.events = events;
+    cv.n_events = n;
+    if ((st = rt3d_set_cube(s, &cv))) return st;
+    rt3d_recon_config c;
+    std::memset(&c, 0, sizeof c);
+    c.max_iters = 1;
+    c.knn_k = 1;
+    c.backtrack_beta = 0.5;
+    c.apss.kernel_radius = 1.0;
+    c.apss.min_neighbors = 6;
+    c.init.max_returns = k;
+    c.init.peak_threshold = threshold;
+    c.init.min_separation = min_sep;
+    Cfg g = cfg_from(&c, PROG_PEAKS);
+    if ((st = ensure_state(s, 1, 1))) return st;
+    Frame F;
+    if ((st = build_frame(s, F, g, 1))) return st;
+    if ((st = launch_frame(s, F, 0))) return st;
+    uint32_t npk = 0;
+    std::vector<double> t(k), rsp(k), mass(k);
+    CUDA_TRY(cudaMemcpyAsync(&npk, s->npk.p, 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(t.data(), s->pk_t.p, 8 * k, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(rsp.data(), s->pk_resp.p, 8 * k, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(mass.data(), s->pk_mass.p, 8 * k, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    for (uint32_t q = 0; q < npk; ++q) out[q] = rt3d_peak{t[q], rsp[q], mass[q]};
+    *n_out = (int32_t)npk;
+    s->have_state = false;
+    return RT3D_OK;
+}
+
+// ---- arbitrary-cloud operators --------------------------------------------
+static rt3d_status upload_cloud_soa(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
+                                    DevBuf& aos, CloudSoA& soa, DevBuf& soabuf) {
+    CUDA_TRY(aos.ensure(std::max<uint64_t>(n, 1) * sizeof(rt3d_point)));
+    if (n)
+        CUDA_TRY(cudaMemcpyAsync(aos.p, cloud, n * sizeof(rt3d_point), cudaMemcpyHostToDevice,
+                                 s->stream));
+    CUDA_TRY(soabuf.ensure(std::max<uint64_t>(n, 1) * 32));
+    double* base = soabuf.as<double>();
+    soa.x = base;
+    soa.y = base + n;
+    soa.z = base + 2 * n;
+    soa.r = base + 3 * n;
+    soa.n = (uint32_t)n;
+    if (n) {
+        split_cloud_kernel<<<(n + 255) / 256, 256, 0, s->stream>>>(
+            aos.as<rt3d_point>(), (uint32_t)n, (double*)soa.x, (double*)soa.y, (double*)soa.z,
+            (double*)soa.r);
+        CUDA_TRY(cudaGetLastError());
+    }
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_apss_project(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
+                              const rt3d_apss_params* prm, const rt3d_point* index_cloud,
+                              uint64_t n_index, double cell, rt3d_point* out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!prm) return fail(RT3D_ERR_INVALID_ARGUMENT, "null params");
+    if (prm->kernel_radius <= 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: kernel_radius must be positive");
+    if (prm->min_neighbors < 4)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: min_neighbors must be >= 4");
+    if (prm->sphere_degeneracy_eps < 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "ApssParams: sphere_degeneracy_eps must be >= 0");
+    if (cell <= 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "SpatialIndex: cell size must be positive");
+    if (n && prm->kernel_radius > cell * (1.0 + 1e-12))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "SpatialIndex: query radius exceeds cell size");
+    if (n >= (1ull << 32) || n_index >= (1ull << 32))
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
+    if (!n) return RT3D_OK;
+    CloudSoA idx, dummy;
+    DevBuf& aos_in = s->misc;
+    static thread_local DevBuf idx_aos, idx_soa, tmp_soa;
+    if ((st = upload_cloud_soa(s, index_cloud, n_index, idx_aos, idx, idx_soa))) return st;
+    if ((st = upload_cloud_soa(s, cloud, n, aos_in, dummy, tmp_soa))) return st;
+    CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point)));
+    apss_general_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(
+        aos_in.as<rt3d_point>(), (uint32_t)n, idx, prm->kernel_radius, prm->min_neighbors,
+        prm->sphere_degeneracy_eps, s->outpts.as<rt3d_point>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, s->outpts.p, n * sizeof(rt3d_point), cudaMemcpyDeviceToHost,
+                             s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_knn_intensity_filter(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
+                                      int32_t k, const rt3d_point* index_cloud, uint64_t n_index,
+                                      double cell, double radius, rt3d_point* out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (k < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "knn_intensity_filter: k must be >= 1");
+    if (radius <= 0.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "knn_intensity_filter: radius must be positive");
+    if (cell <= 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "SpatialIndex: cell size must be positive");
+    if (n && radius > cell * (1.0 + 1e-12))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "SpatialIndex: query radius exceeds cell size");
+    if (n >= (1ull << 32) || n_index >= (1ull << 32))
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
+    if (!n) return RT3D_OK;
+    CloudSoA idx, dummy;
+    static thread_local DevBuf idx_aos, idx_soa, tmp_soa;
+    if ((st = upload_cloud_soa(s, index_cloud, n_index, idx_aos, idx, idx_soa))) return st;
+    if ((st = upload_cloud_soa(s, cloud, n, s->misc, dummy, tmp_soa))) return st;
+    CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point)));
+    knn_general_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(
+        s->misc.as<rt3d_point>(), (uint32_t)n, idx, k, radius, s->outpts.as<rt3d_point>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, s->outpts.p, n * sizeof(rt3d_point), cudaMemcpyDeviceToHost,
+                             s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_prune(rt3d_session* s, const rt3d_point* cloud, uint64_t n, double r_min,
+                       rt3d_point* out, uint64_t* n_out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (r_min < 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "prune: r_min must be >= 0");
+    if (!n_out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null n_out");
+    *n_out = 0;
+    if (!n) return RT3D_OK;
+    if (n >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
+    const uint32_t blocks = (uint32_t)((n + kBlock - 1) / kBlock);
+    CUDA_TRY(s->misc.ensure(n * sizeof(rt3d_point)));
+    CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point) + 4 * blocks + 64));
+    CUDA_TRY(cudaMemcpyAsync(s->misc.p, cloud, n * sizeof(rt3d_point), cudaMemcpyHostToDevice, s->stream));
+    static thread_local DevBuf cnts;
+    CUDA_TRY(cnts.ensure(4 * blocks + 16));
+    uint32_t* total = cnts.as<uint32_t>() + blocks;
+    prune_count_kernel<<<blocks, kBlock, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, r_min,
+                                                         cnts.as<uint32_t>());
+    prune_scatter_kernel<<<blocks, kBlock, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, r_min,
+                                                           cnts.as<uint32_t>(),
+                                                           s->outpts.as<rt3d_point>(), total);
+    CUDA_TRY(cudaGetLastError());
+    uint32_t h_total = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h_total, total, 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (h_total)
+        CUDA_TRY(cudaMemcpy(out, s->outpts.p, (size_t)h_total * sizeof(rt3d_point), cudaMemcpyDeviceToHost));
+    *n_out = h_total;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t rows, int32_t cols,
+                                    double cutoff, int32_t clamp_nonneg, double* out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (cutoff <= 0.0 || cutoff > 1.0)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "fft_lowpass_filter: cutoff must be in (0, 1]");
+    if (rows < 2 || cols < 2)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "fft_lowpass_filter: image must be at least 2x2");
+    const size_t total = (size_t)rows * cols;
+    static thread_local DevBuf buf;
+    CUDA_TRY(buf.ensure(total * 8 * 6));
+    double* d = buf.as<double>();
+    CUDA_TRY(cudaMemcpyAsync(d, img, total * 8, cudaMemcpyHostToDevice, s->stream));
+    double *dimg = d, *dout = d + total, *re = d + 2 * total, *im = d + 3 * total,
+           *re2 = d + 4 * total, *im2 = d + 5 * total;
+    int nr = rows, nc = cols, cl = clamp_nonneg;
+    void* args[] = {&dimg, &dout, &re, &im, &re2, &im2, &nr, &nc, &cutoff, &cl};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fft_kernel, dim3(s->grid_fft), dim3(kBlock),
+                                         args, 0, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(out, dout, total * 8, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    return RT3D_OK;
+}
+
+}  // extern "C"

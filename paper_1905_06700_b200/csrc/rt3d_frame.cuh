@@ -1,0 +1,1144 @@
+// rt3d_frame.cuh — device phases of one RT3D frame and the persistent
+// cooperative kernel that runs them (init + PALM iterations) with grid-wide
+// barriers instead of host round trips.
+//
+// Data layout in HBM (all SoA, points in cloud order = pixel-major, so the
+// SceneState buckets of likelihood.hpp:38-55 are contiguous ranges bo[p] ..
+// bo[p+1] and bucket_points is the identity):
+//   cube      off[npix+1] u32, ev[E] {bin,count} u32x2          (read-only)
+//   points    t[2][P] f64, r[2][P] f64, pix/fi/fj[2][P] i32, fl[2][P] u8
+//   buckets   bo[2][npix+1] u32
+//   pixels    b[2][npix] f64, gb/cb[npix] f64
+// Double buffers hold (current, candidate) for the backtracking line search
+// and (in, out) for the Jacobi-style denoisers and the prune compaction.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rt3d_math.cuh"
+
+namespace rt3d {
+
+namespace cg = cooperative_groups;
+
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kLamCap = 16;        // per-lane rate slots kept in shared memory
+constexpr int kTopSmem = 4096;     // top-of-tree values reduced in shared memory
+constexpr int kMaxReturns = 16;    // InitParams::max_returns supported on device
+constexpr int kKnnFast = 32;       // knn_k handled with an in-register top-k list
+
+enum Program : int {
+    PROG_RECON = 0,   // reconstruct (reconstruct.hpp:457-489)
+    PROG_INIT = 1,    // init_matched_filter (reconstruct.hpp:197-249)
+    PROG_PALM = 2,    // one palm_step on the resident state (reconstruct.hpp:300-435)
+    PROG_NLL = 3,     // nll (likelihood.hpp:136-168)
+    PROG_GRADS = 4,   // grad_depth/intensity/background + block_curvatures
+    PROG_BASELINE = 5,// baseline_xcorr (eval.hpp:91-126)
+    PROG_PEAKS = 6,   // matched_filter_peaks on every pixel, no spawn
+};
+
+enum Kind : int {
+    K_NLL = 0,
+    K_CAND_T = 1,
+    K_CAND_R = 2,
+    K_CAND_B = 3,
+    K_GRAD_T = 4,
+    K_GRAD_R = 5,
+    K_GRAD_B = 6,
+};
+
+enum Op : int {
+    OP_RESULT = 0,
+    OP_GRAD_T_FIRST = 1,
+    OP_GRAD_T_END = 2,
+    OP_GRAD_R = 3,
+    OP_GRAD_B_PRUNED = 4,
+    OP_GRAD_B_EMPTY = 5,
+    OP_CAND_T = 6,
+    OP_CAND_R = 7,
+    OP_CAND_B = 8,
+};
+
+struct BlockDiagDev {
+    double step_used, nll_after_grad, nll_after_denoise;
+    int32_t backtracks, pad_;
+};
+struct StepDiagDev {  // layout of rt3d_step_diag
+    double nll_before, nll_after;
+    unsigned long long points_before, points_after;
+    BlockDiagDev blk[3];
+};
+
+struct Ctl {
+    unsigned int ticket;   // last-block election
+    unsigned int P;        // current point count
+    int iterations;
+    int stop;
+    int done, accept, bt, tc_end;
+    double nll_cur, prev, init_nll, result, alpha, cmax;
+    int rc_end, bc_end, sc_end, pad_;
+    unsigned long long t_start, t_init, t_end;  // %globaltimer stamps (ns)
+};
+
+struct Cfg {
+    int program;
+    int max_iters;
+    double stop_tol;
+    int step_auto[3];
+    double step[3];
+    double beta;
+    double R;          // apss kernel radius (= SpatialIndex cell)
+    double eps;        // sphere degeneracy eps
+    int min_nbrs;
+    int knn_k;
+    double r_min;
+    int bg_mode;
+    double cutoff;
+    int K, sep;
+    double thr;
+    int W;             // fine-pixel window half-width floor(R/pitch)+1
+    int set_oog_flags; // palm: OR out-of-gate into flags
+};
+
+struct Frame {
+    // sensor (sensor.hpp:131-170)
+    int rows, cols, bins, s;
+    int frows, fcols;
+    double pitch, bres, tlim;
+    const IrfDev* irfs;
+    const uint32_t* irf_of_pix;  // nullptr: irfs[0] for every pixel
+    const double* gain;
+    const uint8_t* dead;
+    // cube
+    uint32_t npix;
+    const uint32_t* off;
+    const uint2* ev;
+    // pairwise tree geometry over pixels
+    int G, Gb, wpb;
+    uint32_t nbn;
+    // state
+    double* t[2];
+    double* r[2];
+    double* b[2];
+    uint32_t* pix[2];
+    int32_t* fi[2];
+    int32_t* fj[2];
+    uint8_t* fl[2];
+    uint32_t* bo[2];
+    int tc0, rc0, bc0, sc0;  // initial buffer toggles
+    // scratch
+    double* gt;
+    double* ct;
+    double* gr;
+    double* cr;
+    double* gb;
+    double* cb;
+    uint8_t* oog;
+    double* lam;      // E rate slots for pixels above kLamCap events
+    double* blk;      // nbn block-node sums
+    double* bmax;     // gridDim block maxima
+    uint32_t* cnt;    // npix prefix scratch
+    uint32_t* btot;   // gridDim block totals
+    double* pk_t;
+    double* pk_resp;
+    double* pk_mass;
+    double* pk_int;   // intensity, < 0 marks a peak with no in-gate IRF mass
+    uint32_t* npk;
+    uint32_t* nval;
+    double* fft_re;   // 2*npix complex scratch (fft background mode)
+    double* fft_im;
+    // control / report
+    Ctl* ctl;
+    StepDiagDev* diag;
+    double* trace;
+    Cfg cfg;
+};
+
+struct Smem {
+    double lam[kWarps][kLamCap][32];  // reused as the top-of-tree array
+    double vals[kWarps][32];
+    double node[kWarps];
+    double wmax[kWarps];
+    unsigned int scan[kWarps + 1];
+    int is_last;
+    IrfDev irf0;
+};
+static_assert(sizeof(double) * kWarps * kLamCap * 32 >= sizeof(double) * kTopSmem,
+              "top-of-tree array must fit in the rate slots");
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_cg(const T* p) {
+    return __ldcg(p);
+}
+
+__device__ __forceinline__ const IrfDev& pixel_irf(const Frame& F, const Smem& sm, uint32_t p) {
+    return F.irf_of_pix ? F.irfs[F.irf_of_pix[p]] : sm.irf0;
+}
+
+__device__ __forceinline__ uint32_t lower_bound_bin(const uint2* ev, uint32_t lo, uint32_t hi,
+                                                    uint32_t key) {
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (__ldg(&ev[mid].x) < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// ---------------------------------------------------------------------------
+// block-wide exclusive scan of one u32 per thread
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned int block_exclusive_scan(unsigned int v, Smem& sm,
+                                                             unsigned int& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm.scan[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int acc = 0;
+        for (int w = 0; w < kWarps; ++w) {
+            unsigned int t = sm.scan[w];
+            sm.scan[w] = acc;
+            acc += t;
+        }
+        sm.scan[kWarps] = acc;
+    }
+    __syncthreads();
+    unsigned int ex = sm.scan[warp] + x - v;
+    total = sm.scan[kWarps];
+    __syncthreads();
+    return ex;
+}
+
+// ---------------------------------------------------------------------------
+// Matched filter (reconstruct.hpp:120-189), warp per pixel
+// ---------------------------------------------------------------------------
+// the `response` lambda, reconstruct.hpp:129-138
+__device__ __forceinline__ double mf_response(const uint2* ev, uint32_t e0, uint32_t m,
+                                              const IrfDev& f, double t0) {
+    uint32_t first = (uint32_t)std_max(0.0, ceil(t0 + f.tau_min));
+    uint32_t k = lower_bound_bin(ev, e0, e0 + m, first);
+    double c = 0.0;
+    const double top = t0 + f.tau_max;
+    for (; k < e0 + m; ++k) {
+        uint2 e = __ldg(&ev[k]);
+        if (!((double)e.x <= top)) break;
+        c += (double)e.y * irf_value(f, (double)e.x - t0);
+    }
+    return c / f.h_max;
+}
+
+__device__ void phase_init_peaks(const Frame& F, Smem& sm) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t nwarps = gridDim.x * kWarps;
+    const int K = F.cfg.K, sep = F.cfg.sep, T = F.bins;
+    const double thr = F.cfg.thr;
+    for (uint32_t p = blockIdx.x * kWarps + (threadIdx.x >> 5); p < F.npix; p += nwarps) {
+        const double g = F.dead[p] ? 0.0 : F.gain[p];
+        const uint32_t e0 = F.off[p], e1 = F.off[p + 1], m = e1 - e0;
+        if (g == 0.0 || m == 0) {
+            if (lane == 0) {
+                F.npk[p] = 0;
+                F.nval[p] = 0;
+                F.b[0][p] = kBackgroundFloor;
+            }
+            continue;
+        }
+        const IrfDev& f = pixel_irf(F, sm, p);
+        int taken[kMaxReturns];
+        double tresp[kMaxReturns];
+        int nt = 0;
+        for (int round = 0; round < K; ++round) {
+            double best_r = -INFINITY;
+            int best_l = 0x7fffffff;
+            for (uint32_t e = lane; e < m; e += 32) {
+                const uint32_t bin = __ldg(&F.ev[e0 + e].x);
+                int lo = (int)ceil((double)bin - f.tau_max);
+                lo = lo < 0 ? 0 : lo;
+                int hi = (int)floor((double)bin - f.tau_min);
+                hi = hi > T - 1 ? T - 1 : hi;
+                if (e > 0) {
+                    const uint32_t pb = __ldg(&F.ev[e0 + e - 1].x);
+                    int phi = (int)floor((double)pb - f.tau_min);
+                    phi = phi > T - 1 ? T - 1 : phi;
+                    if (phi + 1 > lo) lo = phi + 1;
+                }
+                for (int t0 = lo; t0 <= hi; ++t0) {
+                    bool clash = false;
+                    for (int q = 0; q < nt; ++q) {
+                        int dd = taken[q] - t0;
+                        if ((dd < 0 ? -dd : dd) < sep) clash = true;
+                    }
+                    if (clash) continue;
+                    double rr = mf_response(F.ev, e0, m, f, (double)t0);
+                    if (rr >= thr && (rr > best_r || (rr == best_r && t0 < best_l))) {
+                        best_r = rr;
+                        best_l = t0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                double orr = __shfl_xor_sync(0xffffffffu, best_r, o);
+                int ol = __shfl_xor_sync(0xffffffffu, best_l, o);
+                if (orr > best_r || (orr == best_r && ol < best_l)) {
+                    best_r = orr;
+                    best_l = ol;
+                }
+            }
+            if (best_r == -INFINITY) break;
+            taken[nt] = best_l;
+            tresp[nt] = best_r;
+            ++nt;
+        }
+        if (lane == 0) {
+            double pt[kMaxReturns], pm[kMaxReturns], pr[kMaxReturns];
+            for (int q = 0; q < nt; ++q) {
+                const int t0 = taken[q];
+                const double c0 = tresp[q];
+                double cm = t0 > 0 ? mf_response(F.ev, e0, m, f, (double)(t0 - 1)) : 0.0;
+                double cp = t0 < T - 1 ? mf_response(F.ev, e0, m, f, (double)(t0 + 1)) : 0.0;
+                double denom = cm - 2.0 * c0 + cp;
+                double delta = fabs(denom) > 1e-12 ? 0.5 * (cm - cp) / denom : 0.0;
+                double tt = t0 + std_clamp(delta, -0.5, 0.5);
+                int wlo, whi;
+                irf_support(f, tt, T, wlo, whi);
+                double mass = 0.0;
+                for (uint32_t k = e0; k < e1; ++k) {
+                    uint2 e = __ldg(&F.ev[k]);
+                    if (e.x >= (uint32_t)wlo && e.x <= (uint32_t)whi) mass += (double)e.y;
+                }
+                // stable insertion by t (std::sort on <= 16 elements)
+                int pos = q;
+                while (pos > 0 && tt < pt[pos - 1]) {
+                    pt[pos] = pt[pos - 1];
+                    pm[pos] = pm[pos - 1];
+                    pr[pos] = pr[pos - 1];
+                    --pos;
+                }
+                pt[pos] = tt;
+                pm[pos] = mass;
+                pr[pos] = c0;
+            }
+            double claimed = 0.0;
+            uint32_t nv = 0;
+            for (int q = 0; q < nt; ++q) {
+                const double irf_mass = irf_mass_in_gate(f, pt[q], T);
+                double inten = -1.0;
+                if (irf_mass > 0.0) {
+                    inten = pm[q] / (g * irf_mass);
+                    claimed += pm[q];
+                    ++nv;
+                }
+                const size_t slot = (size_t)p * K + q;
+                F.pk_t[slot] = pt[q];
+                F.pk_resp[slot] = pr[q];
+                F.pk_mass[slot] = pm[q];
+                F.pk_int[slot] = inten;
+            }
+            double total = 0.0;
+            for (uint32_t k = e0; k < e1; ++k) total += (double)__ldg(&F.ev[k].y);
+            double residual = std_max(0.0, total - std_min(claimed, total));
+            F.b[0][p] = std_max(kBackgroundFloor, residual / (g * T));
+            F.npk[p] = (uint32_t)nt;
+            F.nval[p] = nv;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// chunked grid scan: stage A writes per-pixel block-local prefixes, stage B
+// adds the block base (after a grid barrier)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void chunk_range(uint32_t n, uint32_t& c0, uint32_t& c1) {
+    uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    c0 = blockIdx.x * chunk;
+    c1 = c0 + chunk;
+    if (c0 > n) c0 = n;
+    if (c1 > n) c1 = n;
+}
+
+template <typename CountFn>
+__device__ void scan_stage_a(const Frame& F, Smem& sm, CountFn count) {
+    uint32_t c0, c1;
+    chunk_range(F.npix, c0, c1);
+    unsigned int carry = 0;
+    for (uint32_t base = c0; base < c1; base += kBlock) {
+        uint32_t p = base + threadIdx.x;
+        unsigned int v = p < c1 ? count(p) : 0u, tot;
+        unsigned int ex = block_exclusive_scan(v, sm, tot);
+        if (p < c1) F.cnt[p] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) F.btot[blockIdx.x] = carry;
+}
+
+// returns this block's base; thread 0 of the last block publishes the total
+__device__ unsigned int scan_stage_b_base(const Frame& F, Smem& sm, unsigned int* total_out) {
+    unsigned int part = 0;
+    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kBlock) part += ld_cg(&F.btot[b]);
+    unsigned int tot;
+    unsigned int ex = block_exclusive_scan(part, sm, tot);
+    (void)ex;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
+        *total_out = tot + ld_cg(&F.btot[blockIdx.x]);
+    return tot;
+}
+
+// spawn points of init_matched_filter (reconstruct.hpp:219-237, 245-247)
+__device__ void phase_spawn(const Frame& F, Smem& sm, bool baseline) {
+    unsigned int total = 0;
+    unsigned int base = scan_stage_b_base(F, sm, &total);
+    uint32_t c0, c1;
+    chunk_range(F.npix, c0, c1);
+    const int s = F.s, K = F.cfg.K;
+    for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
+        uint32_t o = base + ld_cg(&F.cnt[p]);
+        F.bo[0][p] = o;
+        const int i = (int)(p / F.cols), j = (int)(p % F.cols);
+        const uint32_t nt = F.npk[p];
+        for (uint32_t q = 0; q < nt; ++q) {
+            const size_t slot = (size_t)p * K + q;
+            const double inten = F.pk_int[slot];
+            if (!(inten >= 0.0)) continue;
+            if (baseline) {
+                // eval.hpp:107-120: one point, first peak, coarse-centre cell
+                F.t[0][o] = F.pk_t[slot];
+                F.r[0][o] = inten;
+                F.pix[0][o] = p;
+                F.fi[0][o] = i * s + s / 2;
+                F.fj[0][o] = j * s + s / 2;
+                F.fl[0][o] = 0;
+                ++o;
+                break;
+            }
+            const double rr = inten / (double)(s * s);
+            for (int a = 0; a < s; ++a)
+                for (int c = 0; c < s; ++c) {
+                    F.t[0][o] = F.pk_t[slot];
+                    F.r[0][o] = rr;
+                    F.pix[0][o] = p;
+                    F.fi[0][o] = i * s + a;
+                    F.fj[0][o] = j * s + c;
+                    F.fl[0][o] = 0;
+                    ++o;
+                }
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        F.bo[0][F.npix] = total;
+        F.ctl->P = total;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Likelihood sweep of one pixel (likelihood.hpp:100-333, reconstruct.hpp:
+// 312-347,382-389,415-421).  Returns the pixel's nll partial.
+// ---------------------------------------------------------------------------
+struct SweepCtx {
+    double alpha;
+    double cfloor;   // 1e-3 * max(curv) + 1e-30 (reconstruct.hpp:315)
+    int tc, rc, bc, sc;
+    int apply_floor; // background floor of reconstruct.hpp:427 before the sweep
+};
+
+template <int KIND>
+__device__ __forceinline__ double sweep_pixel(const Frame& F, const Smem& sm, const SweepCtx& X,
+                                              uint32_t p, double* lam_s, double& cmax) {
+    const uint32_t e0 = F.off[p], e1 = F.off[p + 1], m = e1 - e0;
+    const uint32_t* bo = F.bo[X.sc];
+    const uint32_t n0 = bo[p], n1 = bo[p + 1];
+    const bool dead = F.dead[p] != 0;
+    const double gain = F.gain[p];
+    const double g = dead ? 0.0 : gain;
+    const IrfDev& f = pixel_irf(F, sm, p);
+    const int T = F.bins;
+
+    // background value (current, candidate, or floored current)
+    double b;
+    if (KIND == K_CAND_B) {
+        double dir = F.gb[p];
+        if (F.cfg.step_auto[2]) dir = dir / (F.cb[p] + X.cfloor);
+        b = std_max(0.0, F.b[X.bc][p] - X.alpha * dir);
+        F.b[X.bc ^ 1][p] = b;
+    } else {
+        b = F.b[X.bc][p];
+        if (X.apply_floor) {
+            b = (b < kBackgroundFloor) ? kBackgroundFloor : b;
+            F.b[X.bc][p] = b;
+        }
+    }
+
+    // candidate point values
+    const double* tsrc = F.t[X.tc];
+    const double* rsrc = F.r[X.rc];
+    if (KIND == K_CAND_T) {
+        double* to = F.t[X.tc ^ 1];
+        for (uint32_t n = n0; n < n1; ++n) {
+            double dir = F.gt[n];
+            if (F.cfg.step_auto[0]) dir = dir / (F.ct[n] + X.cfloor);
+            to[n] = std_clamp(tsrc[n] - X.alpha * dir, 0.0, F.tlim);
+        }
+        tsrc = to;
+    }
+    if (KIND == K_CAND_R) {
+        double* ro = F.r[X.rc ^ 1];
+        for (uint32_t n = n0; n < n1; ++n) {
+            double dir = F.gr[n];
+            if (F.cfg.step_auto[1]) dir = dir / (F.cr[n] + X.cfloor);
+            ro[n] = std_max(0.0, rsrc[n] - X.alpha * dir);
+        }
+        rsrc = ro;
+    }
+
+    // rates at the active bins (detail::active_rates, likelihood.hpp:100-121)
+    const bool in_smem = m <= (uint32_t)kLamCap;
+    double* lam = in_smem ? lam_s : (F.lam + e0);
+    const uint32_t ls = in_smem ? 32u : 1u;
+    {
+        const double l0 = (g == 0.0) ? 0.0 : g * b;
+        for (uint32_t k = 0; k < m; ++k) lam[k * ls] = l0;
+        if (g != 0.0) {
+            for (uint32_t n = n0; n < n1; ++n) {
+                const double t = tsrc[n], gr_ = g * rsrc[n];
+                int lo, hi;
+                irf_support(f, t, T, lo, hi);
+                if (lo > hi) continue;
+                for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
+                    const uint32_t bin = __ldg(&F.ev[e0 + k].x);
+                    if (bin > (uint32_t)hi) break;
+                    lam[k * ls] += gr_ * irf_value(f, (double)bin - t);
+                }
+            }
+        }
+    }
+
+    double part = 0.0;
+    if (!dead) {  // nll, likelihood.hpp:141-165
+        double mass = T * b;
+        for (uint32_t n = n0; n < n1; ++n) mass += rsrc[n] * irf_mass_in_gate(f, tsrc[n], T);
+        double acc = gain * mass;
+        for (uint32_t k = 0; k < m; ++k) {
+            const double l = lam[k * ls];
+            if (l <= 0.0) {
+                acc = INFINITY;
+                break;
+            }
+            acc -= (double)__ldg(&F.ev[e0 + k].y) * log(l);
+        }
+        part = acc;
+    }
+
+    if (KIND == K_GRAD_T) {  // grad_depth + block_curvatures().depth
+        const bool skip = (n0 == n1) || g == 0.0;
+        for (uint32_t n = n0; n < n1; ++n) {
+            double gval = 0.0, st = 0.0;
+            uint8_t og = 0;
+            if (!skip) {
+                const double t = tsrc[n], r = rsrc[n];
+                int lo, hi;
+                irf_support(f, t, T, lo, hi);
+                if (lo > hi) {
+                    og = 1;
+                } else {
+                    const double grr = g * r;
+                    double acc = 0.0;
+                    for (int bb = lo; bb <= hi; ++bb) acc -= irf_deriv(f, (double)bb - t);
+                    for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
+                        const uint2 e = __ldg(&F.ev[e0 + k]);
+                        if (e.x > (uint32_t)hi) break;
+                        const double l = lam[k * ls];
+                        const double dv = irf_deriv(f, (double)e.x - t);
+                        if (l > 0.0) acc += dv * (double)e.y / l;
+                        if (!(l <= 0.0)) {  // likelihood.hpp:320
+                            const double zl2 = (double)e.y / (l * l);
+                            const double dh = grr * dv;
+                            st += dh * dh * zl2;
+                        }
+                    }
+                    if (r != 0.0) gval = grr * acc;
+                }
+            }
+            F.gt[n] = gval;
+            F.ct[n] = st;
+            F.oog[n] = og;
+            if (og && F.cfg.set_oog_flags) F.fl[X.sc][n] |= 2u;
+            cmax = std_max(cmax, st);
+        }
+    }
+    if (KIND == K_GRAD_R) {  // grad_intensity + block_curvatures().intensity
+        const bool skip = (n0 == n1) || g == 0.0;
+        for (uint32_t n = n0; n < n1; ++n) {
+            double gval = 0.0, sr = 0.0;
+            if (!skip) {
+                const double t = tsrc[n];
+                double acc = irf_mass_in_gate(f, t, T);
+                int lo, hi;
+                irf_support(f, t, T, lo, hi);
+                if (lo <= hi) {
+                    for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
+                        const uint2 e = __ldg(&F.ev[e0 + k]);
+                        if (e.x > (uint32_t)hi) break;
+                        const double l = lam[k * ls];
+                        const double hv = irf_value(f, (double)e.x - t);
+                        if (l > 0.0) acc -= hv * (double)e.y / l;
+                        if (!(l <= 0.0)) {  // likelihood.hpp:320
+                            const double zl2 = (double)e.y / (l * l);
+                            const double h = g * hv;
+                            sr += h * h * zl2;
+                        }
+                    }
+                }
+                gval = g * acc;
+            }
+            F.gr[n] = gval;
+            F.cr[n] = sr;
+            cmax = std_max(cmax, sr);
+        }
+    }
+    if (KIND == K_GRAD_B) {  // grad_background + block_curvatures().background
+        double gval = 0.0, bs = 0.0;
+        if (g != 0.0) {
+            double acc = g * T;
+            for (uint32_t k = 0; k < m; ++k) {
+                const double l = lam[k * ls];
+                if (l > 0.0) {
+                    const double z = (double)__ldg(&F.ev[e0 + k].y);
+                    acc -= g * z / l;
+                    bs += g * g * z / (l * l);
+                }
+            }
+            gval = acc;
+        }
+        F.gb[p] = gval;
+        F.cb[p] = bs;
+        cmax = std_max(cmax, bs);
+    }
+    return part;
+}
+
+// ---------------------------------------------------------------------------
+// Controller: runs on thread 0 of the last block after each grid reduction
+// ---------------------------------------------------------------------------
+__device__ void set_block(const Frame& F, int blk, double cmax, int it) {
+    Ctl* c = F.ctl;
+    c->cmax = cmax;
+    c->alpha = F.cfg.step_auto[blk] ? 1.0 : F.cfg.step[blk];
+    c->bt = 0;
+    c->accept = 0;
+    c->done = 0;
+    if (c->alpha <= 0.0) {  // safeguarded_step's empty-step exit (reconstruct.hpp:278-281)
+        c->alpha = 0.0;
+        c->done = 1;
+        if (it >= 0) {
+            BlockDiagDev& d = F.diag[it].blk[blk];
+            d.step_used = 0.0;
+            d.backtracks = 0;
+            d.nll_after_grad = c->nll_cur;
+        }
+    }
+}
+
+__device__ void controller(const Frame& F, int op, int it, double v, double cmax) {
+    Ctl* c = F.ctl;
+    switch (op) {
+        case OP_RESULT:
+            c->result = v;
+            c->cmax = cmax;
+            break;
+        case OP_GRAD_T_FIRST:
+            c->nll_cur = v;
+            c->init_nll = v;
+            c->prev = v;
+            F.trace[0] = v;
+            set_block(F, 0, cmax, 0);
+            break;
+        case OP_GRAD_T_END: {
+            StepDiagDev& d = F.diag[it];
+            d.blk[2].nll_after_denoise = v;
+            d.nll_after = v;
+            d.points_after = c->P;
+            F.trace[it + 1] = v;
+            c->iterations = it + 1;
+            // stop rule, reconstruct.hpp:475-477
+            double rel = fabs(c->prev - v) / std_max(1.0, fabs(c->prev));
+            c->prev = v;
+            c->stop = rel < F.cfg.stop_tol;
+            c->nll_cur = v;
+            set_block(F, 0, cmax, it + 1 < F.cfg.max_iters ? it + 1 : -1);
+            break;
+        }
+        case OP_GRAD_R:
+            F.diag[it].blk[0].nll_after_denoise = v;
+            c->nll_cur = v;
+            set_block(F, 1, cmax, it);
+            break;
+        case OP_GRAD_B_PRUNED:
+            F.diag[it].blk[1].nll_after_denoise = v;
+            c->nll_cur = v;
+            set_block(F, 2, cmax, it);
+            break;
+        case OP_GRAD_B_EMPTY:
+            set_block(F, 2, cmax, it);
+            break;
+        case OP_CAND_T:
+        case OP_CAND_R:
+        case OP_CAND_B: {
+            const int blk = op - OP_CAND_T;
+            // safeguarded_step, reconstruct.hpp:282-291
+            if (v <= c->nll_cur) {
+                c->nll_cur = v;
+                c->accept = 1;
+                c->done = 1;
+            } else {
+                c->alpha *= F.cfg.beta;
+                c->bt += 1;
+                if (c->bt >= kMaxBacktracks) {
+                    c->alpha = 0.0;
+                    c->accept = 0;
+                    c->done = 1;
+                }
+            }
+            if (c->done) {
+                BlockDiagDev& d = F.diag[it].blk[blk];
+                d.step_used = c->alpha;
+                d.backtracks = c->bt;
+                d.nll_after_grad = c->nll_cur;
+            }
+            break;
+        }
+    }
+}
+
+// pairwise tree over the nbn block-node sums, in the last block
+__device__ double top_tree(const Frame& F, Smem& sm) {
+    const uint32_t nb = F.nbn;
+    double* v = &sm.lam[0][0][0];
+    if (nb <= (uint32_t)kTopSmem) {
+        for (uint32_t q = threadIdx.x; q < nb; q += kBlock) v[q] = ld_cg(&F.blk[q]);
+        __syncthreads();
+        for (uint32_t w = nb; w > 1; w >>= 1) {
+            for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock) v[q] = v[2 * q] + v[2 * q + 1];
+            __syncthreads();
+        }
+        double r = v[0];
+        __syncthreads();
+        return r;
+    }
+    for (uint32_t w = nb; w > 1; w >>= 1) {
+        for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock)
+            F.blk[q] = ld_cg(&F.blk[2 * q]) + ld_cg(&F.blk[2 * q + 1]);
+        __threadfence_block();
+        __syncthreads();
+    }
+    double r = ld_cg(&F.blk[0]);
+    __syncthreads();
+    return r;
+}
+
+// One likelihood sweep over all pixels in pairwise_sum's tree order
+// (parallel.hpp:52-61): warp = depth-G node (<= 32 pixels, one per lane),
+// block = depth-Gb node; the last block to finish reduces the top of the tree
+// and runs the controller.  Caller issues the grid barrier afterwards.
+template <int KIND>
+__device__ void tree_sweep(const Frame& F, Smem& sm, const SweepCtx& X, int op, int it) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double cmax = 0.0;
+    double* lam_s = &sm.lam[warp][0][lane];
+    for (uint32_t bn = blockIdx.x; bn < F.nbn; bn += gridDim.x) {
+        if (warp < F.wpb) {
+            uint32_t lo, size;
+            tree_node_range(F.npix, F.G, bn * (uint32_t)F.wpb + warp, lo, size);
+            double part = 0.0;
+            if ((uint32_t)lane < size) part = sweep_pixel<KIND>(F, sm, X, lo + lane, lam_s, cmax);
+            sm.vals[warp][lane] = part;
+            __syncwarp();
+            if (lane == 0) sm.node[warp] = pw32(sm.vals[warp], 0, (int)size);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double v[kWarps];
+            for (int w = 0; w < F.wpb; ++w) v[w] = sm.node[w];
+            for (int w = F.wpb; w > 1; w >>= 1)
+                for (int q = 0; q < w / 2; ++q) v[q] = v[2 * q] + v[2 * q + 1];
+            F.blk[bn] = v[0];
+        }
+        __syncthreads();
+    }
+    // block max of the curvature (order-free)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmax = std_max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    if (lane == 0) sm.wmax[warp] = cmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bm = 0.0;
+        for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
+        F.bmax[blockIdx.x] = bm;
+        __threadfence();
+        unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
+        sm.is_last = (tk == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!sm.is_last) return;
+    __threadfence();
+    double total = top_tree(F, sm);
+    if (threadIdx.x == 0) {
+        double gm = 0.0;
+        for (uint32_t b = 0; b < gridDim.x; ++b) gm = std_max(gm, ld_cg(&F.bmax[b]));
+        F.ctl->ticket = 0;
+        controller(F, op, it, total, gm);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Neighbourhoods on the pinned fine grid.  Inside PALM every point sits at
+// its fine-pixel centre (reconstruct.hpp:233,357-361), so the SpatialIndex
+// ball (spatial_index.hpp:31-47: exact |q-p|^2 <= R^2, ascending index) is
+// the set of points of the coarse pixels covering the fine window
+// [fi-W, fi+W] x [fj-W, fj+W], W = floor(R/pitch)+1, visited in raster
+// order (= ascending index, the cloud being pixel-major).
+// ---------------------------------------------------------------------------
+struct Pos {
+    double x, y, z;
+};
+
+template <typename Fn>
+__device__ __forceinline__ void for_each_pinned_neighbor(const Frame& F, int tc, int sc, int fi,
+                                                         int fj, const Pos& q, double r2, Fn fn) {
+    const int W = F.cfg.W, s = F.s;
+    int a0 = fi - W, a1 = fi + W, b0 = fj - W, b1 = fj + W;
+    a0 = a0 < 0 ? 0 : a0;
+    b0 = b0 < 0 ? 0 : b0;
+    a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
+    b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
+    const int ci0 = a0 / s, ci1 = a1 / s, cj0 = b0 / s, cj1 = b1 / s;
+    const uint32_t* bo = F.bo[sc];
+    const double* tt = F.t[tc];
+    const int32_t* FI = F.fi[sc];
+    const int32_t* FJ = F.fj[sc];
+    for (int ci = ci0; ci <= ci1; ++ci) {
+        const uint32_t prow = (uint32_t)ci * F.cols;
+        const uint32_t m0 = bo[prow + cj0], m1 = bo[prow + cj1 + 1];
+        for (uint32_t mm = m0; mm < m1; ++mm) {
+            Pos o;
+            o.x = (FI[mm] + 0.5) * F.pitch;
+            o.y = (FJ[mm] + 0.5) * F.pitch;
+            o.z = tt[mm] * F.bres;
+            const double dx = o.x - q.x, dy = o.y - q.y, dz = o.z - q.z;
+            const double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 <= r2) fn(mm, o, d2);
+        }
+    }
+}
+
+// apss_project for one point (denoise.hpp:163-214), neighbour enumerator
+// supplied by the caller.  Returns the new position in `out` when the fit
+// projected it; updates flags.
+template <typename Enum>
+__device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, int min_nbrs,
+                                           double eps, uint8_t& flags, Pos& out) {
+    const double r2 = R * R;
+    unsigned int cnt = 0;
+    double wsum = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+    each(r2, [&](uint32_t, const Pos& o, double d2) {
+        ++cnt;
+        double w = apss_weight(R, sqrt(d2));
+        wsum += w;
+        m0 += w * o.x;
+        m1 += w * o.y;
+        m2 += w * o.z;
+    });
+    if (cnt < (unsigned int)min_nbrs) {
+        flags |= 1u;
+        return false;
+    }
+    if (wsum <= 0.0) {
+        flags |= 4u;
+        return false;
+    }
+    m0 /= wsum;
+    m1 /= wsum;
+    m2 /= wsum;
+    double c00 = 0, c10 = 0, c11 = 0, c20 = 0, c21 = 0, c22 = 0;
+    each(r2, [&](uint32_t, const Pos& o, double d2) {
+        double w = apss_weight(R, sqrt(d2));
+        double d0 = o.x - m0, d1 = o.y - m1, dd2 = o.z - m2;
+        double w0 = w * d0, w1 = w * d1, w2 = w * dd2;
+        c00 += w0 * d0;
+        c10 += w1 * d0;
+        c11 += w1 * d1;
+        c20 += w2 * d0;
+        c21 += w2 * d1;
+        c22 += w2 * dd2;
+    });
+    c00 /= wsum;
+    c10 /= wsum;
+    c11 /= wsum;
+    c20 /= wsum;
+    c21 /= wsum;
+    c22 /= wsum;
+    double e0, e1, e2;
+    sym3_eigenvalues(c00, c10, c11, c20, c21, c22, e0, e1, e2);
+    if (e2 <= 0.0 || e1 <= 1e-12 * e2) {
+        flags |= 4u;
+        return false;
+    }
+    double M[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) M[k] = 0.0;
+    each(r2, [&](uint32_t, const Pos& o, double d2) {
+        double w = apss_weight(R, sqrt(d2));
+        if (w <= 0.0) return;
+        double y0 = o.x - m0, y1 = o.y - m1, y2 = o.z - m2;
+        double dv[5] = {1.0, y0, y1, y2, y0 * y0 + y1 * y1 + y2 * y2};
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+            double wa = w * dv[a];
+#pragma unroll
+            for (int c = 0; c <= a; ++c) M[lt(a, c)] += wa * dv[c];
+        }
+    });
+    Sphere sp;
+    if (!sphere_from_moments(M, m0, m1, m2, sp) ||
+        !project_sphere(sp, eps, q.x, q.y, q.z, out.x, out.y, out.z)) {
+        flags |= 4u;
+        return false;
+    }
+    return true;
+}
+
+// APSS + pinning, reconstruct.hpp:355-363: t' = clamp(z'/bin_res)
+__device__ void phase_apss(const Frame& F, int tc, int sc, uint32_t P) {
+    const uint32_t nth = gridDim.x * kBlock;
+    for (uint32_t n = blockIdx.x * kBlock + threadIdx.x; n < P; n += nth) {
+        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
+        const double t = F.t[tc][n];
+        Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, t * F.bres};
+        uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
+        Pos o;
+        auto each = [&](double r2, auto fn) { for_each_pinned_neighbor(F, tc, sc, fi, fj, q, r2, fn); };
+        bool moved = apss_point(each, q, F.cfg.R, F.cfg.min_nbrs, F.cfg.eps, fl, o);
+        const double z = moved ? o.z : q.z;
+        F.t[tc ^ 1][n] = std_clamp(z / F.bres, 0.0, F.tlim);
+        F.fl[sc][n] = fl;
+    }
+}
+
+// top-k by (d^2, index), spatial_index.hpp:51-62, then the mean
+// (denoise.hpp:228-235)
+template <typename Enum, typename RFn>
+__device__ __forceinline__ double knn_mean(Enum&& each, int k, double r2, double self_r, RFn rof) {
+    if (k <= kKnnFast) {
+        double kd[kKnnFast];
+        uint32_t ki[kKnnFast];
+        int cnt = 0;
+        each(r2, [&](uint32_t mm, const Pos&, double d2) {
+            if (cnt == k && !(d2 < kd[cnt - 1] || (d2 == kd[cnt - 1] && mm < ki[cnt - 1]))) return;
+            int pos = cnt < k ? cnt : k - 1;
+            while (pos > 0 && (d2 < kd[pos - 1] || (d2 == kd[pos - 1] && mm < ki[pos - 1]))) {
+                kd[pos] = kd[pos - 1];
+                ki[pos] = ki[pos - 1];
+                --pos;
+            }
+            kd[pos] = d2;
+            ki[pos] = mm;
+            if (cnt < k) ++cnt;
+        });
+        if (cnt == 0) return self_r;
+        double acc = 0.0;
+        for (int q = 0; q < cnt; ++q) acc += rof(ki[q]);
+        return acc / (double)cnt;
+    }
+    // large k: successive minimum selection
+    double last_d = -1.0;
+    uint32_t last_i = 0;
+    bool have_last = false;
+    double acc = 0.0;
+    int cnt = 0;
+    for (; cnt < k; ++cnt) {
+        double bd = INFINITY;
+        uint32_t bi = 0xffffffffu;
+        bool found = false;
+        each(r2, [&](uint32_t mm, const Pos&, double d2) {
+            if (have_last && !(d2 > last_d || (d2 == last_d && mm > last_i))) return;
+            if (!found || d2 < bd || (d2 == bd && mm < bi)) {
+                bd = d2;
+                bi = mm;
+                found = true;
+            }
+        });
+        if (!found) break;
+        acc += rof(bi);
+        last_d = bd;
+        last_i = bi;
+        have_last = true;
+    }
+    if (cnt == 0) return self_r;
+    return acc / (double)cnt;
+}
+
+__device__ void phase_knn(const Frame& F, int tc, int rc, int sc, uint32_t P) {
+    const uint32_t nth = gridDim.x * kBlock;
+    const double R = F.cfg.R, r2 = R * R;
+    const double* rr = F.r[rc];
+    for (uint32_t n = blockIdx.x * kBlock + threadIdx.x; n < P; n += nth) {
+        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
+        Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
+        auto each = [&](double rr2, auto fn) { for_each_pinned_neighbor(F, tc, sc, fi, fj, q, rr2, fn); };
+        F.r[rc ^ 1][n] = knn_mean(each, F.cfg.knn_k, r2, rr[n], [&](uint32_t mm) { return rr[mm]; });
+    }
+}
+
+// prune (denoise.hpp:241-248) + SceneState::refresh (likelihood.hpp:38-55):
+// per-pixel survivor counts, grid scan, stable scatter into the other buffers
+__device__ void phase_prune_a(const Frame& F, Smem& sm, int rc, int sc) {
+    const uint32_t* bo = F.bo[sc];
+    const double* r = F.r[rc];
+    const double rmin = F.cfg.r_min;
+    scan_stage_a(F, sm, [&](uint32_t p) {
+        unsigned int c = 0;
+        for (uint32_t n = bo[p]; n < bo[p + 1]; ++n) c += (r[n] >= rmin) ? 1u : 0u;
+        return c;
+    });
+}
+
+__device__ void phase_prune_b(const Frame& F, Smem& sm, int tc, int rc, int sc) {
+    unsigned int total = 0;
+    unsigned int base = scan_stage_b_base(F, sm, &total);
+    uint32_t c0, c1;
+    chunk_range(F.npix, c0, c1);
+    const uint32_t* bo = F.bo[sc];
+    const double rmin = F.cfg.r_min;
+    for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
+        uint32_t o = base + ld_cg(&F.cnt[p]);
+        F.bo[sc ^ 1][p] = o;
+        for (uint32_t n = bo[p]; n < bo[p + 1]; ++n) {
+            const double rv = F.r[rc][n];
+            if (!(rv >= rmin)) continue;
+            F.t[tc ^ 1][o] = F.t[tc][n];
+            F.r[rc ^ 1][o] = rv;
+            F.pix[sc ^ 1][o] = F.pix[sc][n];
+            F.fi[sc ^ 1][o] = F.fi[sc][n];
+            F.fj[sc ^ 1][o] = F.fj[sc][n];
+            F.fl[sc ^ 1][o] = F.fl[sc][n];
+            ++o;
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        F.bo[sc ^ 1][F.npix] = total;
+        F.ctl->P = total;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// FFT background low-pass (denoise.hpp:254-319): unnormalised forward 2-D
+// DFT, radial raised-cosine mask, backward DFT / (nr*nc), clamp >= 0.
+// Separable direct DFTs (exactly reduced twiddle phases), three stages.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double lowpass_mask(double rho, double cutoff) {
+    if (cutoff >= 1.0) return 1.0;
+    double w = std_min(0.2 * cutoff, 1.0 - cutoff);
+    double lo = cutoff - w;
+    if (rho <= lo) return 1.0;
+    if (rho >= cutoff) return 0.0;
+    return 0.5 * (1.0 + cospi((rho - lo) / w));
+}
+
+// stage 1: forward DFT along every row of img (real) -> (re, im)
+__device__ void fft_stage1(const double* img, double* re, double* im, int nr, int nc,
+                           uint32_t gtid, uint32_t nth) {
+    for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
+        const int a = idx / nc, k = idx % nc;
+        double ar = 0.0, ai = 0.0;
+        for (int x = 0; x < nc; ++x) {
+            const int ph = (int)(((long long)k * x) % nc);
+            double sn, cs;
+            sincospi(2.0 * ph / nc, &sn, &cs);
+            const double v = img[(size_t)a * nc + x];
+            ar += v * cs;
+            ai -= v * sn;
+        }
+        re[idx] = ar;
+        im[idx] = ai;
+    }
+}
+
+// stage 2: per column: forward DFT along rows, mask, backward DFT along rows
+__device__ void fft_stage2(double* re, double* im, double* re2, double* im2, int nr, int nc,
+                           double cutoff, uint32_t gtid, uint32_t nth) {
+    const double fmax_r = (double)(nr / 2) / nr;
+    const double fmax_c = (double)(nc / 2) / nc;
+    const double rho_max = sqrt(fmax_r * fmax_r + fmax_c * fmax_c);
+    for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
+        // idx = (ka, b): forward along rows at frequency ka for column b
+        const int ka = idx / nc, b = idx % nc;
+        double ar = 0.0, ai = 0.0;
+        for (int x = 0; x < nr; ++x) {
+            const int ph = (int)(((long long)ka * x) % nr);
+            double sn, cs;
+            sincospi(2.0 * ph / nr, &sn, &cs);
+            const double xr = re[(size_t)x * nc + b], xi = im[(size_t)x * nc + b];
+            ar += xr * cs + xi * sn;
+            ai += xi * cs - xr * sn;
+        }
+        const int far = (ka <= nr / 2) ? ka : ka - nr;
+        const int fac = (b <= nc / 2) ? b : b - nc;
+        const double fr = (double)far / nr, fc = (double)fac / nc;
+        const double mval = lowpass_mask(sqrt(fr * fr + fc * fc) / rho_max, cutoff);
+        re2[idx] = ar * mval;
+        im2[idx] = ai * mval;
+    }
+}
+
+__device__ void fft_stage3(const double* re2, const double* im2, double* re, double* im, int nr,
+                           int nc, uint32_t gtid, uint32_t nth) {
+    // backward along rows (column direction) for each (a, b)
+    for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
+        const int a = idx / nc, b = idx % nc;
+        double ar = 0.0, ai = 0.0;
+        for (int k = 0; k < nr; ++k) {
+            const int ph = (int)(((long long)k * a) % nr);
+            double sn, cs;
+            sincospi(2.0 * ph / nr, &sn, &cs);
+            const double xr = re2[(size_t)k * nc + b], xi = im2[(size_t)k * nc + b];
+            ar += xr * cs - xi * sn;
+            ai += xr * sn + xi * cs;
+        }
+        re[idx] = ar;
+        im[idx] = ai;
+    }
+}
+
+__device__ void fft_stage4(const double* re, const double* im, double* out, int nr, int nc,
+                           int clamp_nonneg, uint32_t gtid, uint32_t nth) {
+    const double total = (double)nr * nc;
+    for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
+        const int a = idx / nc, y = idx % nc;
+        double ar = 0.0;
+        for (int k = 0; k < nc; ++k) {
+            const int ph = (int)(((long long)k * y) % nc);
+            double sn, cs;
+            sincospi(2.0 * ph / nc, &sn, &cs);
+            ar += re[(size_t)a * nc + k] * cs - im[(size_t)a * nc + k] * sn;
+        }
+        const double v = ar / total;
+        out[idx] = clamp_nonneg ? std_max(0.0, v) : v;
+    }
+}
+
+}  // namespace rt3d

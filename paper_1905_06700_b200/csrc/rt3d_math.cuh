@@ -1,0 +1,345 @@
+// rt3d_math.cuh — scalar device math of the RT3D path, restated from the
+// reference with its exact operand order (the translation unit is compiled
+// with -fmad=false, so no FMA is formed and IEEE double +,-,*,/,sqrt give the
+// same bits as the reference's SSE2 code).
+//
+//   Irf::value / deriv / support_bins / mass_in_gate   sensor.hpp:69-98
+//   ApssParams::weight                                  denoise.hpp:38-44
+//   3x3 covariance eigenvalues, 5x5 Pratt pencil        denoise.hpp:66-125,196
+//   project_onto_sphere                                 denoise.hpp:128-150
+#pragma once
+
+#include <cstdint>
+
+namespace rt3d {
+
+constexpr double kBackgroundFloor = 1e-6;  // reconstruct.hpp:23
+constexpr int kMaxBacktracks = 30;         // reconstruct.hpp:268
+
+// std::max / std::min / std::clamp with the reference's exact semantics
+// (argument order decides NaN and signed-zero results).
+__device__ __forceinline__ double std_max(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double std_min(double a, double b) { return (b < a) ? b : a; }
+__device__ __forceinline__ double std_clamp(double v, double lo, double hi) {
+    return (v < lo) ? lo : (hi < v) ? hi : v;
+}
+
+// One IRF: normalised samples + slopes (built on the host with the
+// reference's expressions, sensor.hpp:33-40), tau_max precomputed as
+// tau_min + dtau * (n - 1) (sensor.hpp:63), h_max = max sample
+// (reconstruct.hpp:126-127).
+struct IrfDev {
+    double tau_min, dtau, tau_max, h_max;
+    const double* s;
+    const double* d;
+    uint32_t n;
+    uint32_t pad_;
+};
+
+// sensor.hpp:69-75
+__device__ __forceinline__ double irf_value(const IrfDev& f, double tau) {
+    if (tau < f.tau_min || tau > f.tau_max) return 0.0;
+    double x = (tau - f.tau_min) / f.dtau;
+    unsigned long long k = (unsigned long long)x;
+    if (k > (unsigned long long)(f.n - 2)) k = f.n - 2;
+    double fr = x - (double)k;
+    double s0 = f.s[k], s1 = f.s[k + 1];
+    return s0 + fr * (s1 - s0);
+}
+
+// sensor.hpp:77-82
+__device__ __forceinline__ double irf_deriv(const IrfDev& f, double tau) {
+    if (tau <= f.tau_min || tau >= f.tau_max) return 0.0;
+    double x = (tau - f.tau_min) / f.dtau;
+    unsigned long long k = (unsigned long long)x;
+    if (k > (unsigned long long)(f.n - 2)) k = f.n - 2;
+    return f.d[k];
+}
+
+// sensor.hpp:86-90
+__device__ __forceinline__ void irf_support(const IrfDev& f, double t, int n_bins, int& lo,
+                                            int& hi) {
+    int a = (int)ceil(t + f.tau_min);
+    int b = (int)floor(t + f.tau_max);
+    lo = a < 0 ? 0 : a;
+    hi = b > n_bins - 1 ? n_bins - 1 : b;
+}
+
+// sensor.hpp:93-98
+__device__ __forceinline__ double irf_mass_in_gate(const IrfDev& f, double t, int n_bins) {
+    int lo, hi;
+    irf_support(f, t, n_bins, lo, hi);
+    double m = 0.0;
+    for (int b = lo; b <= hi; ++b) m += irf_value(f, (double)b - t);
+    return m;
+}
+
+// denoise.hpp:38-44
+__device__ __forceinline__ double apss_weight(double radius, double dist) {
+    double x = dist / radius;
+    if (x >= 1.0) return 0.0;
+    double s = 1.0 - x * x;
+    s *= s;
+    return s * s;
+}
+
+// Eigenvalues of the weighted 3x3 covariance (lower triangle c00,c10,c11,
+// c20,c21,c22), ascending, by cyclic Jacobi.  Only the eigenvalues decide
+// anything in apss_project (denoise.hpp:197-203): the eigenvector orients
+// the sign of the fitted field, and the projection is exactly invariant
+// under that sign.  Same rotation sequence as oracle_sym3_eigenvalues.
+__device__ __forceinline__ void sym3_eigenvalues(double a00, double a10, double a11, double a20,
+                                                 double a21, double a22, double& e0, double& e1,
+                                                 double& e2) {
+    double a[3][3] = {{a00, a10, a20}, {a10, a11, a21}, {a20, a21, a22}};
+#pragma unroll 1
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        double off = fabs(a[1][0]) + fabs(a[2][0]) + fabs(a[2][1]);
+        if (off == 0.0) break;
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+            for (int q = p + 1; q < 3; ++q) {
+                double apq = a[q][p];
+                if (apq == 0.0) continue;
+                double app = a[p][p], aqq = a[q][q];
+                double theta = (aqq - app) / (2.0 * apq);
+                double t;
+                if (fabs(theta) > 1e150) {
+                    t = 0.5 / theta;
+                } else {
+                    t = 1.0 / (fabs(theta) + sqrt(theta * theta + 1.0));
+                    if (theta < 0.0) t = -t;
+                }
+                double cs = 1.0 / sqrt(t * t + 1.0);
+                double sn = t * cs;
+                a[p][p] = app - t * apq;
+                a[q][q] = aqq + t * apq;
+                a[p][q] = 0.0;
+                a[q][p] = 0.0;
+                const int r = 3 - p - q;
+                double arp = a[r][p], arq = a[r][q];
+                double nrp = cs * arp - sn * arq;
+                double nrq = sn * arp + cs * arq;
+                a[r][p] = nrp;
+                a[p][r] = nrp;
+                a[r][q] = nrq;
+                a[q][r] = nrq;
+            }
+    }
+    double d0 = a[0][0], d1 = a[1][1], d2 = a[2][2], tmp;
+    if (d1 < d0) { tmp = d0; d0 = d1; d1 = tmp; }
+    if (d2 < d1) { tmp = d1; d1 = d2; d2 = tmp; }
+    if (d1 < d0) { tmp = d0; d0 = d1; d1 = tmp; }
+    e0 = d0;
+    e1 = d1;
+    e2 = d2;
+}
+
+// Symmetric 5x5 in packed lower-triangular order: index (i,j), i>=j, at
+// i*(i+1)/2 + j.
+__device__ __forceinline__ constexpr int lt(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// LDL' of the lower triangle of (M - sigma N), N the Pratt matrix
+// (denoise.hpp:82-84).  1 if all pivots are > 0 (positive definite).
+__device__ __forceinline__ int ldlt5_shift(const double m[15], double sigma, double L[15],
+                                           double d[5]) {
+    double a[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) a[k] = m[k];
+    a[lt(1, 1)] = m[lt(1, 1)] - sigma;
+    a[lt(2, 2)] = m[lt(2, 2)] - sigma;
+    a[lt(3, 3)] = m[lt(3, 3)] - sigma;
+    a[lt(4, 0)] = m[lt(4, 0)] + 2.0 * sigma;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        double s = a[lt(j, j)];
+#pragma unroll
+        for (int k = 0; k < j; ++k) s -= L[lt(j, k)] * L[lt(j, k)] * d[k];
+        if (!(s > 0.0)) return 0;
+        d[j] = s;
+#pragma unroll
+        for (int i = j + 1; i < 5; ++i) {
+            double v = a[lt(i, j)];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v -= L[lt(i, k)] * L[lt(j, k)] * d[k];
+            L[lt(i, j)] = v / s;
+        }
+    }
+    return 1;
+}
+
+// Smallest admissible eigenpair of the Pratt pencil (M, N): the eigenvector
+// that the reference's filter loop over GeneralizedEigenSolver's results keeps
+// (denoise.hpp:86-112).  For PSD M the admissible eigenvalues are the
+// non-negative ones, and the smallest is sup{sigma >= 0 : M - sigma N > 0};
+// bisection on the LDL' definiteness test brackets it, inverse iteration on
+// the last definite shift gives the eigenvector.  Same sequence of operations
+// as oracle_pratt_smallest (bit-identical on identical M).
+__device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
+    double L[15], d[5];
+    const double scale =
+        std_max(m[lt(0, 0)] + m[lt(1, 1)] + m[lt(2, 2)] + m[lt(3, 3)] + m[lt(4, 4)], 1e-300);
+    double sigma;
+    double hi = std_min(std_min(m[lt(1, 1)], m[lt(2, 2)]), m[lt(3, 3)]);
+    if (ldlt5_shift(m, 0.0, L, d) && hi > 0.0) {
+        double lo = 0.0;
+#pragma unroll 1
+        for (int it = 0; it < 200; ++it) {
+            double mid = 0.5 * (lo + hi);
+            if (!(mid > lo && mid < hi)) break;
+            if (ldlt5_shift(m, mid, L, d)) lo = mid;
+            else hi = mid;
+            if (hi - lo <= 1e-14 * hi) break;
+        }
+        sigma = lo;
+    } else {
+        double delta = 1e-15 * scale;
+        int ok = 0;
+#pragma unroll 1
+        for (int k = 0; k < 12 && !ok; ++k) {
+            if (ldlt5_shift(m, -delta, L, d)) ok = 1;
+            else delta *= 10.0;
+        }
+        if (!ok) return 0;
+        sigma = -delta;
+    }
+    if (!ldlt5_shift(m, sigma, L, d)) return 0;
+    double x0 = 1.0, x1 = 1.0, x2 = 1.0, x3 = 1.0, x4 = 1.0;
+#pragma unroll 1
+    for (int it = 0; it < 4; ++it) {
+        double y[5];
+        y[0] = -2.0 * x4;
+        y[1] = x1;
+        y[2] = x2;
+        y[3] = x3;
+        y[4] = -2.0 * x0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            double v = y[i];
+#pragma unroll
+            for (int k = 0; k < i; ++k) v -= L[lt(i, k)] * y[k];
+            y[i] = v;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) y[i] = y[i] / d[i];
+#pragma unroll
+        for (int i = 4; i >= 0; --i) {
+            double v = y[i];
+#pragma unroll
+            for (int k = i + 1; k < 5; ++k) v -= L[lt(k, i)] * y[k];
+            y[i] = v;
+        }
+        double nrm = sqrt(y[0] * y[0] + y[1] * y[1] + y[2] * y[2] + y[3] * y[3] + y[4] * y[4]);
+        if (!(nrm > 0.0) || !isfinite(nrm)) return 0;
+        x0 = y[0] / nrm;
+        x1 = y[1] / nrm;
+        x2 = y[2] / nrm;
+        x3 = y[3] / nrm;
+        x4 = y[4] / nrm;
+    }
+    u[0] = x0;
+    u[1] = x1;
+    u[2] = x2;
+    u[3] = x3;
+    u[4] = x4;
+    return 1;
+}
+
+struct Sphere {
+    double u0, ul0, ul1, ul2, uq;
+};
+
+// fit tail of fit_algebraic_sphere (denoise.hpp:86-117): pencil solve,
+// Pratt normalisation, un-centring.  The orientation flip
+// (denoise.hpp:119-123) negates (u0, ul, uq) together; project_onto_sphere
+// is bitwise invariant under it, so it is omitted.
+__device__ __forceinline__ bool sphere_from_moments(const double m[15], double c0, double c1,
+                                                    double c2, Sphere& out) {
+    double v[5];
+    if (!pratt_smallest(m, v)) return false;
+    double vn2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3] + v[4] * v[4];
+    if (sqrt(vn2) < 1e-300) return false;
+    double nrm = v[1] * v[1] + v[2] * v[2] + v[3] * v[3] - 4.0 * v[0] * v[4];
+    if (nrm <= 1e-14 * vn2) return false;
+    double sq = sqrt(nrm);
+    double u0 = v[0] / sq, l0 = v[1] / sq, l1 = v[2] / sq, l2 = v[3] / sq, uq = v[4] / sq;
+    double dot = l0 * c0 + l1 * c1 + l2 * c2;
+    double csq = c0 * c0 + c1 * c1 + c2 * c2;
+    out.u0 = u0 - dot + uq * csq;
+    double tq = 2.0 * uq;
+    out.ul0 = l0 - tq * c0;
+    out.ul1 = l1 - tq * c1;
+    out.ul2 = l2 - tq * c2;
+    out.uq = uq;
+    return true;
+}
+
+// project_onto_sphere, denoise.hpp:128-150
+__device__ __forceinline__ bool project_sphere(const Sphere& s, double eps, double p0, double p1,
+                                               double p2, double& o0, double& o1, double& o2) {
+    double g2 = s.ul0 * s.ul0 + s.ul1 * s.ul1 + s.ul2 * s.ul2;
+    bool plane = fabs(s.uq) < eps;
+    double c0 = 0, c1 = 0, c2 = 0, disc = 0;
+    if (!plane) {
+        double tq = 2.0 * s.uq;
+        c0 = -s.ul0 / tq;
+        c1 = -s.ul1 / tq;
+        c2 = -s.ul2 / tq;
+        disc = g2 - 4.0 * s.u0 * s.uq;
+        if (disc <= 0.0) plane = true;
+    }
+    if (plane) {
+        if (g2 < 1e-20) return false;
+        double ev = s.u0 + (s.ul0 * p0 + s.ul1 * p1 + s.ul2 * p2) + s.uq * (p0 * p0 + p1 * p1 + p2 * p2);
+        double f = ev / g2;
+        o0 = p0 - f * s.ul0;
+        o1 = p1 - f * s.ul1;
+        o2 = p2 - f * s.ul2;
+        return true;
+    }
+    double radius = sqrt(disc) / (2.0 * fabs(s.uq));
+    double d0 = p0 - c0, d1 = p1 - c1, d2 = p2 - c2;
+    double dn = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (dn < 1e-14) return false;
+    double f = radius / dn;
+    o0 = c0 + f * d0;
+    o1 = c1 + f * d1;
+    o2 = c2 + f * d2;
+    return true;
+}
+
+// Exact parallel::pairwise_sum (parallel.hpp:52-61) of up to 32 values.
+__device__ __forceinline__ double seq_sum(const double* v, int a, int n) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += v[a + k];
+    return s;
+}
+__device__ __forceinline__ double pw16(const double* v, int a, int n) {
+    if (n <= 8) return seq_sum(v, a, n);
+    int h = n / 2;
+    return seq_sum(v, a, h) + seq_sum(v, a + h, n - h);
+}
+__device__ __forceinline__ double pw32(const double* v, int a, int n) {
+    if (n <= 16) return pw16(v, a, n);
+    int h = n / 2;
+    return pw16(v, a, h) + pw16(v, a + h, n - h);
+}
+
+// Range of node k at depth G of pairwise_sum's recursion over n elements.
+__device__ __forceinline__ void tree_node_range(uint32_t n, int G, uint32_t k, uint32_t& lo,
+                                                uint32_t& size) {
+    lo = 0;
+    size = n;
+    for (int b = G - 1; b >= 0; --b) {
+        uint32_t h = size / 2;
+        if ((k >> b) & 1u) {
+            lo += h;
+            size -= h;
+        } else {
+            size = h;
+        }
+    }
+}
+
+}  // namespace rt3d

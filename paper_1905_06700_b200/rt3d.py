@@ -1,0 +1,279 @@
+"""ctypes binding of librt3d.so (include/rt3d.h).
+
+The library is built in-tree (paper_1905_06700_b200/librt3d.so) by
+__graft_entry__.build().  Loading fails loudly when it is missing, and every
+compute call raises when no CUDA device is present: there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+from .abi import (
+    POINT_DTYPE, PEAK_DTYPE, STEP_DIAG_DTYPE, STATUS, ApssParams, Cube, Event, InitParams, Irf,
+    Peak, Point, ReconConfig, Report, Scene, Sensor, StateView, StepDiag, Config, ptr,
+)
+
+LIB_PATH = Path(__file__).resolve().parent / "librt3d.so"
+
+P = C.POINTER
+_dbl, _u64, _u8, _i32, _st = C.c_double, C.c_uint64, C.c_uint8, C.c_int32, C.c_int
+
+
+class Rt3dError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rt3d {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_lib: Optional[C.CDLL] = None
+
+
+def _bind(lib, name, res, args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = args
+
+
+def lib() -> C.CDLL:
+    """Load librt3d.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() first")
+    L = C.CDLL(str(LIB_PATH))
+    SS = C.c_void_p
+    _bind(L, "rt3d_abi_version", C.c_int, [])
+    _bind(L, "rt3d_last_error", C.c_char_p, [])
+    _bind(L, "rt3d_device_count", C.c_int, [])
+    _bind(L, "rt3d_session_create", _st, [C.c_int, P(SS)])
+    _bind(L, "rt3d_session_destroy", _st, [SS])
+    _bind(L, "rt3d_session_synchronize", _st, [SS])
+    _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
+    _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
+    _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
+    _bind(L, "rt3d_report_info", _st, [SS, P(Report)])
+    _bind(L, "rt3d_report_copy", _st, [SS, P(_dbl), P(StepDiag)])
+    _bind(L, "rt3d_state_size", _st, [SS, P(_u64)])
+    _bind(L, "rt3d_state_copy", _st, [SS, P(Point), P(_dbl)])
+    _bind(L, "rt3d_matched_filter_peaks", _st,
+          [SS, P(Event), _u64, P(Irf), _i32, _i32, _dbl, _i32, P(Peak), P(_i32)])
+    _bind(L, "rt3d_init_matched_filter", _st, [SS, P(InitParams)])
+    _bind(L, "rt3d_baseline_xcorr", _st, [SS])
+    _bind(L, "rt3d_state_upload", _st, [SS, P(StateView)])
+    _bind(L, "rt3d_nll", _st, [SS, P(_dbl)])
+    _bind(L, "rt3d_grad_depth", _st, [SS, P(_dbl), P(_u8)])
+    _bind(L, "rt3d_grad_intensity", _st, [SS, P(_dbl)])
+    _bind(L, "rt3d_grad_background", _st, [SS, P(_dbl)])
+    _bind(L, "rt3d_block_curvatures", _st, [SS, P(_dbl), P(_dbl), P(_dbl)])
+    _bind(L, "rt3d_palm_step", _st, [SS, P(ReconConfig), P(StepDiag)])
+    _bind(L, "rt3d_apss_project", _st,
+          [SS, P(Point), _u64, P(ApssParams), P(Point), _u64, _dbl, P(Point)])
+    _bind(L, "rt3d_knn_intensity_filter", _st,
+          [SS, P(Point), _u64, _i32, P(Point), _u64, _dbl, _dbl, P(Point)])
+    _bind(L, "rt3d_prune", _st, [SS, P(Point), _u64, _dbl, P(Point), P(_u64)])
+    _bind(L, "rt3d_fft_lowpass_filter", _st,
+          [SS, P(_dbl), _i32, _i32, _dbl, _i32, P(_dbl)])
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        raise Rt3dError(status, lib().rt3d_last_error().decode(errors="replace"))
+
+
+EXPORTED = [
+    "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
+    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_set_sensor", "rt3d_set_cube",
+    "rt3d_reconstruct", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
+    "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
+    "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
+    "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
+    "rt3d_apss_project", "rt3d_knn_intensity_filter", "rt3d_prune", "rt3d_fft_lowpass_filter",
+]
+
+
+class Session:
+    """One CUDA device + stream with resident sensor / cube / state."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = C.c_void_p()
+        _check(L.rt3d_session_create(device, C.byref(h)))
+        self.h = h
+        self.scene: Optional[Scene] = None
+
+    def close(self):
+        if self.h:
+            lib().rt3d_session_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- inputs ----------------------------------------------------------
+    def set_scene(self, sc: Scene):
+        L = lib()
+        self._sensor = sc.sensor_c()
+        self._cube = sc.cube_c()
+        _check(L.rt3d_set_sensor(self.h, C.byref(self._sensor)))
+        _check(L.rt3d_set_cube(self.h, C.byref(self._cube)))
+        self.scene = sc
+
+    def set_cube(self, sc: Scene):
+        self._cube = sc.cube_c()
+        _check(lib().rt3d_set_cube(self.h, C.byref(self._cube)))
+
+    def upload_state(self, points: np.ndarray, background: np.ndarray):
+        from .abi import buckets
+        sc = self.scene
+        points = np.ascontiguousarray(points, POINT_DTYPE)
+        background = np.ascontiguousarray(background, np.float64)
+        bo, bp = buckets(points, sc.n_rows, sc.n_cols)
+        v = StateView()
+        v.points = ptr(points, Point) if len(points) else None
+        v.n_points = len(points)
+        v.background = ptr(background, _dbl)
+        v.bucket_offsets = ptr(bo, C.c_uint32)
+        v.bucket_points = ptr(bp, C.c_uint32) if len(points) else None
+        self._keep = (points, background, bo, bp)
+        _check(lib().rt3d_state_upload(self.h, C.byref(v)))
+
+    # -- hot path --------------------------------------------------------
+    def reconstruct_async(self, cfg: Config):
+        self._cfg_c = cfg.to_c()
+        _check(lib().rt3d_reconstruct(self.h, C.byref(self._cfg_c)))
+
+    def synchronize(self):
+        _check(lib().rt3d_session_synchronize(self.h))
+
+    def report(self) -> dict:
+        r = Report()
+        _check(lib().rt3d_report_info(self.h, C.byref(r)))
+        it = r.iterations
+        trace = np.zeros(it + 1)
+        steps = np.zeros(max(it, 1), STEP_DIAG_DTYPE)
+        _check(lib().rt3d_report_copy(self.h, ptr(trace, _dbl),
+                                      steps.ctypes.data_as(P(StepDiag))))
+        return dict(iterations=it, points=r.points, init_nll=r.init_nll, final_nll=r.final_nll,
+                    init_seconds=r.init_seconds, iterate_seconds=r.iterate_seconds,
+                    total_seconds=r.total_seconds, trace=trace, steps=steps[:it])
+
+    def state(self):
+        n = _u64()
+        _check(lib().rt3d_state_size(self.h, C.byref(n)))
+        pts = np.zeros(max(n.value, 1), POINT_DTYPE)
+        bg = np.zeros(self.scene.n_pixels)
+        _check(lib().rt3d_state_copy(self.h, ptr(pts, Point), ptr(bg, _dbl)))
+        return pts[: n.value].copy(), bg
+
+    def reconstruct(self, cfg: Config) -> dict:
+        self.reconstruct_async(cfg)
+        rep = self.report()
+        rep["points"], rep["background"] = self.state()
+        return rep
+
+    # -- operators -------------------------------------------------------
+    def init_matched_filter(self, cfg: Config):
+        ip = cfg.init_c()
+        _check(lib().rt3d_init_matched_filter(self.h, C.byref(ip)))
+        return self.state()
+
+    def baseline_xcorr(self):
+        _check(lib().rt3d_baseline_xcorr(self.h))
+        return self.state()[0]
+
+    def nll(self) -> float:
+        v = _dbl()
+        _check(lib().rt3d_nll(self.h, C.byref(v)))
+        return v.value
+
+    def grads(self) -> dict:
+        n = len(self._keep[0])
+        npix = self.scene.n_pixels
+        out = {k: np.zeros(max(n, 1)) for k in ("gd", "gr", "cd", "cr")}
+        out["oog"] = np.zeros(max(n, 1), np.uint8)
+        out["gb"] = np.zeros(npix)
+        out["cb"] = np.zeros(npix)
+        L = lib()
+        _check(L.rt3d_grad_depth(self.h, ptr(out["gd"], _dbl), ptr(out["oog"], _u8)))
+        _check(L.rt3d_grad_intensity(self.h, ptr(out["gr"], _dbl)))
+        _check(L.rt3d_grad_background(self.h, ptr(out["gb"], _dbl)))
+        _check(L.rt3d_block_curvatures(self.h, ptr(out["cd"], _dbl), ptr(out["cr"], _dbl),
+                                       ptr(out["cb"], _dbl)))
+        for k in ("gd", "gr", "cd", "cr", "oog"):
+            out[k] = out[k][:n]
+        return out
+
+    def palm_step(self, cfg: Config):
+        c = cfg.to_c()
+        d = StepDiag()
+        _check(lib().rt3d_palm_step(self.h, C.byref(c), C.byref(d)))
+        pts, bg = self.state()
+        return pts, bg, d
+
+    def matched_filter_peaks(self, events, irf_samples, tau_min, dtau, n_bins, k, thr, min_sep):
+        from .abi import EVENT_DTYPE
+        events = np.ascontiguousarray(events, EVENT_DTYPE)
+        samples = np.ascontiguousarray(irf_samples, np.float64)
+        f = Irf()
+        f.tau_min, f.dtau = tau_min, dtau
+        f.samples = ptr(samples, _dbl)
+        f.n_samples = len(samples)
+        out = np.zeros(max(k, 1), PEAK_DTYPE)
+        n = _i32()
+        _check(lib().rt3d_matched_filter_peaks(
+            self.h, ptr(events, Event) if len(events) else None, len(events), C.byref(f), n_bins,
+            k, thr, min_sep, out.ctypes.data_as(P(Peak)), C.byref(n)))
+        return out[: n.value].copy()
+
+    def apss_project(self, points, radius, min_nbrs=6, eps=1e-3, cell=None, index=None):
+        points = np.ascontiguousarray(points, POINT_DTYPE)
+        index = points if index is None else np.ascontiguousarray(index, POINT_DTYPE)
+        out = np.zeros(len(points), POINT_DTYPE)
+        ap = ApssParams()
+        ap.kernel_radius, ap.min_neighbors, ap.sphere_degeneracy_eps = radius, min_nbrs, eps
+        _check(lib().rt3d_apss_project(self.h, ptr(points, Point), len(points), C.byref(ap),
+                                       ptr(index, Point), len(index),
+                                       radius if cell is None else cell, ptr(out, Point)))
+        return out
+
+    def knn_filter(self, points, k, radius, cell=None, index=None):
+        points = np.ascontiguousarray(points, POINT_DTYPE)
+        index = points if index is None else np.ascontiguousarray(index, POINT_DTYPE)
+        out = np.zeros(len(points), POINT_DTYPE)
+        _check(lib().rt3d_knn_intensity_filter(self.h, ptr(points, Point), len(points), k,
+                                               ptr(index, Point), len(index),
+                                               radius if cell is None else cell, radius,
+                                               ptr(out, Point)))
+        return out
+
+    def prune(self, points, r_min):
+        points = np.ascontiguousarray(points, POINT_DTYPE)
+        out = np.zeros(max(len(points), 1), POINT_DTYPE)
+        n = _u64()
+        _check(lib().rt3d_prune(self.h, ptr(points, Point), len(points), r_min, ptr(out, Point),
+                                C.byref(n)))
+        return out[: n.value].copy()
+
+    def fft_lowpass(self, img, cutoff, clamp=False):
+        img = np.ascontiguousarray(img, np.float64)
+        out = np.zeros_like(img)
+        _check(lib().rt3d_fft_lowpass_filter(self.h, ptr(img, _dbl), img.shape[0], img.shape[1],
+                                             cutoff, int(clamp), ptr(out, _dbl)))
+        return out
