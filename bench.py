@@ -1,0 +1,382 @@
+#!/usr/bin/env python3
+"""RT3D frame benchmark (BASELINE.json metric: frames/s and ms/frame).
+
+Workload (BASELINE.json configs[1]): a synthetic
+141x141-pixel, 4613-bin "polystyrene head" frame (back plane with a hole +
+head bump, 3 signal photons/px, SBR 13), reconstructed with the acceptance
+preset at apss_radius 0.02 m, 25 PALM iterations, stop_tol 0.  One step =
+one frame through splidar::reconstruct's device replacement.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Ours: inputs resident in HBM, one persistent kernel per frame, each frame
+timed with CUDA events on the session stream, the 126 MB L2 flushed between
+frames.  e2e: the same frames through the C ABI from pinned host buffers
+(cube upload + reconstruct + cloud/background download), wall clock.
+N > 1 (torchrun): frames are independent, each rank reconstructs its own
+stream of frames (weak scaling, no collective on the data path).
+--impl reference: the reference CPU implementation (the headers compiled
+unchanged, oracle/_ref/libref.so) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1905_06700_b200.abi import Config  # noqa: E402
+from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
+
+PAPER_MS_PER_FRAME = 13.0  # 141x141x4613 on a Titan Xp
+
+
+def config_b():
+    """141x141 px, 4613 bins of 0.3 mm."""
+    pitch = 0.0025
+    spec = SceneSpec(
+        rows=141, cols=141, bins=4613, bin_resolution_m=0.0003, pixel_pitch_m=pitch,
+        irf_sigma_bins=1.5, target_ppp=3.0, target_sbr=13.0,
+        surfaces=[
+            SurfaceSpec(depth_m=1.2, holes=[(40, 30, 101, 121)]),
+            SurfaceSpec(kind="bump", depth_m=1.0, bump_amp=-0.12, bump_width=0.06,
+                        bump_cx=70.5 * pitch, bump_cy=75.5 * pitch, region=(35, 25, 106, 126)),
+        ])
+    cfg = Config(max_iters=25, stop_tol=0.0, apss_radius=0.02, knn_k=9, r_min=0.25,
+                 init_max_returns=3, init_peak_threshold=0.5, init_min_separation=6)
+    return spec, 141, cfg, "141x141 px x 4613 bins polystyrene-head-like synthetic frame"
+
+
+def frame_bytes(sc, rep) -> float:
+    """Algorithmic HBM bytes of one frame:
+    every likelihood sweep reads the CSR cube (8 B/event), per-pixel
+    offsets/bucket/background/gain/dead (29 B/px) and t, r, bucket index
+    (20 B/point); gradient sweeps write grad+curv (16 B/unit), candidate
+    sweeps write the candidate (8 B/unit); APSS 17 B/pt, kNN 24 B/pt, prune
+    9 B/pt in + 33 B/survivor + 4 B/px; init 8E + 29 Npix + 33 P0."""
+    E, npix = len(sc.events), sc.n_pixels
+    steps = rep["steps"]
+
+    def sweep(P, extra):
+        return 8.0 * E + 29.0 * npix + 20.0 * P + extra
+
+    P0 = int(steps[0]["points_before"]) if len(steps) else 0
+    total = 8.0 * E + 29.0 * npix + 33.0 * P0          # init
+    total += sweep(P0, 16.0 * P0)                          # first grad_t (+ init nll)
+    for st in steps:
+        P, P1 = int(st["points_before"]), int(st["points_after"])
+        if P > 0:
+            total += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
+            total += 17.0 * P                              # APSS
+            total += sweep(P, 16.0 * P)                    # grad_r
+            total += (1 + int(st["intensity_backtracks"])) * sweep(P, 8.0 * P)
+            total += 24.0 * P                              # kNN
+            total += 9.0 * P + 33.0 * P1 + 4.0 * npix      # prune + refresh
+        total += sweep(P1, 16.0 * npix)                    # grad_b
+        total += (1 + int(st["background_backtracks"])) * sweep(P1, 8.0 * npix)
+        total += sweep(P1, 16.0 * P1)                      # grad_t (nll after + next grads)
+    return total
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier_max(value: float, world: int, device: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{device}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def load_measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic_per_frame():
+    """dram bytes per frame-kernel launch from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_frame_kernel.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["dram_bytes_per_launch"])
+        except Exception:
+            return None
+    return None
+
+
+def reference_frame_seconds(sc, cfg, threads: int = 0):
+    """The reference implementation itself (headers compiled unchanged,
+    oracle/_ref/libref.so) timed on the host cores; else the C port."""
+    import ctypes as C
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    if O.ref_available():
+        lib = O.ref()
+        lib.ref_set_threads(threads)
+        n, it, secs = C.c_uint64(), C.c_int(), C.c_double()
+        rc = lib.ref_reconstruct(C.byref(sc.cube_c()), C.byref(sc.sensor_c()),
+                                 C.byref(cfg.to_c()), C.byref(n), C.byref(it), C.byref(secs))
+        if rc != 0:
+            raise RuntimeError(lib.ref_last_error().decode())
+        cores = threads if threads > 0 else (os.cpu_count() or 1)
+        return secs.value, "reference", cores
+    t0 = time.perf_counter()
+    O.reconstruct(sc, cfg, "oracle")
+    return time.perf_counter() - t0, "port", 1
+
+
+def run_reference_arm(args, world, rank):
+    if rank != 0:
+        return 0
+    spec, seed, cfg, workload = config_b()
+    sc = simulate(spec, seed)
+    times = []
+    for k in range(args.warmup + args.steps):
+        secs, kind, cores = reference_frame_seconds(sc, cfg)
+        if k >= args.warmup:
+            times.append(secs)
+    total = sum(times)
+    fps = len(times) / total
+    line = {
+        "impl": "reference", "metric": "frames/s", "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload, "pixels": 141 * 141, "bins": 4613,
+                   "palm_iterations": cfg.max_iters, "events": int(len(sc.events))},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
+                         "sample": f"{len(times)} full frames (25 PALM iterations) after "
+                                   f"{args.warmup} warm-up frames"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_init()
+    if args.impl == "reference":
+        rc = run_reference_arm(args, world, rank)
+        barrier(world)
+        return rc
+
+    import torch
+    from paper_1905_06700_b200.rt3d import Session
+
+    torch.cuda.set_device(local)
+    spec, seed, cfg, workload = config_b()
+    sc = simulate(spec, seed)
+    sess = Session(local)
+    sess.set_scene(sc)
+    stream = torch.cuda.ExternalStream(sess.stream_ptr, device=torch.device("cuda", local))
+    flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
+
+    # warm-up (module load, buffers)
+    for _ in range(args.warmup):
+        sess.reconstruct_async(cfg)
+    sess.synchronize()
+    rep = sess.report()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_wall0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            for k in range(K):
+                flush.zero_()  # evict the frame's working set from L2 between frames
+                ev[k][0].record(stream)
+                sess.reconstruct_async(cfg)
+                ev[k][1].record(stream)
+        stream.synchronize()
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    barrier(world)
+    frame_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_s = sum(frame_ms) / 1e3
+    dev_s_max = barrier_max(dev_s, world, local)
+    value = world * K / dev_s_max
+    rep = sess.report()
+    pts, _ = sess.state()
+
+    # phase breakdown of one (untimed) frame from the in-kernel timer
+    sess.profile(True)
+    sess.reconstruct_async(cfg)
+    sess.synchronize()
+    phases = {}
+    for name, ns in sess.profile_phases():
+        d = phases.setdefault(name, [0, 0.0])
+        d[0] += 1
+        d[1] += ns / 1e3
+    sess.profile(False)
+
+    # e2e through the C ABI from pinned host buffers
+    n_e2e = args.e2e_steps or K
+    pin_off = torch.empty(len(sc.offsets), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+    pin_ev = torch.empty(len(sc.events) * 2, dtype=torch.int32, pin_memory=True).numpy().view(sc.events.dtype)
+    pin_off[:] = sc.offsets
+    pin_ev[:] = sc.events
+    from paper_1905_06700_b200.abi import POINT_DTYPE
+    import copy
+    sc_pin = copy.copy(sc)
+    sc_pin.offsets, sc_pin.events = pin_off, pin_ev
+    out_pts = torch.empty(len(pts) * 64 + 64 * 1024, dtype=torch.uint8, pin_memory=True).numpy()
+    barrier(world)
+    t0 = time.perf_counter()
+    d2h = 0
+    for _ in range(n_e2e):
+        sess.set_cube(sc_pin)              # H2D of the frame's photon cube
+        sess.reconstruct_async(cfg)
+        p_e2e, bg_e2e = sess.state()       # D2H of the cloud + background
+        d2h = p_e2e.nbytes + bg_e2e.nbytes
+    e2e_s = time.perf_counter() - t0
+    e2e_s = barrier_max(e2e_s, world, local)
+    e2e_fps = world * n_e2e / e2e_s
+    h2d = sc.offsets.nbytes + sc.events.nbytes
+
+    peak, peak_src = load_measured_peaks()
+    fb = frame_bytes(sc, rep)
+    avg_frame_s = dev_s / K
+    achieved = fb / avg_frame_s / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        secs, kind, cores = reference_frame_seconds(sc, cfg)
+        cpu = {"value": 1.0 / secs, "unit": "frames/s", "cores": cores, "kind": kind,
+               "sample": "1 full frame of the same workload (25 PALM iterations), "
+                         "reference headers compiled unchanged (oracle/_ref), all host threads"}
+
+    if rank == 0:
+        line = {
+            "metric": "frames/s", "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s_max / K,
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": value / (1000.0 / PAPER_MS_PER_FRAME),
+            "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": workload, "pixels": 141 * 141, "bins": 4613,
+                "palm_iterations": cfg.max_iters, "events": int(len(sc.events)),
+                "points_init": int(rep["steps"][0]["points_before"]) if len(rep["steps"]) else 0,
+                "points_final": int(rep["points"]), "parallelism": f"frames x{world} (replicas)",
+                "l2": "flushed between frames (256 MB write)",
+                "vs_baseline_ref": "paper GPU 13 ms/frame on Titan Xp (BASELINE.md)",
+                "ms_per_frame_p50": statistics.median(frame_ms),
+                "ms_per_frame_min": min(frame_ms),
+            },
+            "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic_per_frame(),
+                         "kernel": "rt3d::frame_kernel (whole frame, 1 launch)",
+                         "algorithmic_bytes_per_launch": fb, "peak_source": peak_src},
+            "gpu_launches": K,
+            "clocks": clocks.summary(),
+            "phases_us_per_frame": {k: round(v[1], 1) for k, v in phases.items()},
+            "phase_counts": {k: v[0] for k, v in phases.items()},
+            "wall_s_timed_region": t_wall,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    sess.close()
+    barrier(world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

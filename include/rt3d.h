@@ -185,6 +185,14 @@ int rt3d_device_count(void);
 rt3d_status rt3d_session_create(int device, rt3d_session** out);
 rt3d_status rt3d_session_destroy(rt3d_session* s);
 rt3d_status rt3d_session_synchronize(rt3d_session* s);
+/* The session's CUDA stream (a cudaStream_t), for callers that time the
+ * stream-ordered entry points with their own CUDA events. */
+void* rt3d_session_stream(rt3d_session* s);
+/* Phase timer: when enabled, the frame kernel stamps (phase id,
+ * %globaltimer ns) after every grid barrier; rt3d_profile_copy reads the
+ * pairs of the last launch.  Off by default (bench.py's breakdown only). */
+rt3d_status rt3d_session_profile(rt3d_session* s, int enable);
+rt3d_status rt3d_profile_copy(rt3d_session* s, uint64_t* pairs, uint32_t cap, uint32_t* n);
 
 /* Upload the sensor (IRF tables, gain, dead mask) and the photon cube.  They
  * stay resident until replaced.  Validation follows SensorModel's ctor

@@ -30,6 +30,19 @@ static_assert(sizeof(rt3d_point) == 64, "point layout");
 // ===========================================================================
 namespace rt3d {
 
+// grid barrier + optional phase stamp (leader thread, after the barrier)
+__device__ __forceinline__ void gsync(cg::grid_group& grid, const Frame& F, int phase) {
+    grid.sync();
+    if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned int k = F.ctl->nprof;
+        if (k < F.ctl->prof_cap) {
+            F.prof[2 * k] = (unsigned long long)phase;
+            F.prof[2 * k + 1] = globaltimer();
+            F.ctl->nprof = k + 1;
+        }
+    }
+}
+
 template <int KIND>
 __device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc, int rc, int bc,
                           int sc, int op, int it) {
@@ -43,7 +56,7 @@ __device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc
         X.sc = sc;
         X.apply_floor = 0;
         tree_sweep<KIND>(F, sm, X, op, it);
-        grid.sync();
+        gsync(grid, F, KIND == K_CAND_T ? PH_CAND_T : KIND == K_CAND_R ? PH_CAND_R : PH_CAND_B);
     }
 }
 
@@ -54,12 +67,24 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
     __syncthreads();
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     const int prog = F.cfg.program;
-    if (leader) F.ctl->t_start = globaltimer();
+    if (leader) {
+        // Ctl is zeroed by cudaMemsetAsync before the launch; nothing else
+        // reads these fields before the first grid barrier.
+        const unsigned long long t0 = globaltimer();
+        F.ctl->t_start = t0;
+        F.ctl->P = F.P0;
+        F.ctl->prof_cap = F.prof_cap;
+        if (F.prof && F.prof_cap) {
+            F.prof[0] = 0;
+            F.prof[1] = t0;
+            F.ctl->nprof = 1;
+        }
+    }
 
     int tc = F.tc0, rc = F.rc0, bc = F.bc0, sc = F.sc0;
     if (prog == PROG_RECON || prog == PROG_INIT || prog == PROG_BASELINE || prog == PROG_PEAKS) {
         phase_init_peaks(F, sm);
-        grid.sync();
+        gsync(grid, F, PH_INIT_PEAKS);
         if (prog == PROG_PEAKS) return;
         const bool baseline = prog == PROG_BASELINE;
         const int s2 = F.s * F.s;
@@ -67,9 +92,9 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             uint32_t nv = F.nval[p];
             return baseline ? (nv > 0 ? 1u : 0u) : nv * (uint32_t)s2;
         });
-        grid.sync();
+        gsync(grid, F, PH_SCAN);
         phase_spawn(F, sm, baseline);
-        grid.sync();
+        gsync(grid, F, PH_SPAWN);
         tc = rc = bc = sc = 0;
         if (prog != PROG_RECON) {
             if (leader) {
@@ -99,16 +124,16 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
     }
     if (prog == PROG_GRADS) {
         tree_sweep<K_GRAD_T>(F, sm, X0, OP_RESULT, 0);
-        grid.sync();
+        gsync(grid, F, PH_GRAD_T);
         tree_sweep<K_GRAD_R>(F, sm, X0, OP_RESULT, 0);
-        grid.sync();
+        gsync(grid, F, PH_GRAD_R);
         tree_sweep<K_GRAD_B>(F, sm, X0, OP_RESULT, 0);
         return;
     }
 
     // ---- PALM iterations (reconstruct.hpp:300-435, 466-478) ----
     tree_sweep<K_GRAD_T>(F, sm, X0, OP_GRAD_T_FIRST, 0);
-    grid.sync();
+    gsync(grid, F, PH_GRAD_T);
     const uint32_t nth = gridDim.x * kBlock;
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     for (int it = 0; it < F.cfg.max_iters; ++it) {
@@ -127,7 +152,7 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             cand_loop<K_CAND_T>(F, sm, grid, tc, rc, bc, sc, OP_CAND_T, it);
             if (ld_cg(&F.ctl->accept)) tc ^= 1;
             phase_apss(F, tc, sc, P);
-            grid.sync();
+            gsync(grid, F, PH_APSS);
             tc ^= 1;
             SweepCtx X = X0;
             X.tc = tc;
@@ -135,17 +160,17 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             X.bc = bc;
             X.sc = sc;
             tree_sweep<K_GRAD_R>(F, sm, X, OP_GRAD_R, it);
-            grid.sync();
+            gsync(grid, F, PH_GRAD_R);
             // intensity block: safeguarded step, kNN filter, prune
             cand_loop<K_CAND_R>(F, sm, grid, tc, rc, bc, sc, OP_CAND_R, it);
             if (ld_cg(&F.ctl->accept)) rc ^= 1;
             phase_knn(F, tc, rc, sc, P);
-            grid.sync();
+            gsync(grid, F, PH_KNN);
             rc ^= 1;
             phase_prune_a(F, sm, rc, sc);
-            grid.sync();
+            gsync(grid, F, PH_PRUNE_A);
             phase_prune_b(F, sm, tc, rc, sc);
-            grid.sync();
+            gsync(grid, F, PH_PRUNE_B);
             tc ^= 1;
             rc ^= 1;
             sc ^= 1;
@@ -153,10 +178,10 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             X.rc = rc;
             X.sc = sc;
             tree_sweep<K_GRAD_B>(F, sm, X, OP_GRAD_B_PRUNED, it);
-            grid.sync();
+            gsync(grid, F, PH_GRAD_B);
         } else {
             tree_sweep<K_GRAD_B>(F, sm, X0, OP_GRAD_B_EMPTY, it);
-            grid.sync();
+            gsync(grid, F, PH_GRAD_B);
         }
         // background block: safeguarded step, FFT low-pass, floor
         cand_loop<K_CAND_B>(F, sm, grid, tc, rc, bc, sc, OP_CAND_B, it);
@@ -168,13 +193,13 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             double* re2 = F.fft_re + F.npix;
             double* im2 = F.fft_im + F.npix;
             fft_stage1(F.b[bc], re, im, nr, nc, gtid, nth);
-            grid.sync();
+            gsync(grid, F, PH_FFT);
             fft_stage2(re, im, re2, im2, nr, nc, F.cfg.cutoff, gtid, nth);
-            grid.sync();
+            gsync(grid, F, PH_FFT);
             fft_stage3(re2, im2, re, im, nr, nc, gtid, nth);
-            grid.sync();
+            gsync(grid, F, PH_FFT);
             fft_stage4(re, im, F.b[bc], nr, nc, 1, gtid, nth);
-            grid.sync();
+            gsync(grid, F, PH_FFT);
         }
         SweepCtx X = X0;
         X.tc = tc;
@@ -183,7 +208,7 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
         X.sc = sc;
         X.apply_floor = 1;
         tree_sweep<K_GRAD_T>(F, sm, X, OP_GRAD_T_END, it);
-        grid.sync();
+        gsync(grid, F, PH_GRAD_T);
         X0 = X;
         X0.apply_floor = 0;
         if (ld_cg(&F.ctl->stop)) break;
@@ -410,7 +435,8 @@ struct rt3d_session {
     size_t pcap = 0;
     DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot;
     DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im;
-    DevBuf ctl, diag, trace, outpts, misc;
+    DevBuf ctl, diag, trace, outpts, misc, prof;
+    bool profile = false;
     Ctl* h_ctl = nullptr;  // pinned staging
     // state description
     bool have_state = false;
@@ -539,6 +565,11 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.fft_re = s->fft_re.as<double>();
     F.fft_im = s->fft_im.as<double>();
     F.ctl = s->ctl.as<Ctl>();
+    F.prof = nullptr;
+    if (s->profile) {
+        CUDA_TRY(s->prof.ensure(16ull * 128 * (std::max(max_iters, 1) + 1)));
+        F.prof = s->prof.as<unsigned long long>();
+    }
     F.diag = s->diag.as<StepDiagDev>();
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
@@ -551,10 +582,10 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
 }
 
 rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
-    Ctl* h = s->h_ctl;
-    std::memset(h, 0, sizeof(Ctl));
-    h->P = P_init;
-    CUDA_TRY(cudaMemcpyAsync(F.ctl, h, sizeof(Ctl), cudaMemcpyHostToDevice, s->stream));
+    // no host staging: back-to-back async launches must not race on it
+    F.P0 = P_init;
+    F.prof_cap = F.prof ? (uint32_t)(s->prof.cap / 16) : 0u;
+    CUDA_TRY(cudaMemsetAsync(F.ctl, 0, sizeof(Ctl), s->stream));
     CUDA_TRY(cudaMemsetAsync(F.diag, 0, sizeof(StepDiagDev) * std::max(F.cfg.max_iters, 1),
                              s->stream));
     void* args[] = {&F};
@@ -731,6 +762,25 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;
+    return RT3D_OK;
+}
+
+void* rt3d_session_stream(rt3d_session* s) { return s ? (void*)s->stream : nullptr; }
+
+rt3d_status rt3d_session_profile(rt3d_session* s, int enable) {
+    if (!s) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session");
+    s->profile = enable != 0;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_profile_copy(rt3d_session* s, uint64_t* pairs, uint32_t cap, uint32_t* n) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = read_ctl(s))) return st;
+    uint32_t k = std::min(cap, s->h_ctl->nprof);
+    if (k && pairs)
+        CUDA_TRY(cudaMemcpy(pairs, s->prof.p, 16ull * k, cudaMemcpyDeviceToHost));
+    if (n) *n = k;
     return RT3D_OK;
 }
 

@@ -63,6 +63,13 @@ enum Op : int {
     OP_CAND_B = 8,
 };
 
+// phase ids of the optional in-kernel timer (Frame::prof)
+enum Phase : int {
+    PH_INIT_PEAKS = 1, PH_SCAN = 2, PH_SPAWN = 3, PH_GRAD_T = 4, PH_CAND_T = 5, PH_APSS = 6,
+    PH_GRAD_R = 7, PH_CAND_R = 8, PH_KNN = 9, PH_PRUNE_A = 10, PH_PRUNE_B = 11, PH_GRAD_B = 12,
+    PH_CAND_B = 13, PH_FFT = 14,
+};
+
 struct BlockDiagDev {
     double step_used, nll_after_grad, nll_after_denoise;
     int32_t backtracks, pad_;
@@ -82,6 +89,7 @@ struct Ctl {
     double nll_cur, prev, init_nll, result, alpha, cmax;
     int rc_end, bc_end, sc_end, pad_;
     unsigned long long t_start, t_init, t_end;  // %globaltimer stamps (ns)
+    unsigned int nprof, prof_cap;
 };
 
 struct Cfg {
@@ -130,6 +138,8 @@ struct Frame {
     uint8_t* fl[2];
     uint32_t* bo[2];
     int tc0, rc0, bc0, sc0;  // initial buffer toggles
+    uint32_t P0;             // initial point count (resident state)
+    uint32_t prof_cap;
     // scratch
     double* gt;
     double* ct;
@@ -152,6 +162,7 @@ struct Frame {
     double* fft_re;   // 2*npix complex scratch (fft background mode)
     double* fft_im;
     // control / report
+    unsigned long long* prof;  // optional (id, %globaltimer) pairs after each barrier
     Ctl* ctl;
     StepDiagDev* diag;
     double* trace;

@@ -54,6 +54,9 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_session_create", _st, [C.c_int, P(SS)])
     _bind(L, "rt3d_session_destroy", _st, [SS])
     _bind(L, "rt3d_session_synchronize", _st, [SS])
+    _bind(L, "rt3d_session_stream", C.c_void_p, [SS])
+    _bind(L, "rt3d_session_profile", _st, [SS, C.c_int])
+    _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
@@ -90,7 +93,8 @@ def _check(status: int):
 
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
-    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_set_sensor", "rt3d_set_cube",
+    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
+    "rt3d_set_sensor", "rt3d_set_cube",
     "rt3d_reconstruct", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
@@ -158,6 +162,33 @@ class Session:
     def reconstruct_async(self, cfg: Config):
         self._cfg_c = cfg.to_c()
         _check(lib().rt3d_reconstruct(self.h, C.byref(self._cfg_c)))
+
+    @property
+    def stream_ptr(self) -> int:
+        return lib().rt3d_session_stream(self.h)
+
+    def profile(self, enable: bool = True):
+        _check(lib().rt3d_session_profile(self.h, int(enable)))
+
+    PHASES = {1: "init_peaks", 2: "init_scan", 3: "init_spawn", 4: "grad_t", 5: "cand_t",
+              6: "apss", 7: "grad_r", 8: "cand_r", 9: "knn", 10: "prune_a", 11: "prune_b",
+              12: "grad_b", 13: "cand_b", 14: "fft"}
+
+    def profile_phases(self):
+        """(name, duration_ns) per barrier-delimited phase of the last launch."""
+        cap = 1 << 16
+        buf = np.zeros(2 * cap, np.uint64)
+        n = C.c_uint32()
+        _check(lib().rt3d_profile_copy(self.h, ptr(buf, _u64), cap, C.byref(n)))
+        r = Report()
+        _check(lib().rt3d_report_info(self.h, C.byref(r)))
+        pairs = buf[: 2 * n.value].reshape(-1, 2)
+        out = []
+        prev = None
+        for pid, ts in pairs:
+            out.append((self.PHASES.get(int(pid), str(pid)), 0 if prev is None else int(ts) - prev))
+            prev = int(ts)
+        return out
 
     def synchronize(self):
         _check(lib().rt3d_session_synchronize(self.h))
