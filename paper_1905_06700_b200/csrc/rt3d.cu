@@ -19,6 +19,7 @@
 
 #include "../../include/rt3d.h"
 #include "rt3d_frame.cuh"
+#include "rt3d_nbr.cuh"
 
 using namespace rt3d;
 
@@ -43,7 +44,7 @@ __device__ __forceinline__ void gsync(cg::grid_group& grid, const Frame& F, int 
     }
 }
 
-template <int KIND>
+template <int KIND, int G>
 __device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc, int rc, int bc,
                           int sc, int op, int it) {
     while (!ld_cg(&F.ctl->done)) {
@@ -55,88 +56,127 @@ __device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc
         X.bc = bc;
         X.sc = sc;
         X.apply_floor = 0;
-        tree_sweep<KIND>(F, sm, X, op, it);
+        X.mig_cached = 0;
+        tree_sweep_g<KIND, G>(F, sm, grid, X, op, it);
         gsync(grid, F, KIND == K_CAND_T ? PH_CAND_T : KIND == K_CAND_R ? PH_CAND_R : PH_CAND_B);
     }
 }
 
-__global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
-    __shared__ Smem sm;
+enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
+
+template <int STAGE, int G>
+__global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it);
+
+__device__ __forceinline__ void stamp(const Frame& F, int phase) {
+    if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned int k = F.ctl->nprof;
+        if (k < F.ctl->prof_cap) {
+            F.prof[2 * k] = (unsigned long long)phase;
+            F.prof[2 * k + 1] = globaltimer();
+            F.ctl->nprof = k + 1;
+        }
+    }
+}
+
+// One stage of a frame: a cooperative kernel whose phases are separated by
+// grid barriers.  Buffer toggles live in Ctl between kernels; every block
+// reads them at entry, the leader writes them back at exit (after at least
+// one barrier, so no block still reads them).
+template <int STAGE, int G>
+__global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it) {
+    constexpr int stage = STAGE;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     cg::grid_group grid = cg::this_grid();
-    if (threadIdx.x == 0 && !F.irf_of_pix) sm.irf0 = F.irfs[0];
-    __syncthreads();
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     const int prog = F.cfg.program;
-    if (leader) {
-        // Ctl is zeroed by cudaMemsetAsync before the launch; nothing else
-        // reads these fields before the first grid barrier.
-        const unsigned long long t0 = globaltimer();
-        F.ctl->t_start = t0;
-        F.ctl->P = F.P0;
-        F.ctl->prof_cap = F.prof_cap;
-        if (F.prof && F.prof_cap) {
-            F.prof[0] = 0;
-            F.prof[1] = t0;
-            F.ctl->nprof = 1;
-        }
-    }
-
-    int tc = F.tc0, rc = F.rc0, bc = F.bc0, sc = F.sc0;
-    if (prog == PROG_RECON || prog == PROG_INIT || prog == PROG_BASELINE || prog == PROG_PEAKS) {
-        phase_init_peaks(F, sm);
-        gsync(grid, F, PH_INIT_PEAKS);
-        if (prog == PROG_PEAKS) return;
-        const bool baseline = prog == PROG_BASELINE;
-        const int s2 = F.s * F.s;
-        scan_stage_a(F, sm, [&](uint32_t p) {
-            uint32_t nv = F.nval[p];
-            return baseline ? (nv > 0 ? 1u : 0u) : nv * (uint32_t)s2;
-        });
-        gsync(grid, F, PH_SCAN);
-        phase_spawn(F, sm, baseline);
-        gsync(grid, F, PH_SPAWN);
-        tc = rc = bc = sc = 0;
-        if (prog != PROG_RECON) {
-            if (leader) {
-                F.ctl->tc_end = tc;
-                F.ctl->rc_end = rc;
-                F.ctl->bc_end = bc;
-                F.ctl->sc_end = sc;
-                F.ctl->t_end = globaltimer();
+    if (STAGE != ST_FIRST && ld_cg(&F.ctl->stop)) return;
+    if (!F.irf_of_pix) {  // shared IRF: tables in shared memory
+        const IrfDev f0 = F.irfs[0];
+        if (f0.n <= (uint32_t)kIrfSmem) {
+            for (uint32_t k = threadIdx.x; k < f0.n; k += kBlock) {
+                sm.irf_tab[k] = f0.s[k];
+                if (k + 1 < f0.n) sm.irf_tab[kIrfSmem + k] = f0.d[k];
             }
-            return;
+        }
+        if (threadIdx.x == 0) {
+            sm.irf0 = f0;
+            if (f0.n <= (uint32_t)kIrfSmem) {
+                sm.irf0.s = sm.irf_tab;
+                sm.irf0.d = sm.irf_tab + kIrfSmem;
+            }
         }
     }
-    if (leader) F.ctl->t_init = globaltimer();
-
+    __syncthreads();
+    int tc, rc, bc, sc;
+    if (stage == ST_FIRST) {
+        tc = F.tc0;
+        rc = F.rc0;
+        bc = F.bc0;
+        sc = F.sc0;
+        if (leader) {
+            // Ctl was zeroed by cudaMemsetAsync; nothing else reads these
+            // before the first barrier.
+            const unsigned long long t0 = globaltimer();
+            F.ctl->t_start = t0;
+            F.ctl->P = F.P0;
+            F.ctl->prof_cap = F.prof_cap;
+            if (F.prof && F.prof_cap) {
+                F.prof[0] = 0;
+                F.prof[1] = t0;
+                F.ctl->nprof = 1;
+            }
+        }
+    } else {
+        tc = ld_cg(&F.ctl->tc);
+        rc = ld_cg(&F.ctl->rc);
+        bc = ld_cg(&F.ctl->bc);
+        sc = ld_cg(&F.ctl->sc);
+        stamp(F, stage == ST_INTENSITY ? PH_APSS : stage == ST_TAIL ? PH_KNN : PH_LAUNCH);
+    }
     SweepCtx X0;
     X0.alpha = 0.0;
     X0.cfloor = 0.0;
-    X0.tc = tc;
-    X0.rc = rc;
-    X0.bc = bc;
-    X0.sc = sc;
     X0.apply_floor = 0;
+    X0.mig_cached = 0;
 
-    if (prog == PROG_NLL) {
-        tree_sweep<K_NLL>(F, sm, X0, OP_RESULT, 0);
-        return;
-    }
-    if (prog == PROG_GRADS) {
-        tree_sweep<K_GRAD_T>(F, sm, X0, OP_RESULT, 0);
-        gsync(grid, F, PH_GRAD_T);
-        tree_sweep<K_GRAD_R>(F, sm, X0, OP_RESULT, 0);
-        gsync(grid, F, PH_GRAD_R);
-        tree_sweep<K_GRAD_B>(F, sm, X0, OP_RESULT, 0);
-        return;
-    }
-
-    // ---- PALM iterations (reconstruct.hpp:300-435, 466-478) ----
-    tree_sweep<K_GRAD_T>(F, sm, X0, OP_GRAD_T_FIRST, 0);
-    gsync(grid, F, PH_GRAD_T);
-    const uint32_t nth = gridDim.x * kBlock;
-    const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
-    for (int it = 0; it < F.cfg.max_iters; ++it) {
+    if constexpr (STAGE == ST_FIRST) {
+        if (prog == PROG_RECON || prog == PROG_INIT || prog == PROG_BASELINE ||
+            prog == PROG_PEAKS) {
+            phase_init_peaks(F, sm);
+            gsync(grid, F, PH_INIT_PEAKS);
+            if (prog == PROG_PEAKS) return;
+            const bool baseline = prog == PROG_BASELINE;
+            const int s2 = F.s * F.s;
+            scan_stage_a(F, sm, [&](uint32_t p) {
+                uint32_t nv = F.nval[p];
+                return baseline ? (nv > 0 ? 1u : 0u) : nv * (uint32_t)s2;
+            });
+            gsync(grid, F, PH_SCAN);
+            phase_spawn(F, sm, baseline);
+            gsync(grid, F, PH_SPAWN);
+            tc = rc = bc = sc = 0;
+        }
+        if (leader) F.ctl->t_init = globaltimer();
+        X0.tc = tc;
+        X0.rc = rc;
+        X0.bc = bc;
+        X0.sc = sc;
+        if (prog == PROG_NLL) {
+            tree_sweep_g<K_NLL, G>(F, sm, grid, X0, OP_RESULT, 0);
+        } else if (prog == PROG_GRADS) {
+            tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X0, OP_RESULT, 0);
+            gsync(grid, F, PH_GRAD_T);
+            tree_sweep_g<K_GRAD_R, G>(F, sm, grid, X0, OP_RESULT, 0);
+            gsync(grid, F, PH_GRAD_R);
+            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X0, OP_RESULT, 0);
+        } else if (prog == PROG_RECON || prog == PROG_PALM) {
+            // nll at the initial state + depth gradients (reconstruct.hpp:466)
+            tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X0, OP_GRAD_T_FIRST, 0);
+            gsync(grid, F, PH_GRAD_T);
+        }
+    } else if constexpr (STAGE == ST_DEPTH) {
+        // depth block, reconstruct.hpp:320-350: safeguarded gradient step
         const uint32_t P = ld_cg(&F.ctl->P);
         if (leader) {
             StepDiagDev& d = F.diag[it];
@@ -148,24 +188,30 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             }
         }
         if (P > 0) {
-            // depth block: safeguarded step, APSS, pin
-            cand_loop<K_CAND_T>(F, sm, grid, tc, rc, bc, sc, OP_CAND_T, it);
+            cand_loop<K_CAND_T, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_T, it);
             if (ld_cg(&F.ctl->accept)) tc ^= 1;
-            phase_apss(F, tc, sc, P);
-            gsync(grid, F, PH_APSS);
+        }
+    } else if constexpr (STAGE == ST_INTENSITY) {
+        // APSS wrote t[tc^1] (apss_kernel); intensity block, :371-392
+        const uint32_t P = ld_cg(&F.ctl->P);
+        if (P > 0) {
             tc ^= 1;
             SweepCtx X = X0;
             X.tc = tc;
             X.rc = rc;
             X.bc = bc;
             X.sc = sc;
-            tree_sweep<K_GRAD_R>(F, sm, X, OP_GRAD_R, it);
+            tree_sweep_g<K_GRAD_R, G>(F, sm, grid, X, OP_GRAD_R, it);
             gsync(grid, F, PH_GRAD_R);
-            // intensity block: safeguarded step, kNN filter, prune
-            cand_loop<K_CAND_R>(F, sm, grid, tc, rc, bc, sc, OP_CAND_R, it);
+            cand_loop<K_CAND_R, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_R, it);
             if (ld_cg(&F.ctl->accept)) rc ^= 1;
-            phase_knn(F, tc, rc, sc, P);
-            gsync(grid, F, PH_KNN);
+        }
+    } else if constexpr (STAGE == ST_TAIL) {
+        // kNN wrote r[rc^1] (knn_kernel); prune + refresh (:395-397), then
+        // the background block (:405-429) and the nll that ends the iteration
+        const uint32_t P = ld_cg(&F.ctl->P);
+        SweepCtx X = X0;
+        if (P > 0) {
             rc ^= 1;
             phase_prune_a(F, sm, rc, sc);
             gsync(grid, F, PH_PRUNE_A);
@@ -176,17 +222,23 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             sc ^= 1;
             X.tc = tc;
             X.rc = rc;
+            X.bc = bc;
             X.sc = sc;
-            tree_sweep<K_GRAD_B>(F, sm, X, OP_GRAD_B_PRUNED, it);
+            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X, OP_GRAD_B_PRUNED, it);
             gsync(grid, F, PH_GRAD_B);
         } else {
-            tree_sweep<K_GRAD_B>(F, sm, X0, OP_GRAD_B_EMPTY, it);
+            X.tc = tc;
+            X.rc = rc;
+            X.bc = bc;
+            X.sc = sc;
+            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X, OP_GRAD_B_EMPTY, it);
             gsync(grid, F, PH_GRAD_B);
         }
-        // background block: safeguarded step, FFT low-pass, floor
-        cand_loop<K_CAND_B>(F, sm, grid, tc, rc, bc, sc, OP_CAND_B, it);
+        cand_loop<K_CAND_B, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_B, it);
         if (ld_cg(&F.ctl->accept)) bc ^= 1;
         if (F.cfg.bg_mode == 1) {
+            const uint32_t nth = gridDim.x * kBlock;
+            const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
             const int nr = F.rows, nc = F.cols;
             double* re = F.fft_re;
             double* im = F.fft_im;
@@ -201,25 +253,35 @@ __global__ void __launch_bounds__(kBlock) frame_kernel(Frame F) {
             fft_stage4(re, im, F.b[bc], nr, nc, 1, gtid, nth);
             gsync(grid, F, PH_FFT);
         }
-        SweepCtx X = X0;
-        X.tc = tc;
-        X.rc = rc;
         X.bc = bc;
-        X.sc = sc;
         X.apply_floor = 1;
-        tree_sweep<K_GRAD_T>(F, sm, X, OP_GRAD_T_END, it);
+        // t unchanged since GRAD_R (APSS output): mass_in_gate is cached,
+        // unless the cloud was empty (no GRAD_R ran)
+        X.mig_cached = ld_cg(&F.ctl->P) > 0 ? 1 : 0;
+        tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X, OP_GRAD_T_END, it);
         gsync(grid, F, PH_GRAD_T);
-        X0 = X;
-        X0.apply_floor = 0;
-        if (ld_cg(&F.ctl->stop)) break;
     }
     if (leader) {
-        F.ctl->tc_end = tc;
-        F.ctl->rc_end = rc;
-        F.ctl->bc_end = bc;
-        F.ctl->sc_end = sc;
+        F.ctl->tc = tc;
+        F.ctl->rc = rc;
+        F.ctl->bc = bc;
+        F.ctl->sc = sc;
         F.ctl->t_end = globaltimer();
     }
+}
+
+__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop)) return;
+    stamp(F, PH_LAUNCH);
+    apss_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw));
+}
+
+__global__ void __launch_bounds__(kNbrBlock, 4) knn_kernel(Frame F) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop)) return;
+    stamp(F, PH_LAUNCH);
+    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw));
 }
 
 // ---------------------------------------------------------------------------
@@ -417,7 +479,8 @@ struct rt3d_session {
     int device = 0;
     int nsm = 0;
     cudaStream_t stream = nullptr;
-    int grid_frame = 0;  // cooperative grid of frame_kernel
+    int grid_frame = 0;  // cooperative grid of stage_kernel
+    int grid_apss = 0, grid_knn = 0;
     int grid_fft = 0;
     // sensor
     bool have_sensor = false;
@@ -433,7 +496,7 @@ struct rt3d_session {
     // state
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
-    DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot;
+    DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot, part, mig[2];
     DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im;
     DevBuf ctl, diag, trace, outpts, misc, prof;
     bool profile = false;
@@ -445,6 +508,7 @@ struct rt3d_session {
     uint32_t P = 0;
     int tc = 0, rc = 0, bc = 0, sc = 0;
     std::vector<uint32_t> perm;  // device order -> caller's cloud order (nll/grads API)
+    uint32_t max_pts_per_pixel = 0;
     // last reconstruct report
     int iterations = 0;
     int report_iters_cap = 0;
@@ -476,6 +540,8 @@ rt3d_status ensure_state(rt3d_session* s, size_t pcap, size_t npix) {
         CUDA_TRY(s->b[k].ensure(npix * 8));
         CUDA_TRY(s->bo[k].ensure((npix + 1) * 4));
     }
+    CUDA_TRY(s->mig[0].ensure(pc * 8));
+    CUDA_TRY(s->mig[1].ensure(pc * 8));
     CUDA_TRY(s->gt.ensure(pc * 8));
     CUDA_TRY(s->ct.ensure(pc * 8));
     CUDA_TRY(s->gr.ensure(pc * 8));
@@ -515,8 +581,11 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.wpb = 1 << (F.G - F.Gb);
     F.nbn = 1u << F.Gb;
     // scratch
-    CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 8));
+    CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 32));
+    F.nev = s->n_events;
     CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
+    CUDA_TRY(s->part.ensure((size_t)npix * 8));
+    F.part = s->part.as<double>();
     CUDA_TRY(s->bmax.ensure((size_t)s->grid_frame * 8));
     CUDA_TRY(s->cnt.ensure((size_t)npix * 4));
     CUDA_TRY(s->btot.ensure((size_t)s->grid_frame * 4));
@@ -544,6 +613,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         F.fl[k] = s->fl[k].as<uint8_t>();
         F.bo[k] = s->bo[k].as<uint32_t>();
     }
+    F.mig[0] = s->mig[0].as<double>();
+    F.mig[1] = s->mig[1].as<double>();
     F.gt = s->gt.as<double>();
     F.ct = s->ct.as<double>();
     F.gr = s->gr.as<double>();
@@ -574,11 +645,32 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
     F.cfg.max_iters = max_iters;
+    // lanes per pixel for the likelihood sweeps: 4 for sparse pixels (a few
+    // events, <= 4 points), a warp otherwise
+    {
+        const uint32_t mpp = std::max<uint32_t>(s->max_pts_per_pixel, 1);
+        const double mean_ev = npix ? (double)s->n_events / npix : 0.0;
+        if (mpp > (uint32_t)kPvc)
+            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: more than %d points in one pixel", kPvc);
+        F.cfg.gsz = (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) ? 4 : 32;
+    }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
     F.bc0 = s->bc;
     F.sc0 = s->sc;
     return RT3D_OK;
+}
+
+using StageFn = void (*)(Frame, int);
+// [config][stage]; config 0: 4 lanes per pixel, 1: a warp per pixel
+static StageFn stage_fn(int cfgi, int st) {
+    static StageFn tab[2][4] = {
+        {stage_kernel<ST_FIRST, 4>, stage_kernel<ST_DEPTH, 4>, stage_kernel<ST_INTENSITY, 4>,
+         stage_kernel<ST_TAIL, 4>},
+        {stage_kernel<ST_FIRST, 32>, stage_kernel<ST_DEPTH, 32>, stage_kernel<ST_INTENSITY, 32>,
+         stage_kernel<ST_TAIL, 32>},
+    };
+    return tab[cfgi][st];
 }
 
 rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
@@ -588,9 +680,29 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
     CUDA_TRY(cudaMemsetAsync(F.ctl, 0, sizeof(Ctl), s->stream));
     CUDA_TRY(cudaMemsetAsync(F.diag, 0, sizeof(StepDiagDev) * std::max(F.cfg.max_iters, 1),
                              s->stream));
-    void* args[] = {&F};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)frame_kernel, dim3(s->grid_frame),
-                                         dim3(kBlock), args, 0, s->stream));
+    // the frame as a stream-ordered kernel sequence; every decision stays on
+    // the device (Ctl), so nothing here waits for the GPU
+    const int cfgi = F.cfg.gsz == 4 ? 0 : 1;
+    auto stage = [&](int st, int it) -> rt3d_status {
+        void* args[] = {&F, &it};
+        CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st), dim3(s->grid_frame),
+                                             dim3(kBlock), args, sizeof(Smem), s->stream));
+        return RT3D_OK;
+    };
+    rt3d_status st;
+    if ((st = stage(ST_FIRST, 0))) return st;
+    const int prog = F.cfg.program;
+    if (prog == PROG_RECON || prog == PROG_PALM) {
+        for (int it = 0; it < F.cfg.max_iters; ++it) {
+            if ((st = stage(ST_DEPTH, it))) return st;
+            apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+            CUDA_TRY(cudaGetLastError());
+            if ((st = stage(ST_INTENSITY, it))) return st;
+            knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
+            CUDA_TRY(cudaGetLastError());
+            if ((st = stage(ST_TAIL, it))) return st;
+        }
+    }
     return RT3D_OK;
 }
 
@@ -664,9 +776,6 @@ rt3d_status require_device(rt3d_session* s) {
 // window half-width for the pinned neighbourhood search
 int window_w(double R, double pitch) { return (int)std::floor(R / pitch) + 1; }
 
-}  // namespace
-
-namespace {
 template <typename T>
 rt3d_status copy_per_point(rt3d_session* s, T* out, const void* dev) {
     if (!out || !s->P) return RT3D_OK;
@@ -718,10 +827,33 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     s->nsm = prop.multiProcessorCount;
     CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, frame_kernel, kBlock, 0));
+    per_sm = 1 << 30;
+    for (int c = 0; c < 2; ++c)
+        for (int st = 0; st < 4; ++st) {
+            int b = 0;
+            CUDA_TRY(cudaFuncSetAttribute((const void*)stage_fn(c, st),
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(Smem)));
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                &b, (const void*)stage_fn(c, st), kBlock, sizeof(Smem)));
+            per_sm = std::min(per_sm, b);
+        }
+    {
+        int a = 0, k = 0;
+        CUDA_TRY(cudaFuncSetAttribute(apss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(ApssWarpSm) * kNbrWarps)));
+        CUDA_TRY(cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(KnnWarpSm) * kNbrWarps)));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, apss_kernel, kNbrBlock,
+                                                               sizeof(ApssWarpSm) * kNbrWarps));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, knn_kernel, kNbrBlock,
+                                                               sizeof(KnnWarpSm) * kNbrWarps));
+        s->grid_apss = prop.multiProcessorCount * std::max(a, 1);
+        s->grid_knn = prop.multiProcessorCount * std::max(k, 1);
+    }
     if (per_sm < 1) {
         delete s;
-        return fail(RT3D_ERR_CUDA, "rt3d: frame kernel does not fit on an SM");
+        return fail(RT3D_ERR_CUDA, "rt3d: stage kernel does not fit on an SM");
     }
     const char* env = getenv("RT3D_BLOCKS_PER_SM");
     int want = env ? atoi(env) : 1;
@@ -742,11 +874,13 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
     DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
-                      &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk,
+                      &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk, &s->part,
                       &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
                       &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->ctl, &s->diag,
                       &s->trace, &s->outpts, &s->misc};
     for (DevBuf* b : bufs) b->release();
+    s->mig[0].release();
+    s->mig[1].release();
     for (int k = 0; k < 2; ++k) {
         s->t[k].release();
         s->r[k].release();
@@ -841,6 +975,11 @@ rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* v) {
         d.tau_max = f.tau_min + f.dtau * (double)(f.n_samples - 1);
         d.h_max = hmax;
         d.n = (uint32_t)f.n_samples;
+        int ex = 0;
+        const double mant = std::frexp(f.dtau, &ex);
+        d.pow2 = (mant == 0.5) ? 1u : 0u;
+        d.inv_dtau = d.pow2 ? std::ldexp(1.0, 1 - ex) : 0.0;
+        d.lim = (double)(f.n_samples - 2);
         o += 2 * f.n_samples;
     }
     CUDA_TRY(s->irf_tab.ensure(total * 8));
@@ -930,6 +1069,7 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     if ((st = ensure_state(s, pcap, npix))) return st;
     g.W = window_w(cfg->apss.kernel_radius, s->pitch);
     g.set_oog_flags = 1;
+    s->max_pts_per_pixel = program == PROG_BASELINE ? 1u : (uint32_t)cfg->init.max_returns * s->s * s->s;
     s->tc = s->rc = s->bc = s->sc = 0;
     Frame F;
     if ((st = build_frame(s, F, g, program == PROG_RECON ? cfg->max_iters : 1))) return st;
@@ -952,10 +1092,10 @@ static rt3d_status resolve_state(rt3d_session* s) {
     if (st) return st;
     const Ctl& c = *s->h_ctl;
     s->P = c.P;
-    s->tc = c.tc_end;
-    s->rc = c.rc_end;
-    s->bc = c.bc_end;
-    s->sc = c.sc_end;
+    s->tc = c.tc;
+    s->rc = c.rc;
+    s->bc = c.bc;
+    s->sc = c.sc;
     s->iterations = c.iterations;
     return RT3D_OK;
 }
@@ -1095,6 +1235,9 @@ rt3d_status rt3d_state_upload(rt3d_session* s, const rt3d_state_view* v) {
     }
     bool identity = true;
     for (size_t k = 0; k < n && identity; ++k) identity = order[k] == k;
+    uint32_t maxpp = 0;
+    for (size_t p = 0; p < npix; ++p) maxpp = std::max(maxpp, counts[p]);
+    s->max_pts_per_pixel = maxpp;
     bool pinned = true;
     std::vector<double> t(n), r(n);
     std::vector<uint32_t> pix(n);

@@ -30,6 +30,7 @@ constexpr int kLamCap = 16;        // per-lane rate slots kept in shared memory
 constexpr int kTopSmem = 4096;     // top-of-tree values reduced in shared memory
 constexpr int kMaxReturns = 16;    // InitParams::max_returns supported on device
 constexpr int kKnnFast = 32;       // knn_k handled with an in-register top-k list
+constexpr int kIrfSmem = 256;      // shared IRF samples kept in shared memory
 
 enum Program : int {
     PROG_RECON = 0,   // reconstruct (reconstruct.hpp:457-489)
@@ -67,7 +68,7 @@ enum Op : int {
 enum Phase : int {
     PH_INIT_PEAKS = 1, PH_SCAN = 2, PH_SPAWN = 3, PH_GRAD_T = 4, PH_CAND_T = 5, PH_APSS = 6,
     PH_GRAD_R = 7, PH_CAND_R = 8, PH_KNN = 9, PH_PRUNE_A = 10, PH_PRUNE_B = 11, PH_GRAD_B = 12,
-    PH_CAND_B = 13, PH_FFT = 14,
+    PH_CAND_B = 13, PH_FFT = 14, PH_LAUNCH = 15,
 };
 
 struct BlockDiagDev {
@@ -85,11 +86,11 @@ struct Ctl {
     unsigned int P;        // current point count
     int iterations;
     int stop;
-    int done, accept, bt, tc_end;
+    int done, accept, bt, pad0_;
     double nll_cur, prev, init_nll, result, alpha, cmax;
-    int rc_end, bc_end, sc_end, pad_;
     unsigned long long t_start, t_init, t_end;  // %globaltimer stamps (ns)
     unsigned int nprof, prof_cap;
+    int tc, rc, bc, sc;    // current buffer of t, r, b and the point structure
 };
 
 struct Cfg {
@@ -110,6 +111,7 @@ struct Cfg {
     double thr;
     int W;             // fine-pixel window half-width floor(R/pitch)+1
     int set_oog_flags; // palm: OR out-of-gate into flags
+    int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };
 
 struct Frame {
@@ -123,6 +125,7 @@ struct Frame {
     const uint8_t* dead;
     // cube
     uint32_t npix;
+    uint64_t nev;      // events (E)
     const uint32_t* off;
     const uint2* ev;
     // pairwise tree geometry over pixels
@@ -141,6 +144,7 @@ struct Frame {
     uint32_t P0;             // initial point count (resident state)
     uint32_t prof_cap;
     // scratch
+    double* mig[2];   // per point mass_in_gate(t) of the current t (see SweepCtx)
     double* gt;
     double* ct;
     double* gr;
@@ -148,7 +152,9 @@ struct Frame {
     double* gb;
     double* cb;
     uint8_t* oog;
-    double* lam;      // E rate slots for pixels above kLamCap events
+    double* lam;      // 4*E per-event slots (rate + 3 terms) for pixels above
+                      // the lane group's shared-memory capacity
+    double* part;     // npix per-pixel nll partials (sweep -> tree reduction)
     double* blk;      // nbn block-node sums
     double* bmax;     // gridDim block maxima
     uint32_t* cnt;    // npix prefix scratch
@@ -169,17 +175,39 @@ struct Frame {
     Cfg cfg;
 };
 
+// Likelihood sweep staging: a warp owns a tree node of <= 32 consecutive
+// pixels; their events and points are contiguous CSR ranges, copied into
+// shared memory with coalesced loads in batches of <= kEvc events and
+// <= kPvc points, then processed by lane groups (one pixel per group).
+constexpr int kEvc = 256;
+constexpr int kPvc = 128;
+struct WarpSweepSm {
+    uint2 ev[kEvc];
+    double lam[kEvc], tn[kEvc], t1[kEvc], t2[kEvc];
+    double pt[kPvc], pr[kPvc], pmig[kPvc];
+    int2 plh[kPvc];
+    uint32_t me0[32], mm[32], mn0[32], mnp[32];
+    double mb[32], mgain[32];
+    uint32_t mdead[32];
+    double vals[32];
+};
+struct SweepSmem {
+    WarpSweepSm w[kWarps];
+};
+
 struct Smem {
-    double lam[kWarps][kLamCap][32];  // reused as the top-of-tree array
-    double vals[kWarps][32];
+    union {
+        SweepSmem sw;
+    } u;
     double node[kWarps];
     double wmax[kWarps];
     unsigned int scan[kWarps + 1];
     int is_last;
     IrfDev irf0;
+    double irf_tab[2 * kIrfSmem];
 };
-static_assert(sizeof(double) * kWarps * kLamCap * 32 >= sizeof(double) * kTopSmem,
-              "top-of-tree array must fit in the rate slots");
+static_assert(sizeof(SweepSmem) >= sizeof(double) * kTopSmem,
+              "top-of-tree array must fit in the sweep staging");
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -466,181 +494,350 @@ struct SweepCtx {
     double cfloor;   // 1e-3 * max(curv) + 1e-30 (reconstruct.hpp:315)
     int tc, rc, bc, sc;
     int apply_floor; // background floor of reconstruct.hpp:427 before the sweep
+    int mig_cached;  // mass_in_gate(t) of the current t is in F.mig[sc]
 };
 
-template <int KIND>
-__device__ __forceinline__ double sweep_pixel(const Frame& F, const Smem& sm, const SweepCtx& X,
-                                              uint32_t p, double* lam_s, double& cmax) {
-    const uint32_t e0 = F.off[p], e1 = F.off[p + 1], m = e1 - e0;
-    const uint32_t* bo = F.bo[X.sc];
-    const uint32_t n0 = bo[p], n1 = bo[p + 1];
-    const bool dead = F.dead[p] != 0;
-    const double gain = F.gain[p];
+// Irf::value / deriv (sensor.hpp:69-82), branch-free so that independent
+// evaluations overlap: for in-range tau, x >= 0 and
+// min((size_t)x, n-2) == min(trunc(x), n-2) as a double, so the segment and
+// the fraction x - k are bit-identical to the reference's; out-of-range taus
+// read a clamped segment and are discarded by the final select.
+__device__ __forceinline__ double irf_value_fast(const IrfDev& f, double tau) {
+    const bool in = (tau >= f.tau_min) && (tau <= f.tau_max);
+    const double x = irf_x(f, tau);
+    const double kd = fmax(fmin(trunc(x), f.lim), 0.0);
+    const uint32_t k = __double2uint_rz(kd);
+    const double fr = x - kd;
+    const double s0 = f.s[k], s1 = f.s[k + 1];
+    const double v = s0 + fr * (s1 - s0);
+    return in ? v : 0.0;
+}
+__device__ __forceinline__ double irf_deriv_fast(const IrfDev& f, double tau) {
+    const bool in = (tau > f.tau_min) && (tau < f.tau_max);
+    const double x = irf_x(f, tau);
+    const double kd = fmax(fmin(trunc(x), f.lim), 0.0);
+    const double v = f.d[__double2uint_rz(kd)];
+    return in ? v : 0.0;
+}
+// sum of -deriv over the support bins (likelihood.hpp:205), evaluations
+// independent, subtraction sequential
+__device__ __forceinline__ double neg_deriv_sum(const IrfDev& f, double t, int lo, int hi) {
+    double acc = 0.0;
+    int b = lo;
+    for (; b + 3 <= hi; b += 4) {
+        const double v0 = irf_deriv_fast(f, (double)b - t);
+        const double v1 = irf_deriv_fast(f, (double)(b + 1) - t);
+        const double v2 = irf_deriv_fast(f, (double)(b + 2) - t);
+        const double v3 = irf_deriv_fast(f, (double)(b + 3) - t);
+        acc -= v0;
+        acc -= v1;
+        acc -= v2;
+        acc -= v3;
+    }
+    for (; b <= hi; ++b) acc -= irf_deriv_fast(f, (double)b - t);
+    return acc;
+}
+// mass_in_gate, sensor.hpp:93-98: evaluations independent, sum sequential
+__device__ __forceinline__ double mig_fast(const IrfDev& f, double t, int lo, int hi) {
+    double m = 0.0;
+    int b = lo;
+    for (; b + 3 <= hi; b += 4) {
+        const double v0 = irf_value_fast(f, (double)b - t);
+        const double v1 = irf_value_fast(f, (double)(b + 1) - t);
+        const double v2 = irf_value_fast(f, (double)(b + 2) - t);
+        const double v3 = irf_value_fast(f, (double)(b + 3) - t);
+        m += v0;
+        m += v1;
+        m += v2;
+        m += v3;
+    }
+    for (; b <= hi; ++b) m += irf_value_fast(f, (double)b - t);
+    return m;
+}
+
+// first event index (relative) with bin >= key, over the pixel's events
+__device__ __forceinline__ uint32_t first_event_ge(const uint2* ev, uint32_t e0, uint32_t m,
+                                                   uint32_t key) {
+    return lower_bound_bin(ev, e0, e0 + m, key) - e0;
+}
+
+// Likelihood sweep of one staged pixel by a group of G lanes
+// (likelihood.hpp:100-333).  Lanes compute per-event terms in parallel; every
+// sum the reference forms sequentially is accumulated by one lane in the
+// reference's order.  Returns the pixel's nll partial on the group leader.
+template <int KIND, int G>
+__device__ __forceinline__ double sweep_staged_pixel(const Frame& F, WarpSweepSm& W,
+                                                     const SweepCtx& X, const IrfDev& f, int q,
+                                                     const uint2* EV, double* LAM, double* TN,
+                                                     double* T1, double* T2, uint32_t pbase,
+                                                     int gl, unsigned gmask, double& cmax) {
+    const uint32_t m = W.mm[q];
+    const uint32_t np = W.mnp[q];
+    const bool dead = W.mdead[q] != 0;
+    const double gain = W.mgain[q];
     const double g = dead ? 0.0 : gain;
-    const IrfDev& f = pixel_irf(F, sm, p);
+    const double b = W.mb[q];
     const int T = F.bins;
-
-    // background value (current, candidate, or floored current)
-    double b;
-    if (KIND == K_CAND_B) {
-        double dir = F.gb[p];
-        if (F.cfg.step_auto[2]) dir = dir / (F.cb[p] + X.cfloor);
-        b = std_max(0.0, F.b[X.bc][p] - X.alpha * dir);
-        F.b[X.bc ^ 1][p] = b;
-    } else {
-        b = F.b[X.bc][p];
-        if (X.apply_floor) {
-            b = (b < kBackgroundFloor) ? kBackgroundFloor : b;
-            F.b[X.bc][p] = b;
-        }
-    }
-
-    // candidate point values
-    const double* tsrc = F.t[X.tc];
-    const double* rsrc = F.r[X.rc];
-    if (KIND == K_CAND_T) {
-        double* to = F.t[X.tc ^ 1];
-        for (uint32_t n = n0; n < n1; ++n) {
-            double dir = F.gt[n];
-            if (F.cfg.step_auto[0]) dir = dir / (F.ct[n] + X.cfloor);
-            to[n] = std_clamp(tsrc[n] - X.alpha * dir, 0.0, F.tlim);
-        }
-        tsrc = to;
-    }
-    if (KIND == K_CAND_R) {
-        double* ro = F.r[X.rc ^ 1];
-        for (uint32_t n = n0; n < n1; ++n) {
-            double dir = F.gr[n];
-            if (F.cfg.step_auto[1]) dir = dir / (F.cr[n] + X.cfloor);
-            ro[n] = std_max(0.0, rsrc[n] - X.alpha * dir);
-        }
-        rsrc = ro;
-    }
+    const double* pt = W.pt + pbase;
+    const double* pr = W.pr + pbase;
+    const int2* plh = W.plh + pbase;
 
     // rates at the active bins (detail::active_rates, likelihood.hpp:100-121)
-    const bool in_smem = m <= (uint32_t)kLamCap;
-    double* lam = in_smem ? lam_s : (F.lam + e0);
-    const uint32_t ls = in_smem ? 32u : 1u;
-    {
-        const double l0 = (g == 0.0) ? 0.0 : g * b;
-        for (uint32_t k = 0; k < m; ++k) lam[k * ls] = l0;
+    for (uint32_t k = gl; k < m; k += G) {
+        const uint2 e = EV[k];
+        double l = 0.0;
         if (g != 0.0) {
-            for (uint32_t n = n0; n < n1; ++n) {
-                const double t = tsrc[n], gr_ = g * rsrc[n];
-                int lo, hi;
-                irf_support(f, t, T, lo, hi);
-                if (lo > hi) continue;
-                for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
-                    const uint32_t bin = __ldg(&F.ev[e0 + k].x);
-                    if (bin > (uint32_t)hi) break;
-                    lam[k * ls] += gr_ * irf_value(f, (double)bin - t);
-                }
+            l = g * b;
+            for (uint32_t qq = 0; qq < np; ++qq) {
+                const int2 lh = plh[qq];
+                if ((int)e.x >= lh.x && (int)e.x <= lh.y)
+                    l += g * pr[qq] * irf_value_fast(f, (double)e.x - pt[qq]);
             }
         }
+        LAM[k] = l;
+        const double z = (double)e.y;
+        TN[k] = (l > 0.0) ? z * log(l) : 0.0;
+        if (KIND == K_GRAD_B) {
+            T1[k] = g * z / l;
+            T2[k] = g * g * z / (l * l);
+        }
     }
+    __syncwarp(gmask);
 
+    // nll partial, likelihood.hpp:141-165 (leader, reference order)
     double part = 0.0;
-    if (!dead) {  // nll, likelihood.hpp:141-165
+    if (gl == 0 && !dead) {
         double mass = T * b;
-        for (uint32_t n = n0; n < n1; ++n) mass += rsrc[n] * irf_mass_in_gate(f, tsrc[n], T);
+        for (uint32_t qq = 0; qq < np; ++qq) mass += pr[qq] * W.pmig[pbase + qq];
         double acc = gain * mass;
         for (uint32_t k = 0; k < m; ++k) {
-            const double l = lam[k * ls];
-            if (l <= 0.0) {
+            if (LAM[k] <= 0.0) {
                 acc = INFINITY;
                 break;
             }
-            acc -= (double)__ldg(&F.ev[e0 + k].y) * log(l);
+            acc -= TN[k];
         }
         part = acc;
     }
 
-    if (KIND == K_GRAD_T) {  // grad_depth + block_curvatures().depth
-        const bool skip = (n0 == n1) || g == 0.0;
-        for (uint32_t n = n0; n < n1; ++n) {
-            double gval = 0.0, st = 0.0;
+    if (KIND == K_GRAD_T || KIND == K_GRAD_R) {  // per point (owner lanes)
+        const bool skip = (np == 0) || g == 0.0;
+        const uint32_t n0 = W.mn0[q];
+        for (uint32_t k = gl; k < np; k += G) {
+            const uint32_t n = n0 + k;
+            double gval = 0.0, cv = 0.0;
             uint8_t og = 0;
             if (!skip) {
-                const double t = tsrc[n], r = rsrc[n];
-                int lo, hi;
-                irf_support(f, t, T, lo, hi);
-                if (lo > hi) {
-                    og = 1;
-                } else {
-                    const double grr = g * r;
-                    double acc = 0.0;
-                    for (int bb = lo; bb <= hi; ++bb) acc -= irf_deriv(f, (double)bb - t);
-                    for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
-                        const uint2 e = __ldg(&F.ev[e0 + k]);
-                        if (e.x > (uint32_t)hi) break;
-                        const double l = lam[k * ls];
-                        const double dv = irf_deriv(f, (double)e.x - t);
-                        if (l > 0.0) acc += dv * (double)e.y / l;
-                        if (!(l <= 0.0)) {  // likelihood.hpp:320
-                            const double zl2 = (double)e.y / (l * l);
-                            const double dh = grr * dv;
-                            st += dh * dh * zl2;
+                const double t = pt[k], r = pr[k];
+                const int2 lh = plh[k];
+                // first staged event with bin >= lo
+                uint32_t kk = 0;
+                if (lh.x <= lh.y)
+                    while (kk < m && EV[kk].x < (uint32_t)lh.x) ++kk;
+                if (KIND == K_GRAD_T) {  // grad_depth + curvature().depth
+                    if (lh.x > lh.y) {
+                        og = 1;
+                    } else {
+                        const double grr = g * r;
+                        double acc = 0.0;
+                        acc = neg_deriv_sum(f, t, lh.x, lh.y);
+                        for (; kk < m; ++kk) {
+                            const uint2 e = EV[kk];
+                            if (e.x > (uint32_t)lh.y) break;
+                            const double l = LAM[kk];
+                            const double dv = irf_deriv_fast(f, (double)e.x - t);
+                            if (l > 0.0) acc += dv * (double)e.y / l;
+                            if (!(l <= 0.0)) {  // likelihood.hpp:320
+                                const double zl2 = (double)e.y / (l * l);
+                                const double dh = grr * dv;
+                                cv += dh * dh * zl2;
+                            }
+                        }
+                        if (r != 0.0) gval = grr * acc;
+                    }
+                } else {  // grad_intensity + curvature().intensity
+                    double acc = W.pmig[pbase + k];
+                    if (lh.x <= lh.y) {
+                        for (; kk < m; ++kk) {
+                            const uint2 e = EV[kk];
+                            if (e.x > (uint32_t)lh.y) break;
+                            const double l = LAM[kk];
+                            const double hv = irf_value_fast(f, (double)e.x - t);
+                            if (l > 0.0) acc -= hv * (double)e.y / l;
+                            if (!(l <= 0.0)) {
+                                const double zl2 = (double)e.y / (l * l);
+                                const double h = g * hv;
+                                cv += h * h * zl2;
+                            }
                         }
                     }
-                    if (r != 0.0) gval = grr * acc;
+                    gval = g * acc;
                 }
             }
-            F.gt[n] = gval;
-            F.ct[n] = st;
-            F.oog[n] = og;
-            if (og && F.cfg.set_oog_flags) F.fl[X.sc][n] |= 2u;
-            cmax = std_max(cmax, st);
-        }
-    }
-    if (KIND == K_GRAD_R) {  // grad_intensity + block_curvatures().intensity
-        const bool skip = (n0 == n1) || g == 0.0;
-        for (uint32_t n = n0; n < n1; ++n) {
-            double gval = 0.0, sr = 0.0;
-            if (!skip) {
-                const double t = tsrc[n];
-                double acc = irf_mass_in_gate(f, t, T);
-                int lo, hi;
-                irf_support(f, t, T, lo, hi);
-                if (lo <= hi) {
-                    for (uint32_t k = lower_bound_bin(F.ev, e0, e1, (uint32_t)lo) - e0; k < m; ++k) {
-                        const uint2 e = __ldg(&F.ev[e0 + k]);
-                        if (e.x > (uint32_t)hi) break;
-                        const double l = lam[k * ls];
-                        const double hv = irf_value(f, (double)e.x - t);
-                        if (l > 0.0) acc -= hv * (double)e.y / l;
-                        if (!(l <= 0.0)) {  // likelihood.hpp:320
-                            const double zl2 = (double)e.y / (l * l);
-                            const double h = g * hv;
-                            sr += h * h * zl2;
-                        }
-                    }
-                }
-                gval = g * acc;
+            if (KIND == K_GRAD_T) {
+                F.gt[n] = gval;
+                F.ct[n] = cv;
+                F.oog[n] = og;
+                if (og && F.cfg.set_oog_flags) F.fl[X.sc][n] |= 2u;
+            } else {
+                F.gr[n] = gval;
+                F.cr[n] = cv;
             }
-            F.gr[n] = gval;
-            F.cr[n] = sr;
-            cmax = std_max(cmax, sr);
+            cmax = std_max(cmax, cv);
         }
     }
-    if (KIND == K_GRAD_B) {  // grad_background + block_curvatures().background
+    if (KIND == K_GRAD_B && gl == 0) {  // grad_background + curvature().background
         double gval = 0.0, bs = 0.0;
         if (g != 0.0) {
             double acc = g * T;
             for (uint32_t k = 0; k < m; ++k) {
-                const double l = lam[k * ls];
-                if (l > 0.0) {
-                    const double z = (double)__ldg(&F.ev[e0 + k].y);
-                    acc -= g * z / l;
-                    bs += g * g * z / (l * l);
+                if (LAM[k] > 0.0) {
+                    acc -= T1[k];
+                    bs += T2[k];
                 }
             }
             gval = acc;
         }
-        F.gb[p] = gval;
-        F.cb[p] = bs;
         cmax = std_max(cmax, bs);
+        // b and gain of pixel q are in registers: hand the results to the
+        // caller (which knows the pixel id) through the same slots
+        W.mb[q] = gval;
+        W.mgain[q] = bs;
     }
+    __syncwarp(gmask);
     return part;
+}
+
+// One warp processes tree node pixels [lo, lo+size): meta (lane per pixel),
+// then batches staged in shared memory, then lane groups per pixel.
+template <int KIND, int G>
+__device__ __forceinline__ void sweep_node(const Frame& F, Smem& sm, const SweepCtx& X,
+                                           uint32_t lo, uint32_t size, double& cmax) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    WarpSweepSm& W = sm.u.sw.w[warp];
+    const int gl = lane % G, grp = lane / G;
+    constexpr int NG = 32 / G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+    // ---- meta, lane per pixel
+    if ((uint32_t)lane < size) {
+        const uint32_t p = lo + lane;
+        const uint32_t e0 = F.off[p], e1 = F.off[p + 1];
+        const uint32_t* bo = F.bo[X.sc];
+        const uint32_t n0 = bo[p], n1 = bo[p + 1];
+        const bool dead = F.dead[p] != 0;
+        double b;
+        if (KIND == K_CAND_B) {
+            double dir = F.gb[p];
+            if (F.cfg.step_auto[2]) dir = dir / (F.cb[p] + X.cfloor);
+            b = std_max(0.0, F.b[X.bc][p] - X.alpha * dir);
+            F.b[X.bc ^ 1][p] = b;
+        } else {
+            b = F.b[X.bc][p];
+            if (X.apply_floor) {
+                b = (b < kBackgroundFloor) ? kBackgroundFloor : b;
+                F.b[X.bc][p] = b;
+            }
+        }
+        W.me0[lane] = e0;
+        W.mm[lane] = e1 - e0;
+        W.mn0[lane] = n0;
+        W.mnp[lane] = n1 - n0;
+        W.mb[lane] = b;
+        W.mgain[lane] = F.gain[p];
+        W.mdead[lane] = dead ? 1u : 0u;
+    }
+    __syncwarp();
+    const double* tcur = F.t[X.tc];
+    const double* rcur = F.r[X.rc];
+    for (uint32_t q0 = 0; q0 < size;) {
+        // batch [q0, q1): events <= kEvc and points <= kPvc (at least 1 pixel)
+        uint32_t q1 = q0, ne = 0, npt = 0;
+        while (q1 < size) {
+            const uint32_t a = W.mm[q1], c = W.mnp[q1];
+            if (q1 > q0 && (ne + a > (uint32_t)kEvc || npt + c > (uint32_t)kPvc)) break;
+            ne += a;
+            npt += c;
+            ++q1;
+        }
+        const bool ev_smem = ne <= (uint32_t)kEvc;
+        const uint32_t E0 = W.me0[q0], N0 = W.mn0[q0];
+        if (ev_smem)
+            for (uint32_t k = lane; k < ne; k += 32) W.ev[k] = __ldg(&F.ev[E0 + k]);
+        // points: candidate values, support, mass_in_gate (lane per point)
+        for (uint32_t k = lane; k < npt; k += 32) {
+            const uint32_t n = N0 + k;
+            uint32_t qk = q0;
+            if (F.irf_of_pix)
+                while (qk + 1 < q1 && W.mn0[qk + 1] - N0 <= k) ++qk;
+            const IrfDev& f = pixel_irf(F, sm, lo + qk);
+            double t = tcur[n], r = rcur[n];
+            if (KIND == K_CAND_T) {
+                double dir = F.gt[n];
+                if (F.cfg.step_auto[0]) dir = dir / (F.ct[n] + X.cfloor);
+                t = std_clamp(t - X.alpha * dir, 0.0, F.tlim);
+                F.t[X.tc ^ 1][n] = t;
+            }
+            if (KIND == K_CAND_R) {
+                double dir = F.gr[n];
+                if (F.cfg.step_auto[1]) dir = dir / (F.cr[n] + X.cfloor);
+                r = std_max(0.0, r - X.alpha * dir);
+                F.r[X.rc ^ 1][n] = r;
+            }
+            int plo, phi;
+            irf_support(f, t, F.bins, plo, phi);
+            W.pt[k] = t;
+            W.pr[k] = r;
+            W.plh[k] = make_int2(plo, phi);
+            // mass_in_gate(t): recomputed when t is a candidate or was just
+            // moved by APSS, else read back (t is unchanged since then)
+            constexpr bool kCompute = KIND == K_CAND_T || KIND == K_GRAD_R || KIND == K_NLL ||
+                                      KIND == K_GRAD_T;
+            double mg;
+            if (kCompute && !(KIND == K_GRAD_T && X.mig_cached)) {
+                mg = mig_fast(f, t, plo, phi);
+                if (KIND == K_GRAD_R) F.mig[X.sc][n] = mg;
+            } else {
+                mg = F.mig[X.sc][n];
+            }
+            W.pmig[k] = mg;
+        }
+        __syncwarp();
+        for (uint32_t qb = q0; qb < q1; qb += NG) {
+            const uint32_t q = qb + grp;
+            if (q < q1) {
+                const uint32_t eoff = W.me0[q] - E0;
+                const uint2* EV;
+                double *LAM, *TN, *T1, *T2;
+                if (ev_smem) {
+                    EV = W.ev + eoff;
+                    LAM = W.lam + eoff;
+                    TN = W.tn + eoff;
+                    T1 = W.t1 + eoff;
+                    T2 = W.t2 + eoff;
+                } else {  // a single pixel above kEvc events: global slots
+                    const uint32_t e0 = W.me0[q];
+                    EV = F.ev + e0;
+                    LAM = F.lam + e0;
+                    TN = F.lam + F.nev + e0;
+                    T1 = F.lam + 2 * F.nev + e0;
+                    T2 = F.lam + 3 * F.nev + e0;
+                }
+                const IrfDev& f = pixel_irf(F, sm, lo + q);
+                const double part = sweep_staged_pixel<KIND, G>(F, W, X, f, (int)q, EV, LAM, TN,
+                                                                T1, T2, W.mn0[q] - N0, gl, gmask,
+                                                                cmax);
+                if (gl == 0) {
+                    F.part[lo + q] = part;
+                    if (KIND == K_GRAD_B) {
+                        F.gb[lo + q] = W.mb[q];
+                        F.cb[lo + q] = W.mgain[q];
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        q0 = q1;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -739,7 +936,7 @@ __device__ void controller(const Frame& F, int op, int it, double v, double cmax
 // pairwise tree over the nbn block-node sums, in the last block
 __device__ double top_tree(const Frame& F, Smem& sm) {
     const uint32_t nb = F.nbn;
-    double* v = &sm.lam[0][0][0];
+    double* v = reinterpret_cast<double*>(&sm.u.sw);
     if (nb <= (uint32_t)kTopSmem) {
         for (uint32_t q = threadIdx.x; q < nb; q += kBlock) v[q] = ld_cg(&F.blk[q]);
         __syncthreads();
@@ -766,20 +963,44 @@ __device__ double top_tree(const Frame& F, Smem& sm) {
 // (parallel.hpp:52-61): warp = depth-G node (<= 32 pixels, one per lane),
 // block = depth-Gb node; the last block to finish reduces the top of the tree
 // and runs the controller.  Caller issues the grid barrier afterwards.
-template <int KIND>
-__device__ void tree_sweep(const Frame& F, Smem& sm, const SweepCtx& X, int op, int it) {
+template <int KIND, int G>
+__device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, const SweepCtx& X,
+                             int op, int it) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double cmax = 0.0;
-    double* lam_s = &sm.lam[warp][0][lane];
+    // phase 1: per-pixel partials, chunks of 32/G consecutive pixels per warp
+    // over the whole grid (all SMs busy regardless of the tree shape)
+    {
+        constexpr uint32_t NG = 32 / G;
+        const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+        const uint32_t nchunks = (F.npix + NG - 1) / NG;
+        for (uint32_t c = gw; c < nchunks; c += nw) {
+            const uint32_t lo = c * NG;
+            const uint32_t size = F.npix - lo < NG ? F.npix - lo : NG;
+            sweep_node<KIND, G>(F, sm, X, lo, size, cmax);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cmax = std_max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    if (lane == 0) sm.wmax[warp] = cmax;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bm = 0.0;
+        for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
+        F.bmax[blockIdx.x] = bm;
+    }
+    grid.sync();
+    // phase 2: pairwise_sum's tree over the partials (parallel.hpp:52-61):
+    // warp = depth-G node (<= 32 partials), block = depth-Gb node, the last
+    // block reduces the top and runs the controller
     for (uint32_t bn = blockIdx.x; bn < F.nbn; bn += gridDim.x) {
         if (warp < F.wpb) {
             uint32_t lo, size;
             tree_node_range(F.npix, F.G, bn * (uint32_t)F.wpb + warp, lo, size);
-            double part = 0.0;
-            if ((uint32_t)lane < size) part = sweep_pixel<KIND>(F, sm, X, lo + lane, lam_s, cmax);
-            sm.vals[warp][lane] = part;
+            double* v = sm.u.sw.w[warp].vals;
+            if ((uint32_t)lane < size) v[lane] = ld_cg(&F.part[lo + lane]);
             __syncwarp();
-            if (lane == 0) sm.node[warp] = pw32(sm.vals[warp], 0, (int)size);
+            if (lane == 0) sm.node[warp] = pw32(v, 0, (int)size);
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -791,15 +1012,7 @@ __device__ void tree_sweep(const Frame& F, Smem& sm, const SweepCtx& X, int op, 
         }
         __syncthreads();
     }
-    // block max of the curvature (order-free)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cmax = std_max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    if (lane == 0) sm.wmax[warp] = cmax;
-    __syncthreads();
     if (threadIdx.x == 0) {
-        double bm = 0.0;
-        for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
-        F.bmax[blockIdx.x] = bm;
         __threadfence();
         unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
         sm.is_last = (tk == gridDim.x - 1);
@@ -808,13 +1021,20 @@ __device__ void tree_sweep(const Frame& F, Smem& sm, const SweepCtx& X, int op, 
     if (!sm.is_last) return;
     __threadfence();
     double total = top_tree(F, sm);
+    double gm = 0.0;
+    for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) gm = std_max(gm, ld_cg(&F.bmax[b]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gm = std_max(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) sm.wmax[warp] = gm;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        double gm = 0.0;
-        for (uint32_t b = 0; b < gridDim.x; ++b) gm = std_max(gm, ld_cg(&F.bmax[b]));
+        gm = 0.0;
+        for (int w = 0; w < kWarps; ++w) gm = std_max(gm, sm.wmax[w]);
         F.ctl->ticket = 0;
         controller(F, op, it, total, gm);
     }
 }
+
 
 // ---------------------------------------------------------------------------
 // Neighbourhoods on the pinned fine grid.  Inside PALM every point sits at
@@ -933,23 +1153,6 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
     return true;
 }
 
-// APSS + pinning, reconstruct.hpp:355-363: t' = clamp(z'/bin_res)
-__device__ void phase_apss(const Frame& F, int tc, int sc, uint32_t P) {
-    const uint32_t nth = gridDim.x * kBlock;
-    for (uint32_t n = blockIdx.x * kBlock + threadIdx.x; n < P; n += nth) {
-        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
-        const double t = F.t[tc][n];
-        Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, t * F.bres};
-        uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
-        Pos o;
-        auto each = [&](double r2, auto fn) { for_each_pinned_neighbor(F, tc, sc, fi, fj, q, r2, fn); };
-        bool moved = apss_point(each, q, F.cfg.R, F.cfg.min_nbrs, F.cfg.eps, fl, o);
-        const double z = moved ? o.z : q.z;
-        F.t[tc ^ 1][n] = std_clamp(z / F.bres, 0.0, F.tlim);
-        F.fl[sc][n] = fl;
-    }
-}
-
 // top-k by (d^2, index), spatial_index.hpp:51-62, then the mean
 // (denoise.hpp:228-235)
 template <typename Enum, typename RFn>
@@ -1003,18 +1206,6 @@ __device__ __forceinline__ double knn_mean(Enum&& each, int k, double r2, double
     return acc / (double)cnt;
 }
 
-__device__ void phase_knn(const Frame& F, int tc, int rc, int sc, uint32_t P) {
-    const uint32_t nth = gridDim.x * kBlock;
-    const double R = F.cfg.R, r2 = R * R;
-    const double* rr = F.r[rc];
-    for (uint32_t n = blockIdx.x * kBlock + threadIdx.x; n < P; n += nth) {
-        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
-        Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
-        auto each = [&](double rr2, auto fn) { for_each_pinned_neighbor(F, tc, sc, fi, fj, q, rr2, fn); };
-        F.r[rc ^ 1][n] = knn_mean(each, F.cfg.knn_k, r2, rr[n], [&](uint32_t mm) { return rr[mm]; });
-    }
-}
-
 // prune (denoise.hpp:241-248) + SceneState::refresh (likelihood.hpp:38-55):
 // per-pixel survivor counts, grid scan, stable scatter into the other buffers
 __device__ void phase_prune_a(const Frame& F, Smem& sm, int rc, int sc) {
@@ -1047,6 +1238,7 @@ __device__ void phase_prune_b(const Frame& F, Smem& sm, int tc, int rc, int sc) 
             F.fi[sc ^ 1][o] = F.fi[sc][n];
             F.fj[sc ^ 1][o] = F.fj[sc][n];
             F.fl[sc ^ 1][o] = F.fl[sc][n];
+            F.mig[sc ^ 1][o] = F.mig[sc][n];
             ++o;
         }
     }

@@ -33,13 +33,23 @@ struct IrfDev {
     const double* s;
     const double* d;
     uint32_t n;
-    uint32_t pad_;
+    uint32_t pow2;     // dtau is a power of two: x/dtau == x*inv_dtau exactly
+    double inv_dtau;
+    double lim;        // (double)(n - 2): the largest segment index
 };
+
+// (tau - tau_min) / dtau, sensor.hpp:71.  Division by a power of two and
+// multiplication by its (exact) reciprocal round identically, so the fast
+// path is bit-identical; any other dtau takes the IEEE division.
+__device__ __forceinline__ double irf_x(const IrfDev& f, double tau) {
+    const double a = tau - f.tau_min;
+    return f.pow2 ? a * f.inv_dtau : a / f.dtau;
+}
 
 // sensor.hpp:69-75
 __device__ __forceinline__ double irf_value(const IrfDev& f, double tau) {
     if (tau < f.tau_min || tau > f.tau_max) return 0.0;
-    double x = (tau - f.tau_min) / f.dtau;
+    double x = irf_x(f, tau);
     unsigned long long k = (unsigned long long)x;
     if (k > (unsigned long long)(f.n - 2)) k = f.n - 2;
     double fr = x - (double)k;
@@ -50,7 +60,7 @@ __device__ __forceinline__ double irf_value(const IrfDev& f, double tau) {
 // sensor.hpp:77-82
 __device__ __forceinline__ double irf_deriv(const IrfDev& f, double tau) {
     if (tau <= f.tau_min || tau >= f.tau_max) return 0.0;
-    double x = (tau - f.tau_min) / f.dtau;
+    double x = irf_x(f, tau);
     unsigned long long k = (unsigned long long)x;
     if (k > (unsigned long long)(f.n - 2)) k = f.n - 2;
     return f.d[k];
