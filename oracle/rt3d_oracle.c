@@ -16,8 +16,9 @@
  *    (denoise.hpp:92-112).  For symmetric PSD M and the Pratt matrix N
  *    (inertia 4+,1-) that is the smallest non-negative eigenvalue, which is
  *    also sup{ sigma >= 0 : M - sigma N positive definite }.  It is found by
- *    bisection on an LDL' definiteness test, and its eigenvector by inverse
- *    iteration on the last definite shift (pratt_smallest below);
+ *    bisection on a division-free definiteness test (pd5), and its
+ *    eigenvector by inverse iteration on an LDL' factor of the last definite
+ *    shift (pratt_smallest below);
  *  - only the eigenVALUES of the 3x3 covariance decide anything
  *    (denoise.hpp:197-203; the eigenvector only orients the sign of u, and the
  *    projection is invariant under u -> -u), computed by cyclic Jacobi;
@@ -880,6 +881,20 @@ static int ldlt5(const double a[5][5], double L[5][5], double d[5]) {
     return 1;
 }
 
+/* Positive definiteness of the lower triangle of a symmetric 5x5 without
+ * divisions: Gaussian elimination with each Schur update scaled by the
+ * (positive) pivot, a[i][j] <- a[k][k] a[i][j] - a[i][k] a[j][k]; the pivots
+ * keep the signs of the LDL' pivots. */
+static int pd5(double a[5][5]) {
+    for (int k = 0; k < 5; ++k) {
+        const double akk = a[k][k];
+        if (!(akk > 0.0)) return 0;
+        for (int i = k + 1; i < 5; ++i)
+            for (int j = k + 1; j <= i; ++j) a[i][j] = akk * a[i][j] - a[i][k] * a[j][k];
+    }
+    return 1;
+}
+
 /* M - sigma N with the Pratt matrix N (denoise.hpp:82-84). */
 static void pencil_shift(const double m[5][5], double sigma, double a[5][5]) {
     memcpy(a, m, sizeof(double) * 25);
@@ -901,13 +916,13 @@ int oracle_pratt_smallest(const double mflat[25], double u[5]) {
     double sigma;
     pencil_shift(m, 0.0, a);
     double hi = std_min(std_min(m[1][1], m[2][2]), m[3][3]);
-    if (ldlt5(a, L, d) && hi > 0.0) {
+    if (pd5(a) && hi > 0.0) {
         double lo = 0.0;
         for (int it = 0; it < 200; ++it) {
             double mid = 0.5 * (lo + hi);
             if (!(mid > lo && mid < hi)) break;
             pencil_shift(m, mid, a);
-            if (ldlt5(a, L, d)) lo = mid;
+            if (pd5(a)) lo = mid;
             else hi = mid;
             if (hi - lo <= 1e-14 * hi) break;
         }
@@ -918,14 +933,29 @@ int oracle_pratt_smallest(const double mflat[25], double u[5]) {
         int ok = 0;
         for (int k = 0; k < 12 && !ok; ++k) {
             pencil_shift(m, -delta, a);
-            if (ldlt5(a, L, d)) ok = 1;
+            if (pd5(a)) ok = 1;
             else delta *= 10.0;
         }
         if (!ok) return 0;
         sigma = -delta;
     }
-    pencil_shift(m, sigma, a);
-    if (!ldlt5(a, L, d)) return 0;
+    /* the factor of the last definite shift; the division-free test and the
+     * LDL' can disagree within rounding of eta*, so step below if needed */
+    {
+        const double base = sigma;
+        double delta = 1e-15 * scale;
+        int ok = 0;
+        for (int k = 0; k < 14; ++k) {
+            pencil_shift(m, sigma, a);
+            if (ldlt5(a, L, d)) {
+                ok = 1;
+                break;
+            }
+            sigma = base - delta;
+            delta *= 10.0;
+        }
+        if (!ok) return 0;
+    }
     /* inverse iteration (M - sigma N) x_{k+1} = N x_k */
     double x[5] = {1.0, 1.0, 1.0, 1.0, 1.0};
     for (int it = 0; it < 4; ++it) {

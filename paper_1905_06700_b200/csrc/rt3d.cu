@@ -270,6 +270,20 @@ __global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it) {
     }
 }
 
+__global__ void __launch_bounds__(kTileThreads) apss_tile_kernel(Frame F) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->P) == 0) return;
+    if (blockIdx.x == 0) stamp(F, PH_LAUNCH);
+    nbr_tile_block<0>(F, smem_raw, F.cfg.tile_cap);
+}
+
+__global__ void __launch_bounds__(kTileThreads) knn_tile_kernel(Frame F) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->P) == 0) return;
+    if (blockIdx.x == 0) stamp(F, PH_LAUNCH);
+    nbr_tile_block<1>(F, smem_raw, F.cfg.tile_cap);
+}
+
 __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop)) return;
@@ -481,6 +495,8 @@ struct rt3d_session {
     cudaStream_t stream = nullptr;
     int grid_frame = 0;  // cooperative grid of stage_kernel
     int grid_apss = 0, grid_knn = 0;
+    int tile_grid = 0;
+    size_t tile_smem = 0;
     int grid_fft = 0;
     // sensor
     bool have_sensor = false;
@@ -509,6 +525,7 @@ struct rt3d_session {
     int tc = 0, rc = 0, bc = 0, sc = 0;
     std::vector<uint32_t> perm;  // device order -> caller's cloud order (nll/grads API)
     uint32_t max_pts_per_pixel = 0;
+    uint32_t P_hint = 0;  // expected point count (tile sizing)
     // last reconstruct report
     int iterations = 0;
     int report_iters_cap = 0;
@@ -653,6 +670,35 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         if (mpp > (uint32_t)kPvc)
             return fail(RT3D_ERR_UNSUPPORTED, "rt3d: more than %d points in one pixel", kPvc);
         F.cfg.gsz = (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) ? 4 : 32;
+        // APSS/kNN tiles: about kTileThreads points per tile, square-ish,
+        // the worst-case staged region (mpp points per pixel) within the
+        // shared-memory budget; else the warp-per-point kernels
+        F.cfg.tile_h = F.cfg.tile_w = 0;
+        const int h = F.cfg.W > 0 ? (F.cfg.W + s->s - 1) / s->s : 0;
+        F.cfg.halo = h;
+        const double ppp = npix ? (double)std::max<uint32_t>(s->P_hint, 1) / npix : 1.0;
+        const size_t budget = 100 * 1024;
+        if (F.cfg.W > 0 && getenv("RT3D_TILES")) {
+            // ~kTileThreads points per tile, at least ~2 tiles per SM
+            int best = 0;
+            int e = (int)std::floor(std::sqrt((double)kTileThreads / std::max(ppp, 1e-3)));
+            e = std::max(1, std::min(e, 32));
+            for (; e >= 1; --e) {
+                const long sp = (long)(e + 2 * h) * (e + 2 * h);
+                const long cap = sp * (long)mpp;
+                if (tile_smem_bytes((int)cap, (int)sp, e) > budget) continue;
+                best = e;
+                const long tiles = (long)((s->rows + e - 1) / e) * ((s->cols + e - 1) / e);
+                if (tiles >= 2L * s->nsm) break;
+            }
+            if (best > 0) {
+                const long sp = (long)(best + 2 * h) * (best + 2 * h);
+                F.cfg.tile_h = F.cfg.tile_w = best;
+                F.cfg.tile_cap = (int)(sp * mpp);
+                s->tile_grid = ((s->rows + best - 1) / best) * ((s->cols + best - 1) / best);
+                s->tile_smem = tile_smem_bytes(F.cfg.tile_cap, (int)sp, best);
+            }
+        }
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
@@ -695,10 +741,16 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
     if (prog == PROG_RECON || prog == PROG_PALM) {
         for (int it = 0; it < F.cfg.max_iters; ++it) {
             if ((st = stage(ST_DEPTH, it))) return st;
-            apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+            if (F.cfg.tile_h > 0)
+                apss_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
+            else
+                apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
             CUDA_TRY(cudaGetLastError());
             if ((st = stage(ST_INTENSITY, it))) return st;
-            knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
+            if (F.cfg.tile_h > 0)
+                knn_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
+            else
+                knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
             CUDA_TRY(cudaGetLastError());
             if ((st = stage(ST_TAIL, it))) return st;
         }
@@ -848,6 +900,10 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
                                                                sizeof(ApssWarpSm) * kNbrWarps));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, knn_kernel, kNbrBlock,
                                                                sizeof(KnnWarpSm) * kNbrWarps));
+        CUDA_TRY(cudaFuncSetAttribute(apss_tile_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(knn_tile_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         s->grid_apss = prop.multiProcessorCount * std::max(a, 1);
         s->grid_knn = prop.multiProcessorCount * std::max(k, 1);
     }
@@ -1070,6 +1126,7 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     g.W = window_w(cfg->apss.kernel_radius, s->pitch);
     g.set_oog_flags = 1;
     s->max_pts_per_pixel = program == PROG_BASELINE ? 1u : (uint32_t)cfg->init.max_returns * s->s * s->s;
+    if (s->P_hint == 0) s->P_hint = (uint32_t)(npix * std::min<double>(1.3, s->max_pts_per_pixel));
     s->tc = s->rc = s->bc = s->sc = 0;
     Frame F;
     if ((st = build_frame(s, F, g, program == PROG_RECON ? cfg->max_iters : 1))) return st;
@@ -1238,6 +1295,7 @@ rt3d_status rt3d_state_upload(rt3d_session* s, const rt3d_state_view* v) {
     uint32_t maxpp = 0;
     for (size_t p = 0; p < npix; ++p) maxpp = std::max(maxpp, counts[p]);
     s->max_pts_per_pixel = maxpp;
+    s->P_hint = (uint32_t)n;
     bool pinned = true;
     std::vector<double> t(n), r(n);
     std::vector<uint32_t> pix(n);

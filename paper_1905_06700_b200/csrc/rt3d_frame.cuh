@@ -112,6 +112,9 @@ struct Cfg {
     int W;             // fine-pixel window half-width floor(R/pitch)+1
     int set_oog_flags; // palm: OR out-of-gate into flags
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
+    int tile_h, tile_w;// APSS/kNN tile (coarse pixels); 0 = warp-per-point kernels
+    int halo;          // ceil(W / s) coarse pixels
+    int tile_cap;      // staged points per tile (shared memory)
 };
 
 struct Frame {

@@ -179,12 +179,37 @@ __device__ __forceinline__ int ldlt5_shift(const double m[15], double sigma, dou
     return 1;
 }
 
+// Positive definiteness of (M - sigma N) without divisions: elimination with
+// each Schur update scaled by the positive pivot (same operations as the
+// oracle's pd5).
+__device__ __forceinline__ int pd5_shift(const double m[15], double sigma) {
+    double a[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) a[k] = m[k];
+    a[lt(1, 1)] = m[lt(1, 1)] - sigma;
+    a[lt(2, 2)] = m[lt(2, 2)] - sigma;
+    a[lt(3, 3)] = m[lt(3, 3)] - sigma;
+    a[lt(4, 0)] = m[lt(4, 0)] + 2.0 * sigma;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const double akk = a[lt(k, k)];
+        if (!(akk > 0.0)) return 0;
+#pragma unroll
+        for (int i = k + 1; i < 5; ++i)
+#pragma unroll
+            for (int j = k + 1; j <= i; ++j)
+                a[lt(i, j)] = akk * a[lt(i, j)] - a[lt(i, k)] * a[lt(j, k)];
+    }
+    return 1;
+}
+
 // Smallest admissible eigenpair of the Pratt pencil (M, N): the eigenvector
 // that the reference's filter loop over GeneralizedEigenSolver's results keeps
 // (denoise.hpp:86-112).  For PSD M the admissible eigenvalues are the
 // non-negative ones, and the smallest is sup{sigma >= 0 : M - sigma N > 0};
-// bisection on the LDL' definiteness test brackets it, inverse iteration on
-// the last definite shift gives the eigenvector.  Same sequence of operations
+// bisection on a division-free definiteness test brackets it, inverse
+// iteration on an LDL' factor of the last definite shift gives the
+// eigenvector.  Same sequence of operations
 // as oracle_pratt_smallest (bit-identical on identical M).
 __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
     double L[15], d[5];
@@ -192,13 +217,13 @@ __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
         std_max(m[lt(0, 0)] + m[lt(1, 1)] + m[lt(2, 2)] + m[lt(3, 3)] + m[lt(4, 4)], 1e-300);
     double sigma;
     double hi = std_min(std_min(m[lt(1, 1)], m[lt(2, 2)]), m[lt(3, 3)]);
-    if (ldlt5_shift(m, 0.0, L, d) && hi > 0.0) {
+    if (pd5_shift(m, 0.0) && hi > 0.0) {
         double lo = 0.0;
 #pragma unroll 1
         for (int it = 0; it < 200; ++it) {
             double mid = 0.5 * (lo + hi);
             if (!(mid > lo && mid < hi)) break;
-            if (ldlt5_shift(m, mid, L, d)) lo = mid;
+            if (pd5_shift(m, mid)) lo = mid;
             else hi = mid;
             if (hi - lo <= 1e-14 * hi) break;
         }
@@ -208,13 +233,28 @@ __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
         int ok = 0;
 #pragma unroll 1
         for (int k = 0; k < 12 && !ok; ++k) {
-            if (ldlt5_shift(m, -delta, L, d)) ok = 1;
+            if (pd5_shift(m, -delta)) ok = 1;
             else delta *= 10.0;
         }
         if (!ok) return 0;
         sigma = -delta;
     }
-    if (!ldlt5_shift(m, sigma, L, d)) return 0;
+    {  // factor of the last definite shift (step below eta* if the LDL'
+       // and the division-free test disagree within rounding)
+        const double base = sigma;
+        double delta = 1e-15 * scale;
+        int ok = 0;
+#pragma unroll 1
+        for (int k = 0; k < 14; ++k) {
+            if (ldlt5_shift(m, sigma, L, d)) {
+                ok = 1;
+                break;
+            }
+            sigma = base - delta;
+            delta *= 10.0;
+        }
+        if (!ok) return 0;
+    }
     double x0 = 1.0, x1 = 1.0, x2 = 1.0, x3 = 1.0, x4 = 1.0;
 #pragma unroll 1
     for (int it = 0; it < 4; ++it) {
