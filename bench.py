@@ -57,35 +57,50 @@ def config_b():
     return spec, 141, cfg, "141x141 px x 4613 bins polystyrene-head-like synthetic frame"
 
 
-def frame_bytes(sc, rep) -> float:
-    """Algorithmic HBM bytes of one frame:
-    every likelihood sweep reads the CSR cube (8 B/event), per-pixel
-    offsets/bucket/background/gain/dead (29 B/px) and t, r, bucket index
-    (20 B/point); gradient sweeps write grad+curv (16 B/unit), candidate
-    sweeps write the candidate (8 B/unit); APSS 17 B/pt, kNN 24 B/pt, prune
-    9 B/pt in + 33 B/survivor + 4 B/px; init 8E + 29 Npix + 33 P0."""
+KERNEL_NAMES = {
+    "stage_first": "rt3d::stage_kernel<ST_FIRST> (init peaks, spawn, first nll+grad sweep)",
+    "stage_depth": "rt3d::stage_kernel<ST_DEPTH> (depth candidates + backtracking)",
+    "apss": "rt3d::apss_kernel (APSS projection + pinning)",
+    "stage_intensity": "rt3d::stage_kernel<ST_INTENSITY> (intensity grad + candidates)",
+    "knn": "rt3d::knn_kernel (kNN intensity filter)",
+    "stage_tail": "rt3d::stage_kernel<ST_TAIL> (prune, background block, nll)",
+}
+
+
+def class_bytes(sc, rep) -> dict:
+    """Algorithmic HBM bytes of one frame per kernel class (DESIGN.md §4,
+    SURVEY.md §8d): every likelihood sweep reads the CSR cube (8 B/event),
+    per-pixel offsets/bucket/background/gain/dead (29 B/px) and t, r, bucket
+    index (20 B/point); gradient sweeps write grad+curv (16 B/unit),
+    candidate sweeps write the candidate (8 B/unit); APSS 17 B/pt, kNN
+    24 B/pt, prune 9 B/pt in + 33 B/survivor + 4 B/px; init 8E + 29 Npix +
+    33 P0."""
     E, npix = len(sc.events), sc.n_pixels
     steps = rep["steps"]
 
     def sweep(P, extra):
         return 8.0 * E + 29.0 * npix + 20.0 * P + extra
 
+    b = dict.fromkeys(KERNEL_NAMES, 0.0)
     P0 = int(steps[0]["points_before"]) if len(steps) else 0
-    total = 8.0 * E + 29.0 * npix + 33.0 * P0          # init
-    total += sweep(P0, 16.0 * P0)                          # first grad_t (+ init nll)
+    b["stage_first"] = 8.0 * E + 29.0 * npix + 33.0 * P0 + sweep(P0, 16.0 * P0)
     for st in steps:
         P, P1 = int(st["points_before"]), int(st["points_after"])
         if P > 0:
-            total += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
-            total += 17.0 * P                              # APSS
-            total += sweep(P, 16.0 * P)                    # grad_r
-            total += (1 + int(st["intensity_backtracks"])) * sweep(P, 8.0 * P)
-            total += 24.0 * P                              # kNN
-            total += 9.0 * P + 33.0 * P1 + 4.0 * npix      # prune + refresh
-        total += sweep(P1, 16.0 * npix)                    # grad_b
-        total += (1 + int(st["background_backtracks"])) * sweep(P1, 8.0 * npix)
-        total += sweep(P1, 16.0 * P1)                      # grad_t (nll after + next grads)
-    return total
+            b["stage_depth"] += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
+            b["apss"] += 17.0 * P
+            b["stage_intensity"] += sweep(P, 16.0 * P) + \
+                (1 + int(st["intensity_backtracks"])) * sweep(P, 8.0 * P)
+            b["knn"] += 24.0 * P
+            b["stage_tail"] += 9.0 * P + 33.0 * P1 + 4.0 * npix
+        b["stage_tail"] += sweep(P1, 16.0 * npix) + \
+            (1 + int(st["background_backtracks"])) * sweep(P1, 8.0 * npix) + \
+            sweep(P1, 16.0 * P1)   # nll after the iteration fused with the next grad_t
+    return b
+
+
+def frame_bytes(sc, rep) -> float:
+    return sum(class_bytes(sc, rep).values())
 
 
 class ClockSampler:
@@ -173,12 +188,13 @@ def load_measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic_per_frame():
-    """dram bytes per frame-kernel launch from the committed ncu capture."""
-    p = ROOT / "profiles" / "ncu_frame_kernel.json"
+def ncu_traffic_per_launch(cls: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of a kernel
+    class, from the committed `ncu --set full` capture summary."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         try:
-            return float(json.loads(p.read_text())["dram_bytes_per_launch"])
+            return float(json.loads(p.read_text())[cls]["dram_bytes_per_launch"])
         except Exception:
             return None
     return None
@@ -272,6 +288,7 @@ def main():
           for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
+    sess.time_kernels(True)   # CUDA events around every launch, session stream
     with ClockSampler(local) as clocks:
         t_wall0 = time.perf_counter()
         with torch.cuda.stream(stream):
@@ -284,6 +301,8 @@ def main():
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     barrier(world)
+    ktimes = sess.kernel_times()
+    sess.time_kernels(False)
     frame_ms = [a.elapsed_time(b) for a, b in ev]
     dev_s = sum(frame_ms) / 1e3
     dev_s_max = barrier_max(dev_s, world, local)
@@ -327,9 +346,19 @@ def main():
     h2d = sc.offsets.nbytes + sc.events.nbytes
 
     peak, peak_src = load_measured_peaks()
-    fb = frame_bytes(sc, rep)
-    avg_frame_s = dev_s / K
-    achieved = fb / avg_frame_s / 1e9
+    cb = class_bytes(sc, rep)
+    fb = sum(cb.values())
+    classes = {}
+    for cls, (ms, n) in ktimes.items():
+        per_launch_bytes = cb[cls] * K / n if n else 0.0
+        classes[cls] = {"ms_per_frame": ms / K, "launches_per_frame": n / K,
+                        "us_per_launch": 1e3 * ms / n if n else None,
+                        "algorithmic_bytes_per_launch": per_launch_bytes,
+                        "gbs": per_launch_bytes / (ms / n) / 1e6 if n and ms else None}
+    dom = max(classes, key=lambda c: classes[c]["ms_per_frame"])
+    dc = classes[dom]
+    achieved = dc["gbs"]
+    launches = sum(n for _, n in ktimes.values())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -358,10 +387,18 @@ def main():
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic_per_frame(),
-                         "kernel": "rt3d::frame_kernel (whole frame, 1 launch)",
-                         "algorithmic_bytes_per_launch": fb, "peak_source": peak_src},
-            "gpu_launches": K,
+                         "frac": achieved / peak, "traffic": ncu_traffic_per_launch(dom),
+                         "kernel": KERNEL_NAMES[dom],
+                         "share_of_frame": dc["ms_per_frame"] / (1e3 * dev_s / K),
+                         "us_per_launch": dc["us_per_launch"],
+                         "algorithmic_bytes_per_launch": dc["algorithmic_bytes_per_launch"],
+                         "peak_source": peak_src,
+                         "timing": "CUDA events on the session stream around every launch, "
+                                   "summed over the timed region"},
+            "frame_roofline": {"achieved": fb / (dev_s / K) / 1e9, "unit": "GB/s",
+                               "algorithmic_bytes_per_frame": fb},
+            "kernel_classes": classes,
+            "gpu_launches": launches,
             "clocks": clocks.summary(),
             "phases_us_per_frame": {k: round(v[1], 1) for k, v in phases.items()},
             "phase_counts": {k: v[0] for k, v in phases.items()},

@@ -193,6 +193,21 @@ void* rt3d_session_stream(rt3d_session* s);
  * pairs of the last launch.  Off by default (bench.py's breakdown only). */
 rt3d_status rt3d_session_profile(rt3d_session* s, int enable);
 rt3d_status rt3d_profile_copy(rt3d_session* s, uint64_t* pairs, uint32_t cap, uint32_t* n);
+/* Kernel-class timing: with it enabled every launch of a frame is bracketed
+ * by CUDA events recorded on the session stream; rt3d_kernel_times
+ * synchronizes and returns the summed milliseconds and launch counts per
+ * class since the last rt3d_session_time_kernels call. */
+enum {
+    RT3D_KC_STAGE_FIRST = 0,     /* init peaks/spawn + first sweeps          */
+    RT3D_KC_STAGE_DEPTH = 1,     /* depth block: grad/curv + backtracking    */
+    RT3D_KC_APSS = 2,            /* APSS projection + pinning (denoise.hpp:159) */
+    RT3D_KC_STAGE_INTENSITY = 3, /* intensity block                          */
+    RT3D_KC_KNN = 4,             /* kNN intensity filter (denoise.hpp:223)   */
+    RT3D_KC_STAGE_TAIL = 5,      /* prune, background block, stop rule       */
+    RT3D_KERNEL_CLASSES = 6
+};
+rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable);
+rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches);
 
 /* Upload the sensor (IRF tables, gain, dead mask) and the photon cube.  They
  * stay resident until replaced.  Validation follows SensorModel's ctor

@@ -530,6 +530,16 @@ struct rt3d_session {
     int iterations = 0;
     int report_iters_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // kernel-class timing with CUDA events on the session stream (opt-in)
+    bool time_kernels = false;
+    struct Timed {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Timed> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    double kt_ms[RT3D_KERNEL_CLASSES] = {};
+    uint64_t kt_n[RT3D_KERNEL_CLASSES] = {};
 };
 
 namespace {
@@ -719,6 +729,49 @@ static StageFn stage_fn(int cfgi, int st) {
     return tab[cfgi][st];
 }
 
+cudaEvent_t pool_event(rt3d_session* s) {
+    if (!s->ev_pool.empty()) {
+        cudaEvent_t e = s->ev_pool.back();
+        s->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// fold completed event pairs into the per-class totals (synchronizes)
+rt3d_status harvest_kernel_times(rt3d_session* s) {
+    if (s->timed.empty()) return RT3D_OK;
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    for (auto& t : s->timed) {
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, t.a, t.b));
+        s->kt_ms[t.cls] += ms;
+        s->kt_n[t.cls] += 1;
+        s->ev_pool.push_back(t.a);
+        s->ev_pool.push_back(t.b);
+    }
+    s->timed.clear();
+    return RT3D_OK;
+}
+
+// launch `fn` bracketed by CUDA events of class `cls` when timing is on
+template <class Fn>
+rt3d_status timed_launch(rt3d_session* s, int cls, Fn&& fn) {
+    if (!s->time_kernels) return fn();
+    if (s->timed.size() > 8192) {
+        rt3d_status st = harvest_kernel_times(s);
+        if (st) return st;
+    }
+    rt3d_session::Timed t{cls, pool_event(s), pool_event(s)};
+    CUDA_TRY(cudaEventRecord(t.a, s->stream));
+    rt3d_status st = fn();
+    CUDA_TRY(cudaEventRecord(t.b, s->stream));
+    s->timed.push_back(t);
+    return st;
+}
+
 rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
     // no host staging: back-to-back async launches must not race on it
     F.P0 = P_init;
@@ -729,11 +782,15 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
     // the frame as a stream-ordered kernel sequence; every decision stays on
     // the device (Ctl), so nothing here waits for the GPU
     const int cfgi = F.cfg.gsz == 4 ? 0 : 1;
+    static const int stage_cls[4] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
+                                     RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL};
     auto stage = [&](int st, int it) -> rt3d_status {
-        void* args[] = {&F, &it};
-        CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st), dim3(s->grid_frame),
-                                             dim3(kBlock), args, sizeof(Smem), s->stream));
-        return RT3D_OK;
+        return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
+            void* args[] = {&F, &it};
+            CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st), dim3(s->grid_frame),
+                                                 dim3(kBlock), args, sizeof(Smem), s->stream));
+            return RT3D_OK;
+        });
     };
     rt3d_status st;
     if ((st = stage(ST_FIRST, 0))) return st;
@@ -741,17 +798,25 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
     if (prog == PROG_RECON || prog == PROG_PALM) {
         for (int it = 0; it < F.cfg.max_iters; ++it) {
             if ((st = stage(ST_DEPTH, it))) return st;
-            if (F.cfg.tile_h > 0)
-                apss_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
-            else
-                apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
-            CUDA_TRY(cudaGetLastError());
+            st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
+                if (F.cfg.tile_h > 0)
+                    apss_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
+                else
+                    apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+                CUDA_TRY(cudaGetLastError());
+                return RT3D_OK;
+            });
+            if (st) return st;
             if ((st = stage(ST_INTENSITY, it))) return st;
-            if (F.cfg.tile_h > 0)
-                knn_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
-            else
-                knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
-            CUDA_TRY(cudaGetLastError());
+            st = timed_launch(s, RT3D_KC_KNN, [&]() -> rt3d_status {
+                if (F.cfg.tile_h > 0)
+                    knn_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
+                else
+                    knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
+                CUDA_TRY(cudaGetLastError());
+                return RT3D_OK;
+            });
+            if (st) return st;
             if ((st = stage(ST_TAIL, it))) return st;
         }
     }
@@ -935,6 +1000,11 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
                       &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->ctl, &s->diag,
                       &s->trace, &s->outpts, &s->misc};
     for (DevBuf* b : bufs) b->release();
+    for (auto& t : s->timed) {
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
+    }
+    for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
     s->mig[0].release();
     s->mig[1].release();
     for (int k = 0; k < 2; ++k) {
@@ -960,6 +1030,29 @@ void* rt3d_session_stream(rt3d_session* s) { return s ? (void*)s->stream : nullp
 rt3d_status rt3d_session_profile(rt3d_session* s, int enable) {
     if (!s) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session");
     s->profile = enable != 0;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = harvest_kernel_times(s))) return st;
+    s->time_kernels = enable != 0;
+    for (int k = 0; k < RT3D_KERNEL_CLASSES; ++k) {
+        s->kt_ms[k] = 0.0;
+        s->kt_n[k] = 0;
+    }
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if ((st = harvest_kernel_times(s))) return st;
+    for (int k = 0; k < RT3D_KERNEL_CLASSES; ++k) {
+        if (ms) ms[k] = s->kt_ms[k];
+        if (launches) launches[k] = s->kt_n[k];
+    }
     return RT3D_OK;
 }
 

@@ -57,6 +57,8 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_session_stream", C.c_void_p, [SS])
     _bind(L, "rt3d_session_profile", _st, [SS, C.c_int])
     _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
+    _bind(L, "rt3d_session_time_kernels", _st, [SS, C.c_int])
+    _bind(L, "rt3d_kernel_times", _st, [SS, P(_dbl), P(_u64)])
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
@@ -94,6 +96,7 @@ def _check(status: int):
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
+    "rt3d_session_time_kernels", "rt3d_kernel_times",
     "rt3d_set_sensor", "rt3d_set_cube",
     "rt3d_reconstruct", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
@@ -189,6 +192,19 @@ class Session:
             out.append((self.PHASES.get(int(pid), str(pid)), 0 if prev is None else int(ts) - prev))
             prev = int(ts)
         return out
+
+    KERNEL_CLASSES = ("stage_first", "stage_depth", "apss", "stage_intensity", "knn", "stage_tail")
+
+    def time_kernels(self, enable: bool = True):
+        """CUDA events around every launch on the session stream (resets totals)."""
+        _check(lib().rt3d_session_time_kernels(self.h, int(enable)))
+
+    def kernel_times(self) -> dict:
+        """{class: (total_ms, launches)} since time_kernels(); synchronizes."""
+        ms = np.zeros(len(self.KERNEL_CLASSES))
+        n = np.zeros(len(self.KERNEL_CLASSES), np.uint64)
+        _check(lib().rt3d_kernel_times(self.h, ptr(ms, _dbl), ptr(n, _u64)))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KERNEL_CLASSES)}
 
     def synchronize(self):
         _check(lib().rt3d_session_synchronize(self.h))
