@@ -60,7 +60,8 @@ def config_b():
 KERNEL_NAMES = {
     "stage_first": "rt3d::stage_kernel<ST_FIRST> (init peaks, spawn, first nll+grad sweep)",
     "stage_depth": "rt3d::stage_kernel<ST_DEPTH> (depth candidates + backtracking)",
-    "apss": "rt3d::apss_kernel (APSS projection + pinning)",
+    "apss": "rt3d::apss_kernel (APSS ball moments, warp per point)",
+    "apss_fit": "rt3d::apss_fit_kernel (sphere fit, projection, pinning)",
     "stage_intensity": "rt3d::stage_kernel<ST_INTENSITY> (intensity grad + candidates)",
     "knn": "rt3d::knn_kernel (kNN intensity filter)",
     "stage_tail": "rt3d::stage_kernel<ST_TAIL> (prune, background block, nll)",
@@ -88,7 +89,8 @@ def class_bytes(sc, rep) -> dict:
         P, P1 = int(st["points_before"]), int(st["points_after"])
         if P > 0:
             b["stage_depth"] += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
-            b["apss"] += 17.0 * P
+            b["apss"] += 8.0 * P          # t in (neighbours are L2/SMEM reuse)
+            b["apss_fit"] += 9.0 * P      # t out + flags
             b["stage_intensity"] += sweep(P, 16.0 * P) + \
                 (1 + int(st["intensity_backtracks"])) * sweep(P, 8.0 * P)
             b["knn"] += 24.0 * P

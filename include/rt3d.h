@@ -200,11 +200,12 @@ rt3d_status rt3d_profile_copy(rt3d_session* s, uint64_t* pairs, uint32_t cap, ui
 enum {
     RT3D_KC_STAGE_FIRST = 0,     /* init peaks/spawn + first sweeps          */
     RT3D_KC_STAGE_DEPTH = 1,     /* depth block: grad/curv + backtracking    */
-    RT3D_KC_APSS = 2,            /* APSS projection + pinning (denoise.hpp:159) */
+    RT3D_KC_APSS = 2,            /* APSS ball moments (denoise.hpp:159-195)  */
     RT3D_KC_STAGE_INTENSITY = 3, /* intensity block                          */
     RT3D_KC_KNN = 4,             /* kNN intensity filter (denoise.hpp:223)   */
     RT3D_KC_STAGE_TAIL = 5,      /* prune, background block, stop rule       */
-    RT3D_KERNEL_CLASSES = 6
+    RT3D_KC_APSS_FIT = 6,        /* APSS sphere fit + projection + pinning   */
+    RT3D_KERNEL_CLASSES = 7
 };
 rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable);
 rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches);

@@ -990,19 +990,9 @@ typedef struct sphere_t {
 } sphere_t;
 
 /* fit_algebraic_sphere, denoise.hpp:66-125 */
-static sphere_t fit_sphere(const double* q, const double* w, uint64_t nq, const double centre[3]) {
-    double M[25];
-    memset(M, 0, sizeof(M));
-    for (uint64_t k = 0; k < nq; ++k) {
-        if (w[k] <= 0.0) continue;
-        double y0 = q[3 * k] - centre[0], y1 = q[3 * k + 1] - centre[1],
-               y2 = q[3 * k + 2] - centre[2];
-        double dv[5] = {1.0, y0, y1, y2, y0 * y0 + y1 * y1 + y2 * y2};
-        for (int r = 0; r < 5; ++r) {
-            double wr = w[k] * dv[r];
-            for (int c = 0; c <= r; ++c) M[r * 5 + c] += wr * dv[c];
-        }
-    }
+/* fit_algebraic_sphere (denoise.hpp:66-125) from its moment matrix M
+ * (lower triangle, row-major 5x5), accumulated by the caller */
+static sphere_t fit_sphere(const double M[25], const double centre[3]) {
     sphere_t best;
     memset(&best, 0, sizeof(best));
     double v[5];
@@ -1064,6 +1054,16 @@ static int project_sphere(const sphere_t* s, double eps, const double p[3], doub
     return 1;
 }
 
+#define APSS_LANES 32
+/* the halving tree over 32 lane partials: p[l] += p[l + o], o = 16 .. 1 */
+static double lane_tree(const double* base, int stride, int col) {
+    double p[APSS_LANES];
+    for (int l = 0; l < APSS_LANES; ++l) p[l] = base[l * stride + col];
+    for (int o = APSS_LANES / 2; o > 0; o >>= 1)
+        for (int l = 0; l < o; ++l) p[l] = p[l] + p[l + o];
+    return p[0];
+}
+
 /* apss_project, denoise.hpp:159-217 */
 int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_params* prm,
                         const rt3d_point* index_cloud, uint64_t n_index, double cell,
@@ -1095,32 +1095,62 @@ int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_par
             q = (double*)realloc(q, sizeof(double) * 3 * qcap);
             w = (double*)realloc(w, sizeof(double) * qcap);
         }
-        double wsum = 0.0, mean[3] = {0.0, 0.0, 0.0};
+        /* Summation order (shared with the device kernel, rt3d_nbr.cuh): ball
+         * member m (ascending index) is accumulated into lane m mod 32,
+         * sequentially; the 32 lane partials are then combined by the halving
+         * tree of lane_tree().  The reference sums each moment sequentially
+         * (denoise.hpp:174-180, 191-194, 74-80); the reassociation moves the
+         * moments at the 1e-16 relative level, far below the eigen-solver
+         * difference. */
+        double pa[APSS_LANES][4];
+        memset(pa, 0, sizeof(pa));
         for (uint64_t m = 0; m < cnt; ++m) {
             const rt3d_point* o = &index_cloud[nb[m]];
+            double* a = pa[m % APSS_LANES];
             q[3 * m] = o->x;
             q[3 * m + 1] = o->y;
             q[3 * m + 2] = o->z;
             w[m] = apss_weight(R, sqrt(sqdist(o->x, o->y, o->z, pt->x, pt->y, pt->z)));
-            wsum += w[m];
-            for (int a = 0; a < 3; ++a) mean[a] += w[m] * q[3 * m + a];
+            a[0] += w[m];
+            for (int c = 0; c < 3; ++c) a[1 + c] += w[m] * q[3 * m + c];
         }
+        double wsum = lane_tree(&pa[0][0], 4, 0), mean[3];
+        for (int c = 0; c < 3; ++c) mean[c] = lane_tree(&pa[0][0], 4, 1 + c);
         if (wsum <= 0.0) {
             out[k].flags = flags | RT3D_FLAG_DEGENERATE;
             continue;
         }
         for (int a = 0; a < 3; ++a) mean[a] /= wsum;
-        double cov[9];
-        memset(cov, 0, sizeof(cov));
+        /* covariance (denoise.hpp:190-195) and the Pratt moments M
+         * (denoise.hpp:73-80, members with w > 0), both centred on the mean */
+        double pb[APSS_LANES][21];
+        memset(pb, 0, sizeof(pb));
         for (uint64_t m = 0; m < cnt; ++m) {
+            double* b = pb[m % APSS_LANES];
             double d[3] = {q[3 * m] - mean[0], q[3 * m + 1] - mean[1], q[3 * m + 2] - mean[2]};
+            int e = 0;
             for (int r = 0; r < 3; ++r) {
                 double wr = w[m] * d[r];
-                for (int c = 0; c <= r; ++c) cov[r * 3 + c] += wr * d[c];
+                for (int c = 0; c <= r; ++c) b[e++] += wr * d[c];
+            }
+            if (w[m] > 0.0) {
+                double dv[5] = {1.0, d[0], d[1], d[2], d[0] * d[0] + d[1] * d[1] + d[2] * d[2]};
+                for (int r = 0; r < 5; ++r) {
+                    double wr = w[m] * dv[r];
+                    for (int c = 0; c <= r; ++c) b[e++] += wr * dv[c];
+                }
             }
         }
-        for (int r = 0; r < 3; ++r)
-            for (int c = 0; c <= r; ++c) cov[r * 3 + c] /= wsum;
+        double cov[9], M[25];
+        memset(cov, 0, sizeof(cov));
+        memset(M, 0, sizeof(M));
+        {
+            int e = 0;
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c <= r; ++c) cov[r * 3 + c] = lane_tree(&pb[0][0], 21, e++) / wsum;
+            for (int r = 0; r < 5; ++r)
+                for (int c = 0; c <= r; ++c) M[r * 5 + c] = lane_tree(&pb[0][0], 21, e++);
+        }
         double ev[3];
         oracle_sym3_eigenvalues(cov, ev);
         double spread = ev[2];
@@ -1128,7 +1158,7 @@ int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_par
             out[k].flags = flags | RT3D_FLAG_DEGENERATE;
             continue;
         }
-        sphere_t fit = fit_sphere(q, w, cnt, mean);
+        sphere_t fit = fit_sphere(M, mean);
         double p[3] = {pt->x, pt->y, pt->z}, proj[3];
         if (!fit.valid || !project_sphere(&fit, prm->sphere_degeneracy_eps, p, proj)) {
             out[k].flags = flags | RT3D_FLAG_DEGENERATE;

@@ -270,25 +270,17 @@ __global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it) {
     }
 }
 
-__global__ void __launch_bounds__(kTileThreads) apss_tile_kernel(Frame F) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->P) == 0) return;
-    if (blockIdx.x == 0) stamp(F, PH_LAUNCH);
-    nbr_tile_block<0>(F, smem_raw, F.cfg.tile_cap);
-}
-
-__global__ void __launch_bounds__(kTileThreads) knn_tile_kernel(Frame F) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->P) == 0) return;
-    if (blockIdx.x == 0) stamp(F, PH_LAUNCH);
-    nbr_tile_block<1>(F, smem_raw, F.cfg.tile_cap);
-}
-
 __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop)) return;
-    stamp(F, PH_LAUNCH);
-    apss_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw));
+    stamp(F, PH_APSS);
+    apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw));
+}
+
+__global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(Frame F) {
+    if (ld_cg(&F.ctl->stop)) return;
+    stamp(F, PH_APSS_FIT);
+    apss_fit_threads(F);
 }
 
 __global__ void __launch_bounds__(kNbrBlock, 4) knn_kernel(Frame F) {
@@ -494,9 +486,7 @@ struct rt3d_session {
     int nsm = 0;
     cudaStream_t stream = nullptr;
     int grid_frame = 0;  // cooperative grid of stage_kernel
-    int grid_apss = 0, grid_knn = 0;
-    int tile_grid = 0;
-    size_t tile_smem = 0;
+    int grid_apss = 0, grid_knn = 0, grid_fit = 0;
     int grid_fft = 0;
     // sensor
     bool have_sensor = false;
@@ -513,7 +503,7 @@ struct rt3d_session {
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
     DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot, part, mig[2];
-    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im;
+    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom;
     DevBuf ctl, diag, trace, outpts, misc, prof;
     bool profile = false;
     Ctl* h_ctl = nullptr;  // pinned staging
@@ -525,7 +515,6 @@ struct rt3d_session {
     int tc = 0, rc = 0, bc = 0, sc = 0;
     std::vector<uint32_t> perm;  // device order -> caller's cloud order (nll/grads API)
     uint32_t max_pts_per_pixel = 0;
-    uint32_t P_hint = 0;  // expected point count (tile sizing)
     // last reconstruct report
     int iterations = 0;
     int report_iters_cap = 0;
@@ -662,6 +651,9 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.nval = s->nval.as<uint32_t>();
     F.fft_re = s->fft_re.as<double>();
     F.fft_im = s->fft_im.as<double>();
+    CUDA_TRY(s->amom.ensure(std::max<size_t>(s->pcap, 1) * kMom * 8));
+    F.amom = s->amom.as<double>();
+    F.amom_stride = (uint32_t)std::max<size_t>(s->pcap, 1);
     F.ctl = s->ctl.as<Ctl>();
     F.prof = nullptr;
     if (s->profile) {
@@ -680,35 +672,6 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         if (mpp > (uint32_t)kPvc)
             return fail(RT3D_ERR_UNSUPPORTED, "rt3d: more than %d points in one pixel", kPvc);
         F.cfg.gsz = (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) ? 4 : 32;
-        // APSS/kNN tiles: about kTileThreads points per tile, square-ish,
-        // the worst-case staged region (mpp points per pixel) within the
-        // shared-memory budget; else the warp-per-point kernels
-        F.cfg.tile_h = F.cfg.tile_w = 0;
-        const int h = F.cfg.W > 0 ? (F.cfg.W + s->s - 1) / s->s : 0;
-        F.cfg.halo = h;
-        const double ppp = npix ? (double)std::max<uint32_t>(s->P_hint, 1) / npix : 1.0;
-        const size_t budget = 100 * 1024;
-        if (F.cfg.W > 0 && getenv("RT3D_TILES")) {
-            // ~kTileThreads points per tile, at least ~2 tiles per SM
-            int best = 0;
-            int e = (int)std::floor(std::sqrt((double)kTileThreads / std::max(ppp, 1e-3)));
-            e = std::max(1, std::min(e, 32));
-            for (; e >= 1; --e) {
-                const long sp = (long)(e + 2 * h) * (e + 2 * h);
-                const long cap = sp * (long)mpp;
-                if (tile_smem_bytes((int)cap, (int)sp, e) > budget) continue;
-                best = e;
-                const long tiles = (long)((s->rows + e - 1) / e) * ((s->cols + e - 1) / e);
-                if (tiles >= 2L * s->nsm) break;
-            }
-            if (best > 0) {
-                const long sp = (long)(best + 2 * h) * (best + 2 * h);
-                F.cfg.tile_h = F.cfg.tile_w = best;
-                F.cfg.tile_cap = (int)(sp * mpp);
-                s->tile_grid = ((s->rows + best - 1) / best) * ((s->cols + best - 1) / best);
-                s->tile_smem = tile_smem_bytes(F.cfg.tile_cap, (int)sp, best);
-            }
-        }
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
@@ -799,20 +762,20 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
         for (int it = 0; it < F.cfg.max_iters; ++it) {
             if ((st = stage(ST_DEPTH, it))) return st;
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
-                if (F.cfg.tile_h > 0)
-                    apss_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
-                else
-                    apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+                apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+                CUDA_TRY(cudaGetLastError());
+                return RT3D_OK;
+            });
+            if (st) return st;
+            st = timed_launch(s, RT3D_KC_APSS_FIT, [&]() -> rt3d_status {
+                apss_fit_kernel<<<s->grid_fit, kFitBlock, 0, s->stream>>>(F);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
             if (st) return st;
             if ((st = stage(ST_INTENSITY, it))) return st;
             st = timed_launch(s, RT3D_KC_KNN, [&]() -> rt3d_status {
-                if (F.cfg.tile_h > 0)
-                    knn_tile_kernel<<<s->tile_grid, kTileThreads, s->tile_smem, s->stream>>>(F);
-                else
-                    knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
+                knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
@@ -965,11 +928,10 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
                                                                sizeof(ApssWarpSm) * kNbrWarps));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, knn_kernel, kNbrBlock,
                                                                sizeof(KnnWarpSm) * kNbrWarps));
-        CUDA_TRY(cudaFuncSetAttribute(apss_tile_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-        CUDA_TRY(cudaFuncSetAttribute(knn_tile_kernel,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
         s->grid_apss = prop.multiProcessorCount * std::max(a, 1);
+        int f = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, apss_fit_kernel, kFitBlock, 0));
+        s->grid_fit = prop.multiProcessorCount * std::max(f, 1);
         s->grid_knn = prop.multiProcessorCount * std::max(k, 1);
     }
     if (per_sm < 1) {
@@ -997,7 +959,7 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
                       &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk, &s->part,
                       &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
-                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->ctl, &s->diag,
+                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->amom, &s->ctl, &s->diag,
                       &s->trace, &s->outpts, &s->misc};
     for (DevBuf* b : bufs) b->release();
     for (auto& t : s->timed) {
@@ -1219,7 +1181,6 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     g.W = window_w(cfg->apss.kernel_radius, s->pitch);
     g.set_oog_flags = 1;
     s->max_pts_per_pixel = program == PROG_BASELINE ? 1u : (uint32_t)cfg->init.max_returns * s->s * s->s;
-    if (s->P_hint == 0) s->P_hint = (uint32_t)(npix * std::min<double>(1.3, s->max_pts_per_pixel));
     s->tc = s->rc = s->bc = s->sc = 0;
     Frame F;
     if ((st = build_frame(s, F, g, program == PROG_RECON ? cfg->max_iters : 1))) return st;
@@ -1388,7 +1349,6 @@ rt3d_status rt3d_state_upload(rt3d_session* s, const rt3d_state_view* v) {
     uint32_t maxpp = 0;
     for (size_t p = 0; p < npix; ++p) maxpp = std::max(maxpp, counts[p]);
     s->max_pts_per_pixel = maxpp;
-    s->P_hint = (uint32_t)n;
     bool pinned = true;
     std::vector<double> t(n), r(n);
     std::vector<uint32_t> pix(n);

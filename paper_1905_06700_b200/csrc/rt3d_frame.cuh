@@ -68,7 +68,7 @@ enum Op : int {
 enum Phase : int {
     PH_INIT_PEAKS = 1, PH_SCAN = 2, PH_SPAWN = 3, PH_GRAD_T = 4, PH_CAND_T = 5, PH_APSS = 6,
     PH_GRAD_R = 7, PH_CAND_R = 8, PH_KNN = 9, PH_PRUNE_A = 10, PH_PRUNE_B = 11, PH_GRAD_B = 12,
-    PH_CAND_B = 13, PH_FFT = 14, PH_LAUNCH = 15,
+    PH_CAND_B = 13, PH_FFT = 14, PH_LAUNCH = 15, PH_APSS_FIT = 16,
 };
 
 struct BlockDiagDev {
@@ -112,9 +112,6 @@ struct Cfg {
     int W;             // fine-pixel window half-width floor(R/pitch)+1
     int set_oog_flags; // palm: OR out-of-gate into flags
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
-    int tile_h, tile_w;// APSS/kNN tile (coarse pixels); 0 = warp-per-point kernels
-    int halo;          // ceil(W / s) coarse pixels
-    int tile_cap;      // staged points per tile (shared memory)
 };
 
 struct Frame {
@@ -168,6 +165,8 @@ struct Frame {
     double* pk_int;   // intensity, < 0 marks a peak with no in-gate IRF mass
     uint32_t* npk;
     uint32_t* nval;
+    double* amom;     // APSS moments, kMom x amom_stride (SoA): apss_kernel -> apss_fit_kernel
+    uint32_t amom_stride;
     double* fft_re;   // 2*npix complex scratch (fft background mode)
     double* fft_im;
     // control / report
@@ -1080,27 +1079,70 @@ __device__ __forceinline__ void for_each_pinned_neighbor(const Frame& F, int tc,
     }
 }
 
+constexpr int kMom = 25;        // APSS moments: wsum, mean(3), cov(6), M(15)
+constexpr int kRedStride = 21;  // APSS pass-B partials per lane (cov 6 + M 15)
+
+// covariance (denoise.hpp:190-195) and Pratt moments (denoise.hpp:73-80) of
+// one member, centred on the mean, into this lane's partials
+__device__ __forceinline__ void apss_pass_b(double (&b)[kRedStride], double w, double x, double y,
+                                            double z, double m0, double m1, double m2) {
+    const double d0 = x - m0, d1 = y - m1, d2 = z - m2;
+    double wr = w * d0;
+    b[0] += wr * d0;
+    wr = w * d1;
+    b[1] += wr * d0;
+    b[2] += wr * d1;
+    wr = w * d2;
+    b[3] += wr * d0;
+    b[4] += wr * d1;
+    b[5] += wr * d2;
+    if (w > 0.0) {
+        const double dv[5] = {1.0, d0, d1, d2, d0 * d0 + d1 * d1 + d2 * d2};
+        int e = 6;
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const double wa = w * dv[r];
+#pragma unroll
+            for (int c = 0; c <= r; ++c) b[e++] += wa * dv[c];
+        }
+    }
+}
+
+// the halving tree over 32 lane partials (column `col` of p[32][stride]):
+// p[l] = p[l] + p[l+o], o = 16..1 (oracle: lane_tree)
+__device__ __forceinline__ double halving_sum32(double* p, int stride, int col) {
+    for (int o = 16; o > 0; o >>= 1)
+        for (int l = 0; l < o; ++l) p[l * stride + col] = p[l * stride + col] + p[(l + o) * stride + col];
+    return p[col];
+}
+
 // apss_project for one point (denoise.hpp:163-214), neighbour enumerator
-// supplied by the caller.  Returns the new position in `out` when the fit
-// projected it; updates flags.
+// supplied by the caller, in the lane-strided summation order of the warp
+// kernel (rt3d_nbr.cuh) emulated sequentially.  Returns the new position in
+// `out` when the fit projected it; updates flags.
 template <typename Enum>
 __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, int min_nbrs,
                                            double eps, uint8_t& flags, Pos& out) {
     const double r2 = R * R;
     unsigned int cnt = 0;
-    double wsum = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+    double pa[32][4];
+    for (int l = 0; l < 32; ++l) pa[l][0] = pa[l][1] = pa[l][2] = pa[l][3] = 0.0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
+        const double w = apss_weight(R, sqrt(d2));
+        double* a = pa[cnt & 31u];
         ++cnt;
-        double w = apss_weight(R, sqrt(d2));
-        wsum += w;
-        m0 += w * o.x;
-        m1 += w * o.y;
-        m2 += w * o.z;
+        a[0] += w;
+        a[1] += w * o.x;
+        a[2] += w * o.y;
+        a[3] += w * o.z;
     });
     if (cnt < (unsigned int)min_nbrs) {
         flags |= 1u;
         return false;
     }
+    const double wsum = halving_sum32(&pa[0][0], 4, 0);
+    double m0 = halving_sum32(&pa[0][0], 4, 1), m1 = halving_sum32(&pa[0][0], 4, 2),
+           m2 = halving_sum32(&pa[0][0], 4, 3);
     if (wsum <= 0.0) {
         flags |= 4u;
         return false;
@@ -1108,45 +1150,23 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
     m0 /= wsum;
     m1 /= wsum;
     m2 /= wsum;
-    double c00 = 0, c10 = 0, c11 = 0, c20 = 0, c21 = 0, c22 = 0;
+    double pb[32][kRedStride];
+    for (int l = 0; l < 32; ++l)
+        for (int e = 0; e < kRedStride; ++e) pb[l][e] = 0.0;
+    unsigned int c2 = 0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        double w = apss_weight(R, sqrt(d2));
-        double d0 = o.x - m0, d1 = o.y - m1, dd2 = o.z - m2;
-        double w0 = w * d0, w1 = w * d1, w2 = w * dd2;
-        c00 += w0 * d0;
-        c10 += w1 * d0;
-        c11 += w1 * d1;
-        c20 += w2 * d0;
-        c21 += w2 * d1;
-        c22 += w2 * dd2;
+        apss_pass_b(pb[c2 & 31u], apss_weight(R, sqrt(d2)), o.x, o.y, o.z, m0, m1, m2);
+        ++c2;
     });
-    c00 /= wsum;
-    c10 /= wsum;
-    c11 /= wsum;
-    c20 /= wsum;
-    c21 /= wsum;
-    c22 /= wsum;
+    double cv[6], M[15];
+    for (int e = 0; e < 6; ++e) cv[e] = halving_sum32(&pb[0][0], kRedStride, e) / wsum;
+    for (int e = 0; e < 15; ++e) M[e] = halving_sum32(&pb[0][0], kRedStride, 6 + e);
     double e0, e1, e2;
-    sym3_eigenvalues(c00, c10, c11, c20, c21, c22, e0, e1, e2);
+    sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
     if (e2 <= 0.0 || e1 <= 1e-12 * e2) {
         flags |= 4u;
         return false;
     }
-    double M[15];
-#pragma unroll
-    for (int k = 0; k < 15; ++k) M[k] = 0.0;
-    each(r2, [&](uint32_t, const Pos& o, double d2) {
-        double w = apss_weight(R, sqrt(d2));
-        if (w <= 0.0) return;
-        double y0 = o.x - m0, y1 = o.y - m1, y2 = o.z - m2;
-        double dv[5] = {1.0, y0, y1, y2, y0 * y0 + y1 * y1 + y2 * y2};
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            double wa = w * dv[a];
-#pragma unroll
-            for (int c = 0; c <= a; ++c) M[lt(a, c)] += wa * dv[c];
-        }
-    });
     Sphere sp;
     if (!sphere_from_moments(M, m0, m1, m2, sp) ||
         !project_sphere(sp, eps, q.x, q.y, q.z, out.x, out.y, out.z)) {

@@ -175,7 +175,7 @@ class Session:
 
     PHASES = {1: "init_peaks", 2: "init_scan", 3: "init_spawn", 4: "grad_t", 5: "cand_t",
               6: "apss", 7: "grad_r", 8: "cand_r", 9: "knn", 10: "prune_a", 11: "prune_b",
-              12: "grad_b", 13: "cand_b", 14: "fft"}
+              12: "grad_b", 13: "cand_b", 14: "fft", 15: "launch", 16: "apss_fit"}
 
     def profile_phases(self):
         """(name, duration_ns) per barrier-delimited phase of the last launch."""
@@ -193,7 +193,8 @@ class Session:
             prev = int(ts)
         return out
 
-    KERNEL_CLASSES = ("stage_first", "stage_depth", "apss", "stage_intensity", "knn", "stage_tail")
+    KERNEL_CLASSES = ("stage_first", "stage_depth", "apss", "stage_intensity", "knn", "stage_tail",
+                      "apss_fit")
 
     def time_kernels(self, enable: bool = True):
         """CUDA events around every launch on the session stream (resets totals)."""
