@@ -663,6 +663,14 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.diag = s->diag.as<StepDiagDev>();
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
+    {
+        // first kNN window: about k fine pixels; no pruning on huge grids
+        // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
+        int w0 = (int)std::ceil(std::sqrt((double)std::max(cfg.knn_k, 1)) / 2.0);
+        w0 = std::max(w0, 1);
+        if (F.frows >= (1 << 20) || F.fcols >= (1 << 20) || getenv("RT3D_KNN_NO_PRUNE")) w0 = cfg.W;
+        F.cfg.knn_w0 = w0;
+    }
     F.cfg.max_iters = max_iters;
     // lanes per pixel for the likelihood sweeps: 4 for sparse pixels (a few
     // events, <= 4 points), a warp otherwise

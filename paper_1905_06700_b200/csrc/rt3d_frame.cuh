@@ -110,6 +110,7 @@ struct Cfg {
     int K, sep;
     double thr;
     int W;             // fine-pixel window half-width floor(R/pitch)+1
+    int knn_w0;        // first kNN window half-width (see knn_warps)
     int set_oog_flags; // palm: OR out-of-gate into flags
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };

@@ -49,6 +49,8 @@ struct ApssWarpSm {
 struct KnnWarpSm {
     double d2[kKnnCap];
     uint32_t idx[kKnnCap];
+    uint32_t sel[kKnnCap];  // the selection in rank order
+    double kth;
     RowTab rt;
 };
 
@@ -63,9 +65,10 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 template <typename Visit, typename Flush>
 __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab& rt, int fi,
                                           int fj, const Pos& q, double r2, Visit visit,
-                                          Flush flush) {
+                                          Flush flush, int Wq = -1) {
     const int lane = threadIdx.x & 31;
-    const int W = F.cfg.W, s = F.s;
+    // Wq < W restricts the scan to the fine window of half-width Wq (kNN)
+    const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W, s = F.s;
     const double rw = F.cfg.R / F.pitch;
     const double lim2 = rw * rw * (1.0 + 1e-9);
     int a0 = fi - W, a1 = fi + W;
@@ -307,7 +310,77 @@ __device__ void apss_fit_threads(const Frame& F) {
     }
 }
 
+// k smallest (d^2, index) keys of the warp's list in rank order
+// (spatial_index.hpp:51-62) -> K.sel[0..taken); kth = the last key's d^2.
+__device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k, double& kth) {
+    const int lane = threadIdx.x & 31;
+    if (cnt <= 64u) {
+        // rank counting: the list is in ascending index order, so the
+        // (d^2, index) order is (d^2, slot); ranks are a permutation
+        const int taken = (unsigned int)k < cnt ? k : (int)cnt;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const unsigned int sl = (unsigned int)lane + 32u * h;
+            if (sl < cnt) {
+                const double my = K.d2[sl];
+                int rank = 0;
+                for (unsigned int e = 0; e < cnt; ++e) {
+                    const double d = K.d2[e];
+                    rank += (d < my || (d == my && e < sl)) ? 1 : 0;
+                }
+                if (rank < taken) K.sel[rank] = K.idx[sl];
+                if (rank == taken - 1) K.kth = my;
+            }
+        }
+        __syncwarp();
+        kth = taken > 0 ? K.kth : 0.0;
+        __syncwarp();
+        return taken;
+    }
+    double last_d = 0.0;
+    uint32_t last_i = 0;
+    int taken = 0;
+    for (; taken < k && (unsigned int)taken < cnt; ++taken) {
+        double bd = INFINITY;
+        uint32_t bi = 0xffffffffu;
+        for (unsigned int e = lane; e < cnt; e += 32) {
+            const double d = K.d2[e];
+            const uint32_t i = K.idx[e];
+            const bool after = taken == 0 || d > last_d || (d == last_d && i > last_i);
+            if (after && (d < bd || (d == bd && i < bi))) {
+                bd = d;
+                bi = i;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (od < bd || (od == bd && oi < bi)) {
+                bd = od;
+                bi = oi;
+            }
+        }
+        if (lane == 0) K.sel[taken] = bi;
+        last_d = bd;
+        last_i = bi;
+    }
+    kth = last_d;
+    __syncwarp();
+    return taken;
+}
+
 // kNN intensity filter over the current state; writes r[rc^1].
+//
+// Window pruning (exact): a member whose fine pixel lies outside the window
+// of half-width w differs by >= w+1 pixels along one axis, so its d^2 is at
+// least ((w+1) pitch)^2 (1 - 1e-9) (d^2 = (dx^2 + dy^2) + dz^2 only grows with
+// the added squares; the margin covers the rounding of the pixel-centre
+// coordinates for grids below 2^20 fine pixels).  The scan starts with the
+// small window knn_w0; if the k-th key found there is below that bound for
+// the next ring, no member outside can enter the top k and the selection is
+// final; otherwise the window grows to the first ring whose bound exceeds
+// the k-th key (at most W, the full ball).
 __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KnnWarpSm& K = wsm[warp];
@@ -317,59 +390,84 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
     const uint32_t gw = blockIdx.x * kNbrWarps + warp, nw = gridDim.x * kNbrWarps;
     const double R = F.cfg.R, r2 = R * R;
     const double* rr = F.r[rc];
-    const int k = F.cfg.knn_k;
+    const int k = F.cfg.knn_k, Wfull = F.cfg.W;
+    const double pitch = F.pitch;
     for (uint32_t n = gw; n < P; n += nw) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
-        const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
-        unsigned int cnt = 0;
-        ball_scan(
-            F, tc, sc, K.rt, fi, fj, q, r2,
-            [&](int rank, uint32_t mm, const Pos&, double d2, int, int) {
-                const unsigned int slot = cnt + (unsigned int)rank;
-                if (slot < (unsigned int)kKnnCap) {
-                    K.d2[slot] = d2;
-                    K.idx[slot] = mm;
-                }
-            },
-            [&](int nm) { cnt += (unsigned int)nm; });
-        // k smallest (d^2, index) in rank order (spatial_index.hpp:51-62),
-        // averaged in that order (denoise.hpp:233-234)
-        double last_d = 0.0, acc = 0.0;
-        uint32_t last_i = 0;
+        const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, F.t[tc][n] * F.bres};
+        int w = F.cfg.knn_w0 < Wfull ? F.cfg.knn_w0 : Wfull;
+        double kth = 0.0;
         int taken = 0;
-        const bool listed = cnt <= (unsigned int)kKnnCap;
-        for (; taken < k && (unsigned int)taken < cnt; ++taken) {
-            double bd = INFINITY;
-            uint32_t bi = 0xffffffffu;
-            auto consider = [&](double d, uint32_t i) {
-                const bool after = taken == 0 || d > last_d || (d == last_d && i > last_i);
-                if (after && (d < bd || (d == bd && i < bi))) {
-                    bd = d;
-                    bi = i;
-                }
-            };
-            if (listed) {
-                for (unsigned int e = lane; e < cnt; e += 32) consider(K.d2[e], K.idx[e]);
-            } else {  // list overflow: rescan the ball
+        unsigned int cnt;
+        for (;;) {
+            cnt = 0;
+            ball_scan(
+                F, tc, sc, K.rt, fi, fj, q, r2,
+                [&](int rank, uint32_t mm, const Pos&, double d2, int, int) {
+                    const unsigned int slot = cnt + (unsigned int)rank;
+                    if (slot < (unsigned int)kKnnCap) {
+                        K.d2[slot] = d2;
+                        K.idx[slot] = mm;
+                    }
+                },
+                [&](int nm) { cnt += (unsigned int)nm; }, w);
+            __syncwarp();
+            if (cnt > (unsigned int)kKnnCap) break;  // overflow: exact rescan below
+            taken = knn_select(K, cnt, k, kth);
+            if (w >= Wfull) break;
+            if (taken < k) {  // too few in the small window: take the full ball
+                w = Wfull;
+                continue;
+            }
+            int wn = w;
+            while (wn < Wfull) {
+                const double b = (double)(wn + 1) * pitch;
+                if (b * b * (1.0 - 1e-9) > kth) break;
+                ++wn;
+            }
+            if (wn == w) break;  // nothing outside the window can enter the top k
+            w = wn;
+        }
+        double result;
+        if (cnt > (unsigned int)kKnnCap) {
+            // list overflow (full window): successive minima over rescans
+            double last_d = 0.0, acc = 0.0;
+            uint32_t last_i = 0;
+            int tk = 0;
+            for (; tk < k && (unsigned int)tk < cnt; ++tk) {
+                double bd = INFINITY;
+                uint32_t bi = 0xffffffffu;
                 ball_scan(
                     F, tc, sc, K.rt, fi, fj, q, r2,
-                    [&](int, uint32_t mm, const Pos&, double d2, int, int) { consider(d2, mm); },
-                    [&](int) {});
-            }
+                    [&](int, uint32_t mm, const Pos&, double d, int, int) {
+                        const bool after = tk == 0 || d > last_d || (d == last_d && mm > last_i);
+                        if (after && (d < bd || (d == bd && mm < bi))) {
+                            bd = d;
+                            bi = mm;
+                        }
+                    },
+                    [&](int) {}, w);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-                const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (od < bd || (od == bd && oi < bi)) {
-                    bd = od;
-                    bi = oi;
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                    const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (od < bd || (od == bd && oi < bi)) {
+                        bd = od;
+                        bi = oi;
+                    }
                 }
+                acc += rr[bi];
+                last_d = bd;
+                last_i = bi;
             }
-            acc += rr[bi];
-            last_d = bd;
-            last_i = bi;
+            result = cnt == 0 ? rr[n] : acc / (double)tk;
+        } else {
+            // mean over the selection in rank order (denoise.hpp:233-234)
+            double acc = 0.0;
+            if (lane == 0)
+                for (int t = 0; t < taken; ++t) acc += rr[K.sel[t]];
+            result = taken == 0 ? rr[n] : acc / (double)taken;
         }
-        const double result = cnt == 0 ? rr[n] : acc / (double)taken;
         if (lane == 0) F.r[rc ^ 1][n] = result;
         __syncwarp();
     }

@@ -168,3 +168,41 @@ def test_fft_lowpass(gpu):
                                atol=1e-12)
     img = d["img"]
     np.testing.assert_allclose(gpu.fft_lowpass(img, 1.0), img, atol=1e-12)
+
+
+def _recon_with_env(gpu, sc, cfg, env):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        gpu.set_scene(sc)
+        return gpu.reconstruct(cfg)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name", G.SCENE_NAMES + ["config_b"])
+def test_knn_window_pruning_is_exact(gpu, name):
+    """The kNN kernel's window pruning (knn_warps) selects exactly the
+    neighbours of the full-ball scan: bit-identical reconstructions,
+    including the full-size bench frame."""
+    if name == "config_b":
+        import sys
+        from pathlib import Path
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        import bench
+        from paper_1905_06700_b200.scene import simulate
+        spec, seed, cfg, _ = bench.config_b()
+        cfg.max_iters = 4
+        sc = simulate(spec, seed)
+    else:
+        sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_KNN_NO_PRUNE": "1"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
