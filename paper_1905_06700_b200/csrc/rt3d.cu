@@ -45,7 +45,7 @@ __device__ __forceinline__ void gsync(cg::grid_group& grid, const Frame& F, int 
 }
 
 template <int KIND, int G>
-__device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc, int rc, int bc,
+__device__ void cand_loop(const Frame& F, SmemT<G>& sm, cg::grid_group& grid, int tc, int rc, int bc,
                           int sc, int op, int it) {
     while (!ld_cg(&F.ctl->done)) {
         SweepCtx X;
@@ -65,7 +65,7 @@ __device__ void cand_loop(const Frame& F, Smem& sm, cg::grid_group& grid, int tc
 enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
 
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it);
+__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it);
 
 __device__ __forceinline__ void stamp(const Frame& F, int phase) {
     if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -83,10 +83,10 @@ __device__ __forceinline__ void stamp(const Frame& F, int phase) {
 // reads them at entry, the leader writes them back at exit (after at least
 // one barrier, so no block still reads them).
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, 1) stage_kernel(Frame F, int it) {
+__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it) {
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);
     cg::grid_group grid = cg::this_grid();
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     const int prog = F.cfg.program;
@@ -485,7 +485,8 @@ struct rt3d_session {
     int device = 0;
     int nsm = 0;
     cudaStream_t stream = nullptr;
-    int grid_frame = 0;  // cooperative grid of stage_kernel
+    int grid_frame = 0;      // max over the configs (per-block scratch sizing)
+    int grid_frame_c[3] = {0, 0, 0};  // cooperative grid of stage_kernel per lane-group config
     int grid_apss = 0, grid_knn = 0, grid_fit = 0;
     int grid_fft = 0;
     // sensor
@@ -677,9 +678,23 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     {
         const uint32_t mpp = std::max<uint32_t>(s->max_pts_per_pixel, 1);
         const double mean_ev = npix ? (double)s->n_events / npix : 0.0;
-        if (mpp > (uint32_t)kPvc)
-            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: more than %d points in one pixel", kPvc);
-        F.cfg.gsz = (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) ? 4 : 32;
+        if (mpp > (uint32_t)SmemT<32>::kPvc)
+            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: more than %d points in one pixel",
+                        SmemT<32>::kPvc);
+        // sparse pixels: lane groups; groups of 3 (10 pixels per warp chunk)
+        // when groups of 4 would leave more chunks than warps
+        if (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) {
+            const uint64_t warps4 = (uint64_t)s->grid_frame_c[0] * kWarps;
+            const uint64_t chunks4 = (npix + 7) / 8;
+            F.cfg.gsz = (chunks4 > warps4 && !getenv("RT3D_G4")) ? 3 : 4;
+        } else {
+            F.cfg.gsz = 32;
+        }
+        // test hook: force a lane-group config (3, 4 need <= 4 points per pixel)
+        if (const char* gs = getenv("RT3D_GSZ")) {
+            const int g = atoi(gs);
+            if (g == 32 || ((g == 3 || g == 4) && mpp <= 4)) F.cfg.gsz = g;
+        }
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
@@ -689,13 +704,21 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
 }
 
 using StageFn = void (*)(Frame, int);
-// [config][stage]; config 0: 4 lanes per pixel, 1: a warp per pixel
+// lane-group configs of the stage kernels: lanes per pixel
+constexpr int kNumCfg = 3;
+// dynamic shared memory of the stage kernels per config
+static size_t stage_smem(int cfgi) {
+    return cfgi == 0 ? sizeof(SmemT<4>) : cfgi == 1 ? sizeof(SmemT<32>) : sizeof(SmemT<3>);
+}
+// [config][stage]
 static StageFn stage_fn(int cfgi, int st) {
-    static StageFn tab[2][4] = {
+    static StageFn tab[kNumCfg][4] = {
         {stage_kernel<ST_FIRST, 4>, stage_kernel<ST_DEPTH, 4>, stage_kernel<ST_INTENSITY, 4>,
          stage_kernel<ST_TAIL, 4>},
         {stage_kernel<ST_FIRST, 32>, stage_kernel<ST_DEPTH, 32>, stage_kernel<ST_INTENSITY, 32>,
          stage_kernel<ST_TAIL, 32>},
+        {stage_kernel<ST_FIRST, 3>, stage_kernel<ST_DEPTH, 3>, stage_kernel<ST_INTENSITY, 3>,
+         stage_kernel<ST_TAIL, 3>},
     };
     return tab[cfgi][st];
 }
@@ -752,14 +775,15 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
                              s->stream));
     // the frame as a stream-ordered kernel sequence; every decision stays on
     // the device (Ctl), so nothing here waits for the GPU
-    const int cfgi = F.cfg.gsz == 4 ? 0 : 1;
+    const int cfgi = F.cfg.gsz == 4 ? 0 : F.cfg.gsz == 32 ? 1 : 2;
     static const int stage_cls[4] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
                                      RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL};
     auto stage = [&](int st, int it) -> rt3d_status {
         return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
             void* args[] = {&F, &it};
-            CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st), dim3(s->grid_frame),
-                                                 dim3(kBlock), args, sizeof(Smem), s->stream));
+            CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st),
+                                                 dim3(s->grid_frame_c[cfgi]), dim3(kBlock), args,
+                                                 stage_smem(cfgi), s->stream));
             return RT3D_OK;
         });
     };
@@ -914,18 +938,18 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     s->device = device;
     s->nsm = prop.multiProcessorCount;
     CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    int per_sm = 0;
-    per_sm = 1 << 30;
-    for (int c = 0; c < 2; ++c)
+    int per_sm_c[kNumCfg] = {1 << 30, 1 << 30, 1 << 30};
+    for (int c = 0; c < kNumCfg; ++c)
         for (int st = 0; st < 4; ++st) {
             int b = 0;
+            const size_t sz = stage_smem(c);
             CUDA_TRY(cudaFuncSetAttribute((const void*)stage_fn(c, st),
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(Smem)));
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sz));
             CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                &b, (const void*)stage_fn(c, st), kBlock, sizeof(Smem)));
-            per_sm = std::min(per_sm, b);
+                &b, (const void*)stage_fn(c, st), kBlock, sz));
+            per_sm_c[c] = std::min(per_sm_c[c], b);
         }
+    const int per_sm = std::min(std::min(per_sm_c[0], per_sm_c[1]), per_sm_c[2]);
     {
         int a = 0, k = 0;
         CUDA_TRY(cudaFuncSetAttribute(apss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -947,9 +971,12 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
         return fail(RT3D_ERR_CUDA, "rt3d: stage kernel does not fit on an SM");
     }
     const char* env = getenv("RT3D_BLOCKS_PER_SM");
-    int want = env ? atoi(env) : 1;
+    int want = env ? atoi(env) : 2;
     if (want < 1) want = 1;
-    s->grid_frame = s->nsm * std::min(per_sm, want);
+    for (int c = 0; c < kNumCfg; ++c) {
+        s->grid_frame_c[c] = s->nsm * std::min(per_sm_c[c], want);
+        s->grid_frame = std::max(s->grid_frame, s->grid_frame_c[c]);
+    }
     int per_sm_fft = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock, 0));
     s->grid_fft = s->nsm * std::max(1, per_sm_fft);

@@ -27,7 +27,6 @@ namespace cg = cooperative_groups;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kLamCap = 16;        // per-lane rate slots kept in shared memory
-constexpr int kTopSmem = 4096;     // top-of-tree values reduced in shared memory
 constexpr int kMaxReturns = 16;    // InitParams::max_returns supported on device
 constexpr int kKnnFast = 32;       // knn_k handled with an in-register top-k list
 constexpr int kIrfSmem = 256;      // shared IRF samples kept in shared memory
@@ -182,25 +181,36 @@ struct Frame {
 // pixels; their events and points are contiguous CSR ranges, copied into
 // shared memory with coalesced loads in batches of <= kEvc events and
 // <= kPvc points, then processed by lane groups (one pixel per group).
-constexpr int kEvc = 256;
-constexpr int kPvc = 128;
-struct WarpSweepSm {
-    uint2 ev[kEvc];
-    double lam[kEvc], tn[kEvc], t1[kEvc], t2[kEvc];
-    double pt[kPvc], pr[kPvc], pmig[kPvc];
-    int2 plh[kPvc];
+// Staging capacities: lane groups of 4 (sparse frames, <= 4 points and ~12
+// events per pixel) stage 8 pixels per batch; a warp per pixel stages up to
+// 32.  The smaller footprint lets two 256-thread blocks share an SM.
+template <int G>
+struct SweepDims {
+    static constexpr int EVC = G >= 32 ? 256 : 64;
+    static constexpr int PVC = G >= 32 ? 128 : 32;
+};
+template <int EVC, int PVC>
+struct WarpSweepSmT {
+    uint2 ev[EVC];
+    double lam[EVC], tn[EVC], t1[EVC], t2[EVC];
+    double pt[PVC], pr[PVC], pmig[PVC];
+    int2 plh[PVC];
     uint32_t me0[32], mm[32], mn0[32], mnp[32];
     double mb[32], mgain[32];
     uint32_t mdead[32];
     double vals[32];
 };
-struct SweepSmem {
-    WarpSweepSm w[kWarps];
-};
-
-struct Smem {
+constexpr int kTopMin = 1024;  // top-of-tree values always reducible in shared memory
+template <int G>
+struct SmemT {
+    static constexpr int kEvc = SweepDims<G>::EVC;
+    static constexpr int kPvc = SweepDims<G>::PVC;
+    using Warp = WarpSweepSmT<kEvc, kPvc>;
     union {
-        SweepSmem sw;
+        struct {
+            Warp w[kWarps];
+        } sw;
+        double top[kTopMin];
     } u;
     double node[kWarps];
     double wmax[kWarps];
@@ -209,8 +219,6 @@ struct Smem {
     IrfDev irf0;
     double irf_tab[2 * kIrfSmem];
 };
-static_assert(sizeof(SweepSmem) >= sizeof(double) * kTopSmem,
-              "top-of-tree array must fit in the sweep staging");
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -223,7 +231,21 @@ __device__ __forceinline__ T ld_cg(const T* p) {
     return __ldcg(p);
 }
 
-__device__ __forceinline__ const IrfDev& pixel_irf(const Frame& F, const Smem& sm, uint32_t p) {
+// profiling stamp from the calling thread (sweep-internal sub-phases)
+__device__ __forceinline__ void sub_stamp(const Frame& F, int id) {
+    if (F.prof) {
+        unsigned int k = F.ctl->nprof;
+        if (k < F.ctl->prof_cap) {
+            F.prof[2 * k] = (unsigned long long)id;
+            F.prof[2 * k + 1] = globaltimer();
+            F.ctl->nprof = k + 1;
+        }
+    }
+}
+
+
+template <class SM>
+__device__ __forceinline__ const IrfDev& pixel_irf(const Frame& F, const SM& sm, uint32_t p) {
     return F.irf_of_pix ? F.irfs[F.irf_of_pix[p]] : sm.irf0;
 }
 
@@ -240,7 +262,8 @@ __device__ __forceinline__ uint32_t lower_bound_bin(const uint2* ev, uint32_t lo
 // ---------------------------------------------------------------------------
 // block-wide exclusive scan of one u32 per thread
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned int block_exclusive_scan(unsigned int v, Smem& sm,
+template <class SM>
+__device__ __forceinline__ unsigned int block_exclusive_scan(unsigned int v, SM& sm,
                                                              unsigned int& total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned int x = v;
@@ -285,7 +308,8 @@ __device__ __forceinline__ double mf_response(const uint2* ev, uint32_t e0, uint
     return c / f.h_max;
 }
 
-__device__ void phase_init_peaks(const Frame& F, Smem& sm) {
+template <class SM>
+__device__ void phase_init_peaks(const Frame& F, SM& sm) {
     const int lane = threadIdx.x & 31;
     const uint32_t nwarps = gridDim.x * kWarps;
     const int K = F.cfg.K, sep = F.cfg.sep, T = F.bins;
@@ -415,8 +439,8 @@ __device__ __forceinline__ void chunk_range(uint32_t n, uint32_t& c0, uint32_t& 
     if (c1 > n) c1 = n;
 }
 
-template <typename CountFn>
-__device__ void scan_stage_a(const Frame& F, Smem& sm, CountFn count) {
+template <class SM, typename CountFn>
+__device__ void scan_stage_a(const Frame& F, SM& sm, CountFn count) {
     uint32_t c0, c1;
     chunk_range(F.npix, c0, c1);
     unsigned int carry = 0;
@@ -431,7 +455,8 @@ __device__ void scan_stage_a(const Frame& F, Smem& sm, CountFn count) {
 }
 
 // returns this block's base; thread 0 of the last block publishes the total
-__device__ unsigned int scan_stage_b_base(const Frame& F, Smem& sm, unsigned int* total_out) {
+template <class SM>
+__device__ unsigned int scan_stage_b_base(const Frame& F, SM& sm, unsigned int* total_out) {
     unsigned int part = 0;
     for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kBlock) part += ld_cg(&F.btot[b]);
     unsigned int tot;
@@ -443,7 +468,8 @@ __device__ unsigned int scan_stage_b_base(const Frame& F, Smem& sm, unsigned int
 }
 
 // spawn points of init_matched_filter (reconstruct.hpp:219-237, 245-247)
-__device__ void phase_spawn(const Frame& F, Smem& sm, bool baseline) {
+template <class SM>
+__device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
     unsigned int total = 0;
     unsigned int base = scan_stage_b_base(F, sm, &total);
     uint32_t c0, c1;
@@ -569,7 +595,7 @@ __device__ __forceinline__ uint32_t first_event_ge(const uint2* ev, uint32_t e0,
 // sum the reference forms sequentially is accumulated by one lane in the
 // reference's order.  Returns the pixel's nll partial on the group leader.
 template <int KIND, int G>
-__device__ __forceinline__ double sweep_staged_pixel(const Frame& F, WarpSweepSm& W,
+__device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename SmemT<G>::Warp& W,
                                                      const SweepCtx& X, const IrfDev& f, int q,
                                                      const uint2* EV, double* LAM, double* TN,
                                                      double* T1, double* T2, uint32_t pbase,
@@ -714,13 +740,16 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, WarpSweepSm
 // One warp processes tree node pixels [lo, lo+size): meta (lane per pixel),
 // then batches staged in shared memory, then lane groups per pixel.
 template <int KIND, int G>
-__device__ __forceinline__ void sweep_node(const Frame& F, Smem& sm, const SweepCtx& X,
+__device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
                                            uint32_t lo, uint32_t size, double& cmax) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    WarpSweepSm& W = sm.u.sw.w[warp];
+    typename SmemT<G>::Warp& W = sm.u.sw.w[warp];
+    constexpr int kEvc = SmemT<G>::kEvc, kPvc = SmemT<G>::kPvc;
     const int gl = lane % G, grp = lane / G;
     constexpr int NG = 32 / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+    const bool w0t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    if (w0t0) sub_stamp(F, 110);
     // ---- meta, lane per pixel
     if ((uint32_t)lane < size) {
         const uint32_t p = lo + lane;
@@ -750,6 +779,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, Smem& sm, const Sweep
         W.mdead[lane] = dead ? 1u : 0u;
     }
     __syncwarp();
+    if (w0t0) sub_stamp(F, 111);
     const double* tcur = F.t[X.tc];
     const double* rcur = F.r[X.rc];
     for (uint32_t q0 = 0; q0 < size;) {
@@ -805,6 +835,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, Smem& sm, const Sweep
             W.pmig[k] = mg;
         }
         __syncwarp();
+        if (w0t0) sub_stamp(F, 112);
         for (uint32_t qb = q0; qb < q1; qb += NG) {
             const uint32_t q = qb + grp;
             if (q < q1) {
@@ -839,6 +870,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, Smem& sm, const Sweep
             }
         }
         __syncwarp();
+        if (w0t0) sub_stamp(F, 113);
         q0 = q1;
     }
 }
@@ -937,10 +969,11 @@ __device__ void controller(const Frame& F, int op, int it, double v, double cmax
 }
 
 // pairwise tree over the nbn block-node sums, in the last block
-__device__ double top_tree(const Frame& F, Smem& sm) {
+template <class SM>
+__device__ double top_tree(const Frame& F, SM& sm) {
     const uint32_t nb = F.nbn;
-    double* v = reinterpret_cast<double*>(&sm.u.sw);
-    if (nb <= (uint32_t)kTopSmem) {
+    double* v = reinterpret_cast<double*>(&sm.u);
+    if (nb <= (uint32_t)(sizeof(sm.u) / sizeof(double))) {
         for (uint32_t q = threadIdx.x; q < nb; q += kBlock) v[q] = ld_cg(&F.blk[q]);
         __syncthreads();
         for (uint32_t w = nb; w > 1; w >>= 1) {
@@ -967,10 +1000,12 @@ __device__ double top_tree(const Frame& F, Smem& sm) {
 // block = depth-Gb node; the last block to finish reduces the top of the tree
 // and runs the controller.  Caller issues the grid barrier afterwards.
 template <int KIND, int G>
-__device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, const SweepCtx& X,
+__device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, cg::grid_group& grid, const SweepCtx& X,
                              int op, int it) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double cmax = 0.0;
+    const bool b0t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    if (b0t0) sub_stamp(F, 100);
     // phase 1: per-pixel partials, chunks of 32/G consecutive pixels per warp
     // over the whole grid (all SMs busy regardless of the tree shape)
     {
@@ -992,7 +1027,9 @@ __device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, con
         for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
         F.bmax[blockIdx.x] = bm;
     }
+    if (b0t0) sub_stamp(F, 101);
     grid.sync();
+    if (b0t0) sub_stamp(F, 102);
     // phase 2: pairwise_sum's tree over the partials (parallel.hpp:52-61):
     // warp = depth-G node (<= 32 partials), block = depth-Gb node, the last
     // block reduces the top and runs the controller
@@ -1015,6 +1052,7 @@ __device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, con
         }
         __syncthreads();
     }
+    if (b0t0) sub_stamp(F, 103);
     if (threadIdx.x == 0) {
         __threadfence();
         unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
@@ -1023,7 +1061,9 @@ __device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, con
     __syncthreads();
     if (!sm.is_last) return;
     __threadfence();
+    if (threadIdx.x == 0) sub_stamp(F, 104);
     double total = top_tree(F, sm);
+    if (threadIdx.x == 0) sub_stamp(F, 105);
     double gm = 0.0;
     for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) gm = std_max(gm, ld_cg(&F.bmax[b]));
 #pragma unroll
@@ -1035,6 +1075,7 @@ __device__ void tree_sweep_g(const Frame& F, Smem& sm, cg::grid_group& grid, con
         for (int w = 0; w < kWarps; ++w) gm = std_max(gm, sm.wmax[w]);
         F.ctl->ticket = 0;
         controller(F, op, it, total, gm);
+        sub_stamp(F, 106);
     }
 }
 
@@ -1232,7 +1273,8 @@ __device__ __forceinline__ double knn_mean(Enum&& each, int k, double r2, double
 
 // prune (denoise.hpp:241-248) + SceneState::refresh (likelihood.hpp:38-55):
 // per-pixel survivor counts, grid scan, stable scatter into the other buffers
-__device__ void phase_prune_a(const Frame& F, Smem& sm, int rc, int sc) {
+template <class SM>
+__device__ void phase_prune_a(const Frame& F, SM& sm, int rc, int sc) {
     const uint32_t* bo = F.bo[sc];
     const double* r = F.r[rc];
     const double rmin = F.cfg.r_min;
@@ -1243,7 +1285,8 @@ __device__ void phase_prune_a(const Frame& F, Smem& sm, int rc, int sc) {
     });
 }
 
-__device__ void phase_prune_b(const Frame& F, Smem& sm, int tc, int rc, int sc) {
+template <class SM>
+__device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
     unsigned int total = 0;
     unsigned int base = scan_stage_b_base(F, sm, &total);
     uint32_t c0, c1;

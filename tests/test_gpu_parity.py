@@ -206,3 +206,16 @@ def test_knn_window_pruning_is_exact(gpu, name):
     assert np.array_equal(a["points"], b["points"])
     assert np.array_equal(a["background"], b["background"])
     assert np.array_equal(a["trace"], b["trace"])
+
+
+@pytest.mark.parametrize("gsz", ["3", "4", "32"])
+@pytest.mark.parametrize("name", G.SCENE_NAMES)
+def test_lane_group_configs_agree(gpu, name, gsz):
+    """Every lane-group configuration of the likelihood sweeps (3 or 4 lanes
+    per pixel, or a warp per pixel) gives the same bits."""
+    sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_GSZ": gsz})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
