@@ -208,6 +208,9 @@ enum {
     RT3D_KERNEL_CLASSES = 7
 };
 rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable);
+/* Debug aid (RT3D_DEBUG set at session creation): mapped host memory with
+ * per-block progress records and fault records; NULL otherwise. */
+void* rt3d_debug_buffer(rt3d_session* s);
 rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches);
 
 /* Upload the sensor (IRF tables, gain, dead mask) and the photon cube.  They

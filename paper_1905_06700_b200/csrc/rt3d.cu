@@ -32,8 +32,9 @@ static_assert(sizeof(rt3d_point) == 64, "point layout");
 namespace rt3d {
 
 // grid barrier + optional phase stamp (leader thread, after the barrier)
-__device__ __forceinline__ void gsync(cg::grid_group& grid, const Frame& F, int phase) {
-    grid.sync();
+template <class SM>
+__device__ __forceinline__ void gsync(SM& sm, const Frame& F, int phase) {
+    gbar(F, sm, 1000 + phase);
     if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned int k = F.ctl->nprof;
         if (k < F.ctl->prof_cap) {
@@ -43,29 +44,6 @@ __device__ __forceinline__ void gsync(cg::grid_group& grid, const Frame& F, int 
         }
     }
 }
-
-template <int KIND, int G>
-__device__ void cand_loop(const Frame& F, SmemT<G>& sm, cg::grid_group& grid, int tc, int rc, int bc,
-                          int sc, int op, int it) {
-    while (!ld_cg(&F.ctl->done)) {
-        SweepCtx X;
-        X.alpha = ld_cg(&F.ctl->alpha);
-        X.cfloor = 1e-3 * ld_cg(&F.ctl->cmax) + 1e-30;
-        X.tc = tc;
-        X.rc = rc;
-        X.bc = bc;
-        X.sc = sc;
-        X.apply_floor = 0;
-        X.mig_cached = 0;
-        tree_sweep_g<KIND, G>(F, sm, grid, X, op, it);
-        gsync(grid, F, KIND == K_CAND_T ? PH_CAND_T : KIND == K_CAND_R ? PH_CAND_R : PH_CAND_B);
-    }
-}
-
-enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
-
-template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it);
 
 __device__ __forceinline__ void stamp(const Frame& F, int phase) {
     if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -78,6 +56,31 @@ __device__ __forceinline__ void stamp(const Frame& F, int phase) {
     }
 }
 
+template <int KIND, int G>
+__device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc,
+                          int sc, int op, int it) {
+    // sm.c is this block's controller replica: every block sees the same
+    // decisions after each sweep (tree_sweep_g ends with a block barrier)
+    while (!sm.c.done) {
+        SweepCtx X;
+        X.alpha = sm.c.alpha;
+        X.cfloor = 1e-3 * sm.c.cmax + 1e-30;
+        X.tc = tc;
+        X.rc = rc;
+        X.bc = bc;
+        X.sc = sc;
+        X.apply_floor = 0;
+        X.mig_cached = 0;
+        tree_sweep_g<KIND, G>(F, sm, X, op, it);
+        stamp(F, KIND == K_CAND_T ? PH_CAND_T : KIND == K_CAND_R ? PH_CAND_R : PH_CAND_B);
+    }
+}
+
+enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
+
+template <int STAGE, int G>
+__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it);
+
 // One stage of a frame: a cooperative kernel whose phases are separated by
 // grid barriers.  Buffer toggles live in Ctl between kernels; every block
 // reads them at entry, the leader writes them back at exit (after at least
@@ -87,10 +90,9 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);
-    cg::grid_group grid = cg::this_grid();
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     const int prog = F.cfg.program;
-    if (STAGE != ST_FIRST && ld_cg(&F.ctl->stop)) return;
+    if (STAGE != ST_FIRST && (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort))) return;
     if (!F.irf_of_pix) {  // shared IRF: tables in shared memory
         const IrfDev f0 = F.irfs[0];
         if (f0.n <= (uint32_t)kIrfSmem) {
@@ -106,6 +108,16 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
                 sm.irf0.d = sm.irf_tab + kIrfSmem;
             }
         }
+    }
+    if (threadIdx.x == 0) {
+        sm.nsweep = 0;
+        sm.aborted = 0;
+        // controller replica: zero for a new frame, else the state the
+        // previous kernel's block 0 wrote back
+        uint64_t* d = reinterpret_cast<uint64_t*>(&sm.c);
+        const uint64_t* g = reinterpret_cast<const uint64_t*>(F.ctl);
+        for (int k = 0; k < (int)(sizeof(Ctl) / 8); ++k) d[k] = stage == ST_FIRST ? 0ull : ld_cg(&g[k]);
+        if (stage == ST_FIRST) sm.c.P = F.P0;
     }
     __syncthreads();
     int tc, rc, bc, sc;
@@ -144,7 +156,7 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
         if (prog == PROG_RECON || prog == PROG_INIT || prog == PROG_BASELINE ||
             prog == PROG_PEAKS) {
             phase_init_peaks(F, sm);
-            gsync(grid, F, PH_INIT_PEAKS);
+            gsync(sm, F, PH_INIT_PEAKS);
             if (prog == PROG_PEAKS) return;
             const bool baseline = prog == PROG_BASELINE;
             const int s2 = F.s * F.s;
@@ -152,9 +164,9 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
                 uint32_t nv = F.nval[p];
                 return baseline ? (nv > 0 ? 1u : 0u) : nv * (uint32_t)s2;
             });
-            gsync(grid, F, PH_SCAN);
+            gsync(sm, F, PH_SCAN);
             phase_spawn(F, sm, baseline);
-            gsync(grid, F, PH_SPAWN);
+            gsync(sm, F, PH_SPAWN);
             tc = rc = bc = sc = 0;
         }
         if (leader) F.ctl->t_init = globaltimer();
@@ -163,24 +175,22 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
         X0.bc = bc;
         X0.sc = sc;
         if (prog == PROG_NLL) {
-            tree_sweep_g<K_NLL, G>(F, sm, grid, X0, OP_RESULT, 0);
+            tree_sweep_g<K_NLL, G>(F, sm, X0, OP_RESULT, 0);
         } else if (prog == PROG_GRADS) {
-            tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X0, OP_RESULT, 0);
-            gsync(grid, F, PH_GRAD_T);
-            tree_sweep_g<K_GRAD_R, G>(F, sm, grid, X0, OP_RESULT, 0);
-            gsync(grid, F, PH_GRAD_R);
-            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X0, OP_RESULT, 0);
+            tree_sweep_g<K_GRAD_T, G>(F, sm, X0, OP_RESULT, 0);
+            tree_sweep_g<K_GRAD_R, G>(F, sm, X0, OP_RESULT, 0);
+            tree_sweep_g<K_GRAD_B, G>(F, sm, X0, OP_RESULT, 0);
         } else if (prog == PROG_RECON || prog == PROG_PALM) {
             // nll at the initial state + depth gradients (reconstruct.hpp:466)
-            tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X0, OP_GRAD_T_FIRST, 0);
-            gsync(grid, F, PH_GRAD_T);
+            tree_sweep_g<K_GRAD_T, G>(F, sm, X0, OP_GRAD_T_FIRST, 0);
+            stamp(F, PH_GRAD_T);
         }
     } else if constexpr (STAGE == ST_DEPTH) {
         // depth block, reconstruct.hpp:320-350: safeguarded gradient step
         const uint32_t P = ld_cg(&F.ctl->P);
         if (leader) {
             StepDiagDev& d = F.diag[it];
-            d.nll_before = ld_cg(&F.ctl->nll_cur);
+            d.nll_before = sm.c.nll_cur;
             d.points_before = P;
             if (P == 0) {
                 d.blk[0].nll_after_grad = d.blk[0].nll_after_denoise = d.nll_before;
@@ -188,8 +198,8 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
             }
         }
         if (P > 0) {
-            cand_loop<K_CAND_T, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_T, it);
-            if (ld_cg(&F.ctl->accept)) tc ^= 1;
+            cand_loop<K_CAND_T, G>(F, sm, tc, rc, bc, sc, OP_CAND_T, it);
+            if (sm.c.accept) tc ^= 1;
         }
     } else if constexpr (STAGE == ST_INTENSITY) {
         // APSS wrote t[tc^1] (apss_kernel); intensity block, :371-392
@@ -201,10 +211,10 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
             X.rc = rc;
             X.bc = bc;
             X.sc = sc;
-            tree_sweep_g<K_GRAD_R, G>(F, sm, grid, X, OP_GRAD_R, it);
-            gsync(grid, F, PH_GRAD_R);
-            cand_loop<K_CAND_R, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_R, it);
-            if (ld_cg(&F.ctl->accept)) rc ^= 1;
+            tree_sweep_g<K_GRAD_R, G>(F, sm, X, OP_GRAD_R, it);
+            stamp(F, PH_GRAD_R);
+            cand_loop<K_CAND_R, G>(F, sm, tc, rc, bc, sc, OP_CAND_R, it);
+            if (sm.c.accept) rc ^= 1;
         }
     } else if constexpr (STAGE == ST_TAIL) {
         // kNN wrote r[rc^1] (knn_kernel); prune + refresh (:395-397), then
@@ -214,9 +224,9 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
         if (P > 0) {
             rc ^= 1;
             phase_prune_a(F, sm, rc, sc);
-            gsync(grid, F, PH_PRUNE_A);
+            gsync(sm, F, PH_PRUNE_A);
             phase_prune_b(F, sm, tc, rc, sc);
-            gsync(grid, F, PH_PRUNE_B);
+            gsync(sm, F, PH_PRUNE_B);
             tc ^= 1;
             rc ^= 1;
             sc ^= 1;
@@ -224,18 +234,18 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
             X.rc = rc;
             X.bc = bc;
             X.sc = sc;
-            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X, OP_GRAD_B_PRUNED, it);
-            gsync(grid, F, PH_GRAD_B);
+            tree_sweep_g<K_GRAD_B, G>(F, sm, X, OP_GRAD_B_PRUNED, it);
+            stamp(F, PH_GRAD_B);
         } else {
             X.tc = tc;
             X.rc = rc;
             X.bc = bc;
             X.sc = sc;
-            tree_sweep_g<K_GRAD_B, G>(F, sm, grid, X, OP_GRAD_B_EMPTY, it);
-            gsync(grid, F, PH_GRAD_B);
+            tree_sweep_g<K_GRAD_B, G>(F, sm, X, OP_GRAD_B_EMPTY, it);
+            stamp(F, PH_GRAD_B);
         }
-        cand_loop<K_CAND_B, G>(F, sm, grid, tc, rc, bc, sc, OP_CAND_B, it);
-        if (ld_cg(&F.ctl->accept)) bc ^= 1;
+        cand_loop<K_CAND_B, G>(F, sm, tc, rc, bc, sc, OP_CAND_B, it);
+        if (sm.c.accept) bc ^= 1;
         if (F.cfg.bg_mode == 1) {
             const uint32_t nth = gridDim.x * kBlock;
             const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
@@ -245,23 +255,36 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
             double* re2 = F.fft_re + F.npix;
             double* im2 = F.fft_im + F.npix;
             fft_stage1(F.b[bc], re, im, nr, nc, gtid, nth);
-            gsync(grid, F, PH_FFT);
+            gsync(sm, F, PH_FFT);
             fft_stage2(re, im, re2, im2, nr, nc, F.cfg.cutoff, gtid, nth);
-            gsync(grid, F, PH_FFT);
+            gsync(sm, F, PH_FFT);
             fft_stage3(re2, im2, re, im, nr, nc, gtid, nth);
-            gsync(grid, F, PH_FFT);
+            gsync(sm, F, PH_FFT);
             fft_stage4(re, im, F.b[bc], nr, nc, 1, gtid, nth);
-            gsync(grid, F, PH_FFT);
+            gsync(sm, F, PH_FFT);
         }
         X.bc = bc;
         X.apply_floor = 1;
         // t unchanged since GRAD_R (APSS output): mass_in_gate is cached,
         // unless the cloud was empty (no GRAD_R ran)
         X.mig_cached = ld_cg(&F.ctl->P) > 0 ? 1 : 0;
-        tree_sweep_g<K_GRAD_T, G>(F, sm, grid, X, OP_GRAD_T_END, it);
-        gsync(grid, F, PH_GRAD_T);
+        tree_sweep_g<K_GRAD_T, G>(F, sm, X, OP_GRAD_T_END, it);
+        stamp(F, PH_GRAD_T);
     }
-    if (leader) {
+    if (leader && !sm.aborted) {
+        // the controller replica back to F.ctl for the next kernel and the host
+        Ctl* c = F.ctl;
+        c->iterations = sm.c.iterations;
+        c->stop = sm.c.stop;
+        c->done = sm.c.done;
+        c->accept = sm.c.accept;
+        c->bt = sm.c.bt;
+        c->nll_cur = sm.c.nll_cur;
+        c->prev = sm.c.prev;
+        c->init_nll = sm.c.init_nll;
+        c->result = sm.c.result;
+        c->alpha = sm.c.alpha;
+        c->cmax = sm.c.cmax;
         F.ctl->tc = tc;
         F.ctl->rc = rc;
         F.ctl->bc = bc;
@@ -272,20 +295,20 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
 
 __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ld_cg(&F.ctl->stop)) return;
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
     apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw));
 }
 
 __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(Frame F) {
-    if (ld_cg(&F.ctl->stop)) return;
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS_FIT);
     apss_fit_threads(F);
 }
 
 __global__ void __launch_bounds__(kNbrBlock, 4) knn_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    if (ld_cg(&F.ctl->stop)) return;
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
     knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw));
 }
@@ -505,7 +528,7 @@ struct rt3d_session {
     size_t pcap = 0;
     DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot, part, mig[2];
     DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom;
-    DevBuf ctl, diag, trace, outpts, misc, prof;
+    DevBuf ctl, diag, trace, outpts, misc, prof, tblk, tbmax;
     bool profile = false;
     Ctl* h_ctl = nullptr;  // pinned staging
     // state description
@@ -520,6 +543,9 @@ struct rt3d_session {
     int iterations = 0;
     int report_iters_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    unsigned long long* h_dbg = nullptr;  // RT3D_DEBUG records (pinned copy)
+    unsigned long long* d_dbg = nullptr;
+    cudaStream_t side = nullptr;
     // kernel-class timing with CUDA events on the session stream (opt-in)
     bool time_kernels = false;
     struct Timed {
@@ -601,6 +627,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 32));
     F.nev = s->n_events;
     CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
+    CUDA_TRY(s->tblk.ensure((size_t)npix * 16 + 64));
+    CUDA_TRY(s->tbmax.ensure((size_t)npix * 16 + 64));
     CUDA_TRY(s->part.ensure((size_t)npix * 8));
     F.part = s->part.as<double>();
     CUDA_TRY(s->bmax.ensure((size_t)s->grid_frame * 8));
@@ -656,6 +684,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.amom = s->amom.as<double>();
     F.amom_stride = (uint32_t)std::max<size_t>(s->pcap, 1);
     F.ctl = s->ctl.as<Ctl>();
+    F.dbg = s->d_dbg;
     F.prof = nullptr;
     if (s->profile) {
         CUDA_TRY(s->prof.ensure(16ull * 128 * (std::max(max_iters, 1) + 1)));
@@ -664,6 +693,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.diag = s->diag.as<StepDiagDev>();
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
+    F.cfg.blocktree = getenv("RT3D_TREE_OLD") ? 0 : 1;
     {
         // first kNN window: about k fine pixels; no pruning on huge grids
         // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
@@ -695,6 +725,20 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
             const int g = atoi(gs);
             if (g == 32 || ((g == 3 || g == 4) && mpp <= 4)) F.cfg.gsz = g;
         }
+    }
+    {
+        // blocktree block nodes: the shallowest depth <= G whose nodes hold at
+        // most one chunk per warp (ceil(npix / 2^d) <= kWarps * 32/gsz)
+        const uint64_t cap = (uint64_t)kWarps * (uint64_t)(32 / F.cfg.gsz);
+        int d = 0;
+        while (d < F.G && (((uint64_t)npix + (1ull << d) - 1) >> d) > cap) ++d;
+        if (const char* e = getenv("RT3D_TBG")) d = std::max(d, std::min(atoi(e), F.G));
+        F.tb_G = d;
+        F.tb_nbn = 1u << d;
+        F.tblk[0] = s->tblk.as<double>();
+        F.tblk[1] = F.tblk[0] + F.tb_nbn;
+        F.tbmax[0] = s->tbmax.as<double>();
+        F.tbmax[1] = F.tbmax[0] + F.tb_nbn;
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
@@ -821,6 +865,12 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
 rt3d_status read_ctl(rt3d_session* s) {
     CUDA_TRY(cudaMemcpyAsync(s->h_ctl, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
+    const Ctl& c = *s->h_ctl;
+    if (c.abort)
+        return fail(RT3D_ERR_CUDA,
+                    "rt3d: grid barrier watchdog aborted the frame (block %u, op %d, iteration %d, "
+                    "%u of %d blocks arrived, sweep %u)",
+                    c.abort_block, c.abort_op, c.abort_it, c.abort_count, 0, c.abort_nsweep);
     return RT3D_OK;
 }
 
@@ -981,6 +1031,13 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock, 0));
     s->grid_fft = s->nsm * std::max(1, per_sm_fft);
     CUDA_TRY(cudaMallocHost(&s->h_ctl, sizeof(Ctl)));
+    if (getenv("RT3D_DEBUG")) {
+        // device-resident records, read on a side stream (rt3d_debug_peek)
+        CUDA_TRY(cudaMallocHost(&s->h_dbg, 8 * 4096));
+        CUDA_TRY(cudaMalloc(&s->d_dbg, 8 * 4096));
+        CUDA_TRY(cudaMemset(s->d_dbg, 0, 8 * 4096));
+        CUDA_TRY(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+    }
     CUDA_TRY(cudaEventCreate(&s->ev0));
     CUDA_TRY(cudaEventCreate(&s->ev1));
     *out = s;
@@ -994,7 +1051,7 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
                       &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk, &s->part,
                       &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
-                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->amom, &s->ctl, &s->diag,
+                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->amom, &s->tblk, &s->tbmax, &s->ctl, &s->diag,
                       &s->trace, &s->outpts, &s->misc};
     for (DevBuf* b : bufs) b->release();
     for (auto& t : s->timed) {
@@ -1028,6 +1085,16 @@ rt3d_status rt3d_session_profile(rt3d_session* s, int enable) {
     if (!s) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session");
     s->profile = enable != 0;
     return RT3D_OK;
+}
+
+void* rt3d_debug_buffer(rt3d_session* s) {
+    // snapshot of the device records taken on a side stream, so it works
+    // while the session stream is busy
+    if (!s || !s->d_dbg) return nullptr;
+    if (cudaMemcpyAsync(s->h_dbg, s->d_dbg, 8 * 4096, cudaMemcpyDeviceToHost, s->side) != cudaSuccess)
+        return nullptr;
+    cudaStreamSynchronize(s->side);
+    return (void*)s->h_dbg;
 }
 
 rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable) {

@@ -90,7 +90,14 @@ struct Ctl {
     unsigned long long t_start, t_init, t_end;  // %globaltimer stamps (ns)
     unsigned int nprof, prof_cap;
     int tc, rc, bc, sc;    // current buffer of t, r, b and the point structure
+    double red_total, red_max;  // barrier-tree fallback: the last block's results
+    // grid barrier (gbar) and its watchdog: a barrier that waits longer than
+    // kBarrierTimeoutNs aborts the frame instead of hanging the device
+    unsigned int bar_count, bar_gen, abort, abort_block;
+    int abort_op, abort_it;
+    unsigned int abort_count, abort_nsweep;
 };
+constexpr unsigned long long kBarrierTimeoutNs = 2000000000ull;
 
 struct Cfg {
     int program;
@@ -111,6 +118,7 @@ struct Cfg {
     int W;             // fine-pixel window half-width floor(R/pitch)+1
     int knn_w0;        // first kNN window half-width (see knn_warps)
     int set_oog_flags; // palm: OR out-of-gate into flags
+    int blocktree;     // sweeps: block-node aligned phase 1 + replicated top tree
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };
 
@@ -157,6 +165,11 @@ struct Frame {
     double* part;     // npix per-pixel nll partials (sweep -> tree reduction)
     double* blk;      // nbn block-node sums
     double* bmax;     // gridDim block maxima
+    // blocktree sweeps: block nodes at depth tb_G, sums / maxima by sweep parity
+    int tb_G;
+    uint32_t tb_nbn;
+    double* tblk[2];
+    double* tbmax[2];
     uint32_t* cnt;    // npix prefix scratch
     uint32_t* btot;   // gridDim block totals
     double* pk_t;
@@ -171,6 +184,7 @@ struct Frame {
     double* fft_im;
     // control / report
     unsigned long long* prof;  // optional (id, %globaltimer) pairs after each barrier
+    volatile unsigned long long* dbg;  // mapped host memory: progress / fault records
     Ctl* ctl;
     StepDiagDev* diag;
     double* trace;
@@ -216,6 +230,11 @@ struct SmemT {
     double wmax[kWarps];
     unsigned int scan[kWarps + 1];
     int is_last;
+    unsigned int nsweep;  // sweeps run by this kernel (blocktree buffer parity)
+    int aborted;          // the frame was aborted by the barrier watchdog
+    Ctl c;                // this block's replica of the controller state
+    double bpart[kWarps * 32];  // blocktree: the block node's pixel partials
+    double node2[32];
     IrfDev irf0;
     double irf_tab[2 * kIrfSmem];
 };
@@ -741,7 +760,8 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
 // then batches staged in shared memory, then lane groups per pixel.
 template <int KIND, int G>
 __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
-                                           uint32_t lo, uint32_t size, double& cmax) {
+                                           uint32_t lo, uint32_t size, double& cmax,
+                                           double* spart = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     typename SmemT<G>::Warp& W = sm.u.sw.w[warp];
     constexpr int kEvc = SmemT<G>::kEvc, kPvc = SmemT<G>::kPvc;
@@ -861,7 +881,8 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
                                                                 T1, T2, W.mn0[q] - N0, gl, gmask,
                                                                 cmax);
                 if (gl == 0) {
-                    F.part[lo + q] = part;
+                    if (spart) spart[q] = part;
+                    else F.part[lo + q] = part;
                     if (KIND == K_GRAD_B) {
                         F.gb[lo + q] = W.mb[q];
                         F.cb[lo + q] = W.mgain[q];
@@ -878,8 +899,11 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
 // ---------------------------------------------------------------------------
 // Controller: runs on thread 0 of the last block after each grid reduction
 // ---------------------------------------------------------------------------
-__device__ void set_block(const Frame& F, int blk, double cmax, int it) {
-    Ctl* c = F.ctl;
+// The controller state is replicated: every block runs the same decisions on
+// the same reduced values (its own Ctl copy in shared memory); only block 0
+// (`writer`) records the diagnostics and trace, and writes the state back to
+// F.ctl at the end of the kernel.
+__device__ void set_block(const Frame& F, Ctl* c, bool writer, int blk, double cmax, int it) {
     c->cmax = cmax;
     c->alpha = F.cfg.step_auto[blk] ? 1.0 : F.cfg.step[blk];
     c->bt = 0;
@@ -888,7 +912,7 @@ __device__ void set_block(const Frame& F, int blk, double cmax, int it) {
     if (c->alpha <= 0.0) {  // safeguarded_step's empty-step exit (reconstruct.hpp:278-281)
         c->alpha = 0.0;
         c->done = 1;
-        if (it >= 0) {
+        if (it >= 0 && writer) {
             BlockDiagDev& d = F.diag[it].blk[blk];
             d.step_used = 0.0;
             d.backtracks = 0;
@@ -897,8 +921,8 @@ __device__ void set_block(const Frame& F, int blk, double cmax, int it) {
     }
 }
 
-__device__ void controller(const Frame& F, int op, int it, double v, double cmax) {
-    Ctl* c = F.ctl;
+__device__ void controller(const Frame& F, Ctl* c, bool writer, int op, int it, double v,
+                           double cmax) {
     switch (op) {
         case OP_RESULT:
             c->result = v;
@@ -908,36 +932,38 @@ __device__ void controller(const Frame& F, int op, int it, double v, double cmax
             c->nll_cur = v;
             c->init_nll = v;
             c->prev = v;
-            F.trace[0] = v;
-            set_block(F, 0, cmax, 0);
+            if (writer) F.trace[0] = v;
+            set_block(F, c, writer, 0, cmax, 0);
             break;
         case OP_GRAD_T_END: {
-            StepDiagDev& d = F.diag[it];
-            d.blk[2].nll_after_denoise = v;
-            d.nll_after = v;
-            d.points_after = c->P;
-            F.trace[it + 1] = v;
+            if (writer) {
+                StepDiagDev& d = F.diag[it];
+                d.blk[2].nll_after_denoise = v;
+                d.nll_after = v;
+                d.points_after = ld_cg(&F.ctl->P);
+                F.trace[it + 1] = v;
+            }
             c->iterations = it + 1;
             // stop rule, reconstruct.hpp:475-477
             double rel = fabs(c->prev - v) / std_max(1.0, fabs(c->prev));
             c->prev = v;
             c->stop = rel < F.cfg.stop_tol;
             c->nll_cur = v;
-            set_block(F, 0, cmax, it + 1 < F.cfg.max_iters ? it + 1 : -1);
+            set_block(F, c, writer, 0, cmax, it + 1 < F.cfg.max_iters ? it + 1 : -1);
             break;
         }
         case OP_GRAD_R:
-            F.diag[it].blk[0].nll_after_denoise = v;
+            if (writer) F.diag[it].blk[0].nll_after_denoise = v;
             c->nll_cur = v;
-            set_block(F, 1, cmax, it);
+            set_block(F, c, writer, 1, cmax, it);
             break;
         case OP_GRAD_B_PRUNED:
-            F.diag[it].blk[1].nll_after_denoise = v;
+            if (writer) F.diag[it].blk[1].nll_after_denoise = v;
             c->nll_cur = v;
-            set_block(F, 2, cmax, it);
+            set_block(F, c, writer, 2, cmax, it);
             break;
         case OP_GRAD_B_EMPTY:
-            set_block(F, 2, cmax, it);
+            set_block(F, c, writer, 2, cmax, it);
             break;
         case OP_CAND_T:
         case OP_CAND_R:
@@ -957,7 +983,7 @@ __device__ void controller(const Frame& F, int op, int it, double v, double cmax
                     c->done = 1;
                 }
             }
-            if (c->done) {
+            if (c->done && writer) {
                 BlockDiagDev& d = F.diag[it].blk[blk];
                 d.step_used = c->alpha;
                 d.backtracks = c->bt;
@@ -966,6 +992,52 @@ __device__ void controller(const Frame& F, int op, int it, double v, double cmax
             break;
         }
     }
+}
+
+__device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
+    return *reinterpret_cast<const volatile unsigned int*>(p);
+}
+
+// Grid barrier of the cooperative stage kernels (all blocks co-resident):
+// arrival counter + generation, with a watchdog.  Returns true when the frame
+// has been aborted (a barrier waited longer than kBarrierTimeoutNs); every
+// later barrier then returns immediately so that all blocks run out.
+template <class SM>
+__device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
+    __syncthreads();
+    if (threadIdx.x == 0 && !sm.aborted) {
+        // one word: block 0 adds 2^31 - (n - 1), the others 1, so the top bit
+        // flips exactly when the last block arrives and the low bits return
+        // to where they were
+        Ctl* c = F.ctl;
+        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+        __threadfence();
+        const unsigned int old = atomicAdd(&c->bar_count, inc);
+        const unsigned long long t0 = globaltimer();
+        unsigned int spins = 0;
+        while (((ld_volatile(&c->bar_count) ^ old) & 0x80000000u) == 0u) {
+            if (((++spins) & 255u) == 0u) {
+                if (ld_volatile(&c->abort)) {
+                    sm.aborted = 1;
+                    break;
+                }
+                if (globaltimer() - t0 > kBarrierTimeoutNs) {
+                    if (atomicExch(&c->abort, 1u) == 0u) {
+                        c->abort_block = blockIdx.x;
+                        c->abort_op = op;
+                        c->abort_it = it;
+                        c->abort_count = ld_volatile(&c->bar_count);
+                        c->abort_nsweep = sm.nsweep;
+                    }
+                    sm.aborted = 1;
+                    break;
+                }
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    return sm.aborted != 0;
 }
 
 // pairwise tree over the nbn block-node sums, in the last block
@@ -995,90 +1067,205 @@ __device__ double top_tree(const Frame& F, SM& sm) {
     return r;
 }
 
-// One likelihood sweep over all pixels in pairwise_sum's tree order
-// (parallel.hpp:52-61): warp = depth-G node (<= 32 pixels, one per lane),
-// block = depth-Gb node; the last block to finish reduces the top of the tree
-// and runs the controller.  Caller issues the grid barrier afterwards.
-template <int KIND, int G>
-__device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, cg::grid_group& grid, const SweepCtx& X,
-                             int op, int it) {
+// sum over a perfect binary tree (pairs (2q, 2q+1) at every level) of nb
+// values (a power of two) and their max, in every block (all threads return
+// both).  Up to kBlock values are loaded one per thread; above that each
+// thread first reduces a contiguous power-of-two run with the binary-counter
+// form of the same tree.
+template <class SM>
+__device__ void top_all(const double* vals, const double* mx, uint32_t nb, SM& sm, double& total,
+                        double& gm) {
+    double* v = reinterpret_cast<double*>(&sm.u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double cmax = 0.0;
-    const bool b0t0 = blockIdx.x == 0 && threadIdx.x == 0;
-    if (b0t0) sub_stamp(F, 100);
-    // phase 1: per-pixel partials, chunks of 32/G consecutive pixels per warp
-    // over the whole grid (all SMs busy regardless of the tree shape)
-    {
-        constexpr uint32_t NG = 32 / G;
-        const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
-        const uint32_t nchunks = (F.npix + NG - 1) / NG;
-        for (uint32_t c = gw; c < nchunks; c += nw) {
-            const uint32_t lo = c * NG;
-            const uint32_t size = F.npix - lo < NG ? F.npix - lo : NG;
-            sweep_node<KIND, G>(F, sm, X, lo, size, cmax);
+    double m = 0.0;
+    uint32_t w = nb;
+    if (nb <= (uint32_t)kBlock) {
+        if (threadIdx.x < nb) {
+            v[threadIdx.x] = ld_cg(&vals[threadIdx.x]);
+            m = ld_cg(&mx[threadIdx.x]);
         }
+    } else {
+        const uint32_t per = nb / kBlock;
+        double st[16];
+        const uint32_t base = threadIdx.x * per;
+        for (uint32_t j = 0; j < per; ++j) {
+            double x = ld_cg(&vals[base + j]);
+            m = std_max(m, ld_cg(&mx[base + j]));
+            int l = 0;
+            for (uint32_t bb = j; bb & 1u; bb >>= 1, ++l) x = st[l] + x;
+            st[l] = x;
+        }
+        int L = 0;
+        while ((1u << L) < per) ++L;
+        v[threadIdx.x] = st[L];
+        w = kBlock;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cmax = std_max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
-    if (lane == 0) sm.wmax[warp] = cmax;
+    for (int o = 16; o > 0; o >>= 1) m = std_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) sm.wmax[warp] = m;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double bm = 0.0;
-        for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
-        F.bmax[blockIdx.x] = bm;
-    }
-    if (b0t0) sub_stamp(F, 101);
-    grid.sync();
-    if (b0t0) sub_stamp(F, 102);
-    // phase 2: pairwise_sum's tree over the partials (parallel.hpp:52-61):
-    // warp = depth-G node (<= 32 partials), block = depth-Gb node, the last
-    // block reduces the top and runs the controller
-    for (uint32_t bn = blockIdx.x; bn < F.nbn; bn += gridDim.x) {
-        if (warp < F.wpb) {
-            uint32_t lo, size;
-            tree_node_range(F.npix, F.G, bn * (uint32_t)F.wpb + warp, lo, size);
-            double* v = sm.u.sw.w[warp].vals;
-            if ((uint32_t)lane < size) v[lane] = ld_cg(&F.part[lo + lane]);
-            __syncwarp();
-            if (lane == 0) sm.node[warp] = pw32(v, 0, (int)size);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double v[kWarps];
-            for (int w = 0; w < F.wpb; ++w) v[w] = sm.node[w];
-            for (int w = F.wpb; w > 1; w >>= 1)
-                for (int q = 0; q < w / 2; ++q) v[q] = v[2 * q] + v[2 * q + 1];
-            F.blk[bn] = v[0];
-        }
+    for (; w > 1; w >>= 1) {
+        for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock) v[q] = v[2 * q] + v[2 * q + 1];
         __syncthreads();
     }
-    if (b0t0) sub_stamp(F, 103);
-    if (threadIdx.x == 0) {
-        __threadfence();
-        unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
-        sm.is_last = (tk == gridDim.x - 1);
-    }
+    total = v[0];
+    m = 0.0;
+    for (int k = 0; k < kWarps; ++k) m = std_max(m, sm.wmax[k]);
+    gm = m;
     __syncthreads();
-    if (!sm.is_last) return;
-    __threadfence();
-    if (threadIdx.x == 0) sub_stamp(F, 104);
-    double total = top_tree(F, sm);
-    if (threadIdx.x == 0) sub_stamp(F, 105);
-    double gm = 0.0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) gm = std_max(gm, ld_cg(&F.bmax[b]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gm = std_max(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0) sm.wmax[warp] = gm;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        gm = 0.0;
-        for (int w = 0; w < kWarps; ++w) gm = std_max(gm, sm.wmax[w]);
-        F.ctl->ticket = 0;
-        controller(F, op, it, total, gm);
-        sub_stamp(F, 106);
-    }
 }
 
+// One likelihood sweep over all pixels in pairwise_sum's tree order
+// (parallel.hpp:52-61), ending with the controller decision in every block.
+//
+// blocktree (default): block b owns the block nodes b, b + grid, ... at depth
+// tb_G (each at most one chunk per warp); its warps sweep the node's chunks
+// into shared memory, the block reduces the node (pw32 per depth-G node, then
+// their perfect tree) and publishes it; one grid barrier; then every block
+// reduces the block-node sums itself (top_all) and runs its replica of the
+// controller, so the next sweep starts without a second barrier.  Ownership
+// of pixels and points is the same in every sweep, so per-point scratch
+// (gradients, candidates, mass_in_gate) is block-private between barriers.
+//
+// fallback: chunks over all warps, barrier, block nodes at depth Gb, last
+// block reduces the top and publishes it, barrier, every block reads it.
+template <int KIND, int G>
+__device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
+                             int op, int it) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t NG = 32 / G;
+    const bool b0t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    if (b0t0) sub_stamp(F, 100);
+    if (threadIdx.x == 0 && F.dbg)
+        F.dbg[64 + blockIdx.x] = ((unsigned long long)it << 40) | ((unsigned long long)op << 32) |
+                                 (unsigned long long)sm.nsweep;
+    double total = 0.0, gm = 0.0;
+    if (F.cfg.blocktree) {
+        const uint32_t par = sm.nsweep & 1u;
+        double* blk = F.tblk[par];
+        double* bmx = F.tbmax[par];
+        const int dG = F.G - F.tb_G;
+        for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
+            uint32_t blo, bsz;
+            tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
+            const uint32_t nch = (bsz + NG - 1) / NG;
+            double cm = 0.0;
+            for (uint32_t c = warp; c < nch; c += kWarps) {
+                const uint32_t lo = blo + c * NG;
+                const uint32_t size = blo + bsz - lo < NG ? blo + bsz - lo : NG;
+                sweep_node<KIND, G>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cm = std_max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+            if (lane == 0) sm.wmax[warp] = cm;
+            __syncthreads();
+            if (threadIdx.x < (1u << dG)) {
+                uint32_t lo, size;
+                tree_node_range(F.npix, F.G, (bn << dG) | threadIdx.x, lo, size);
+                sm.node2[threadIdx.x] = pw32(sm.bpart, (int)(lo - blo), (int)size);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (uint32_t w = 1u << dG; w > 1; w >>= 1)
+                    for (uint32_t q = 0; q < w / 2; ++q)
+                        sm.node2[q] = sm.node2[2 * q] + sm.node2[2 * q + 1];
+                blk[bn] = sm.node2[0];
+                double bm = 0.0;
+                for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
+                bmx[bn] = bm;
+            }
+            __syncthreads();
+        }
+        if (b0t0) sub_stamp(F, 101);
+        if (gbar(F, sm, op, it)) {
+            if (threadIdx.x == 0) sm.c.done = 1;
+            __syncthreads();
+            return;
+        }
+        if (b0t0) sub_stamp(F, 102);
+        top_all(blk, bmx, F.tb_nbn, sm, total, gm);
+    } else {
+        double cmax = 0.0;
+        {
+            const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+            const uint32_t nchunks = (F.npix + NG - 1) / NG;
+            for (uint32_t c = gw; c < nchunks; c += nw) {
+                const uint32_t lo = c * NG;
+                const uint32_t size = F.npix - lo < NG ? F.npix - lo : NG;
+                sweep_node<KIND, G>(F, sm, X, lo, size, cmax);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cmax = std_max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+        if (lane == 0) sm.wmax[warp] = cmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double bm = 0.0;
+            for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
+            F.bmax[blockIdx.x] = bm;
+        }
+        if (gbar(F, sm, op, it)) {
+            if (threadIdx.x == 0) sm.c.done = 1;
+            __syncthreads();
+            return;
+        }
+        for (uint32_t bn = blockIdx.x; bn < F.nbn; bn += gridDim.x) {
+            if (warp < F.wpb) {
+                uint32_t lo, size;
+                tree_node_range(F.npix, F.G, bn * (uint32_t)F.wpb + warp, lo, size);
+                double* v = sm.u.sw.w[warp].vals;
+                if ((uint32_t)lane < size) v[lane] = ld_cg(&F.part[lo + lane]);
+                __syncwarp();
+                if (lane == 0) sm.node[warp] = pw32(v, 0, (int)size);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double v[kWarps];
+                for (int w = 0; w < F.wpb; ++w) v[w] = sm.node[w];
+                for (int w = F.wpb; w > 1; w >>= 1)
+                    for (int q = 0; q < w / 2; ++q) v[q] = v[2 * q] + v[2 * q + 1];
+                F.blk[bn] = v[0];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
+            sm.is_last = (tk == gridDim.x - 1);
+        }
+        __syncthreads();
+        if (sm.is_last) {
+            __threadfence();
+            double t = top_tree(F, sm);
+            double g = 0.0;
+            for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) g = std_max(g, ld_cg(&F.bmax[b]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) g = std_max(g, __shfl_xor_sync(0xffffffffu, g, o));
+            if (lane == 0) sm.wmax[warp] = g;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                g = 0.0;
+                for (int w = 0; w < kWarps; ++w) g = std_max(g, sm.wmax[w]);
+                F.ctl->ticket = 0;
+                F.ctl->red_total = t;
+                F.ctl->red_max = g;
+            }
+        }
+        if (gbar(F, sm, op, it)) {
+            if (threadIdx.x == 0) sm.c.done = 1;
+            __syncthreads();
+            return;
+        }
+        total = ld_cg(&F.ctl->red_total);
+        gm = ld_cg(&F.ctl->red_max);
+    }
+    if (threadIdx.x == 0) {
+        controller(F, &sm.c, blockIdx.x == 0, op, it, total, gm);
+        sm.nsweep += 1u;
+    }
+    if (b0t0) sub_stamp(F, 103);
+    __syncthreads();
+}
 
 // ---------------------------------------------------------------------------
 // Neighbourhoods on the pinned fine grid.  Inside PALM every point sits at

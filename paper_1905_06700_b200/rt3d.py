@@ -59,6 +59,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
     _bind(L, "rt3d_session_time_kernels", _st, [SS, C.c_int])
     _bind(L, "rt3d_kernel_times", _st, [SS, P(_dbl), P(_u64)])
+    _bind(L, "rt3d_debug_buffer", C.c_void_p, [SS])
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
@@ -96,7 +97,7 @@ def _check(status: int):
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
-    "rt3d_session_time_kernels", "rt3d_kernel_times",
+    "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube",
     "rt3d_reconstruct", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",

@@ -219,3 +219,15 @@ def test_lane_group_configs_agree(gpu, name, gsz):
     assert np.array_equal(a["points"], b["points"])
     assert np.array_equal(a["background"], b["background"])
     assert np.array_equal(a["trace"], b["trace"])
+
+
+@pytest.mark.parametrize("name", G.SCENE_NAMES)
+def test_blocktree_and_barrier_tree_reductions_agree(gpu, name):
+    """The block-node reduction with replicated controllers (default) and
+    the barrier-separated last-block reduction give the same bits."""
+    sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_TREE_OLD": "1"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
