@@ -225,6 +225,20 @@ rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* cube);
  * session stream (returns before the frame finishes). */
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg);
 rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
+
+/* Pipelined frames (a video stream through one session):
+ * rt3d_frame_submit validates `cube`, copies it (pinned host memory avoids a
+ * staging copy) on the session's copy stream into one of two device slots
+ * and enqueues reconstruct (reconstruct.hpp:457-489) plus an end-of-frame copy
+ * of the cloud and background into a result slot; it returns at once with a
+ * ticket.  rt3d_frame_collect waits for that frame and copies its cloud
+ * (cap points at most; *n_points receives the count), background and report
+ * out.  At most two frames are in flight; `cube` must stay valid until its
+ * frame is collected. */
+rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* cube, const rt3d_recon_config* cfg,
+                              uint64_t* ticket);
+rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* points, uint64_t cap,
+                               uint64_t* n_points, double* background, rt3d_report* info);
 /* nll_trace holds iterations+1 values, steps holds iterations entries. */
 rt3d_status rt3d_report_copy(rt3d_session* s, double* nll_trace, rt3d_step_diag* steps);
 

@@ -424,6 +424,35 @@ __global__ void fft_kernel(const double* img, double* out, double* re, double* i
 // SoA state -> AoS rt3d_point (cloud order), positions per world_from_lidar
 // (sensor.hpp:200-203) or the baseline's coarse-centre placement
 // (eval.hpp:116-118).
+// end-of-frame copy for pipelined frames: the cloud (AoS), the background
+// and the controller state into a result slot; P and the buffer toggles are
+// read on the device, so nothing waits for the frame on the host
+__global__ void gather_frame_kernel(Frame F, rt3d_point* out, double* bg, Ctl* ctl_out) {
+    const Ctl* c = F.ctl;
+    const uint32_t P = ld_cg(&c->P);
+    const int tc = ld_cg(&c->tc), rc = ld_cg(&c->rc), bc = ld_cg(&c->bc), sc = ld_cg(&c->sc);
+    const uint32_t nth = gridDim.x * blockDim.x;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t n = tid; n < P; n += nth) {
+        rt3d_point q;
+        const uint32_t p = F.pix[sc][n];
+        q.i = (int)(p / F.cols);
+        q.j = (int)(p % F.cols);
+        q.fi = F.fi[sc][n];
+        q.fj = F.fj[sc][n];
+        q.t = F.t[tc][n];
+        q.intensity = F.r[rc][n];
+        q.flags = F.fl[sc][n];
+        for (int k = 0; k < 7; ++k) q.pad_[k] = 0;
+        q.x = (q.fi + 0.5) * F.pitch;
+        q.y = (q.fj + 0.5) * F.pitch;
+        q.z = q.t * F.bres;
+        out[n] = q;
+    }
+    for (uint32_t p = tid; p < F.npix; p += nth) bg[p] = F.b[bc][p];
+    if (tid == 0) *ctl_out = *c;
+}
+
 __global__ void gather_points_kernel(Frame F, uint32_t P, int tc, int rc, int sc, int baseline,
                                      rt3d_point* out) {
     uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -523,6 +552,19 @@ struct rt3d_session {
     int c_rows = 0, c_cols = 0, c_bins = 0;
     uint64_t n_events = 0;
     DevBuf off, ev;
+    // pipelined frames (rt3d_frame_submit / rt3d_frame_collect): a second
+    // cube slot, a copy stream, result slots
+    DevBuf off2, ev2;
+    int cube_slot = 0;
+    cudaStream_t cstream = nullptr;
+    uint32_t* h_off[2] = {nullptr, nullptr};
+    size_t h_off_cap[2] = {0, 0};
+    cudaEvent_t cube_ready[2] = {nullptr, nullptr}, frame_done[2] = {nullptr, nullptr};
+    DevBuf res_pts[2], res_bg[2], res_ctl[2];
+    Ctl* h_res_ctl = nullptr;
+    uint64_t next_ticket = 0;
+    int inflight[2] = {0, 0};
+    uint64_t slot_ticket[2] = {0, 0};
     // state
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
@@ -617,8 +659,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.gain = s->gain.as<double>();
     F.dead = s->dead.as<uint8_t>();
     F.npix = npix;
-    F.off = s->off.as<uint32_t>();
-    F.ev = s->ev.as<uint2>();
+    F.off = (s->cube_slot ? s->off2 : s->off).as<uint32_t>();
+    F.ev = (s->cube_slot ? s->ev2 : s->ev).as<uint2>();
     F.G = tree_depth(npix);
     F.Gb = std::max(0, F.G - 3);
     F.wpb = 1 << (F.G - F.Gb);
@@ -1059,6 +1101,21 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
         cudaEventDestroy(t.b);
     }
     for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+    if (s->cstream) {
+        cudaStreamSynchronize(s->cstream);
+        for (int k = 0; k < 2; ++k) {
+            cudaEventDestroy(s->cube_ready[k]);
+            cudaEventDestroy(s->frame_done[k]);
+            if (s->h_off[k]) cudaFreeHost(s->h_off[k]);
+            s->res_pts[k].release();
+            s->res_bg[k].release();
+            s->res_ctl[k].release();
+        }
+        cudaFreeHost(s->h_res_ctl);
+        cudaStreamDestroy(s->cstream);
+    }
+    s->off2.release();
+    s->ev2.release();
     s->mig[0].release();
     s->mig[1].release();
     for (int k = 0; k < 2; ++k) {
@@ -1226,18 +1283,15 @@ rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* v) {
     return RT3D_OK;
 }
 
-rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
-    rt3d_status st = require_device(s);
-    if (st) return st;
+// PhotonCube::validate (cube.hpp:84-112) + the u32 offset table
+static rt3d_status validate_cube(const rt3d_cube* c, uint32_t* off32) {
     if (!c) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube");
-    // PhotonCube::validate, cube.hpp:84-112
     if (c->n_rows <= 0 || c->n_cols <= 0 || c->n_bins <= 0)
         return fail(RT3D_ERR_FORMAT, "cube: non-positive dimensions");
     const size_t npix = (size_t)c->n_rows * c->n_cols;
     if (!c->offsets || c->offsets[0] != 0 || c->offsets[npix] != c->n_events)
         return fail(RT3D_ERR_FORMAT, "cube: bad offset table");
     if (c->n_events >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: >= 2^32 events");
-    std::vector<uint32_t> off32(npix + 1);
     for (size_t p = 0; p < npix; ++p) {
         if (c->offsets[p] > c->offsets[p + 1])
             return fail(RT3D_ERR_FORMAT, "cube: negative event range at pixel %zu", p);
@@ -1256,6 +1310,21 @@ rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
         off32[p] = (uint32_t)c->offsets[p];
     }
     off32[npix] = (uint32_t)c->offsets[npix];
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!c) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube");
+    if (c->n_rows <= 0 || c->n_cols <= 0 || c->n_bins <= 0)
+        return fail(RT3D_ERR_FORMAT, "cube: non-positive dimensions");
+    const size_t npix = (size_t)c->n_rows * c->n_cols;
+    std::vector<uint32_t> off32(npix + 1);
+    if ((st = validate_cube(c, off32.data()))) return st;
+    // the device may still read the other slot's / this slot's buffers
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->cube_slot = 0;
     CUDA_TRY(s->off.ensure((npix + 1) * 4));
     CUDA_TRY(s->ev.ensure(std::max<uint64_t>(c->n_events, 1) * 8));
     CUDA_TRY(cudaMemcpyAsync(s->off.p, off32.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
@@ -1315,6 +1384,119 @@ static rt3d_status resolve_state(rt3d_session* s) {
 
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
     return run_init_like(s, cfg, PROG_RECON);
+}
+
+static rt3d_status pipeline_init(rt3d_session* s) {
+    if (s->cstream) return RT3D_OK;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s->cstream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(cudaEventCreateWithFlags(&s->cube_ready[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&s->frame_done[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaMallocHost(&s->h_res_ctl, sizeof(Ctl)));
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* c, const rt3d_recon_config* cfg,
+                              uint64_t* ticket) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!c || !ticket) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube / ticket");
+    if ((st = validate_cfg(cfg))) return st;
+    if (!s->have_sensor) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no sensor set");
+    if (c->n_rows != s->rows || c->n_cols != s->cols || c->n_bins != s->bins)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "likelihood: state/cube dimension mismatch");
+    if ((st = pipeline_init(s))) return st;
+    const int slot = (int)(s->next_ticket & 1u);
+    if (s->inflight[slot])
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: two frames in flight; collect ticket %llu first",
+                    (unsigned long long)s->slot_ticket[slot]);
+    const size_t npix = (size_t)c->n_rows * c->n_cols;
+    if (s->h_off_cap[slot] < npix + 1) {
+        if (s->h_off[slot]) cudaFreeHost(s->h_off[slot]);
+        CUDA_TRY(cudaMallocHost(&s->h_off[slot], (npix + 1) * 4));
+        s->h_off_cap[slot] = npix + 1;
+    }
+    if ((st = validate_cube(c, s->h_off[slot]))) return st;
+    // H2D on the copy stream into this slot (its previous frame was collected)
+    DevBuf& off = slot ? s->off2 : s->off;
+    DevBuf& ev = slot ? s->ev2 : s->ev;
+    CUDA_TRY(off.ensure((npix + 1) * 4));
+    CUDA_TRY(ev.ensure(std::max<uint64_t>(c->n_events, 1) * 8));
+    CUDA_TRY(cudaMemcpyAsync(off.p, s->h_off[slot], (npix + 1) * 4, cudaMemcpyHostToDevice, s->cstream));
+    if (c->n_events)
+        CUDA_TRY(cudaMemcpyAsync(ev.p, c->events, c->n_events * 8, cudaMemcpyHostToDevice, s->cstream));
+    CUDA_TRY(cudaEventRecord(s->cube_ready[slot], s->cstream));
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, s->cube_ready[slot], 0));
+    s->cube_slot = slot;
+    s->have_cube = true;
+    s->c_rows = c->n_rows;
+    s->c_cols = c->n_cols;
+    s->c_bins = c->n_bins;
+    s->n_events = c->n_events;
+    if ((st = run_init_like(s, cfg, PROG_RECON))) return st;
+    // the frame's results into the slot, then the frame's completion event
+    const size_t pcap = (size_t)cfg->init.max_returns * s->s * s->s * npix;
+    CUDA_TRY(s->res_pts[slot].ensure(std::max<size_t>(pcap, 1) * sizeof(rt3d_point)));
+    CUDA_TRY(s->res_bg[slot].ensure(npix * 8));
+    CUDA_TRY(s->res_ctl[slot].ensure(sizeof(Ctl)));
+    Frame F;
+    Cfg g;
+    std::memset(&g, 0, sizeof g);
+    if ((st = build_frame(s, F, g, 1))) return st;
+    gather_frame_kernel<<<s->nsm * 4, 256, 0, s->stream>>>(F, s->res_pts[slot].as<rt3d_point>(),
+                                                          s->res_bg[slot].as<double>(),
+                                                          s->res_ctl[slot].as<Ctl>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(s->frame_done[slot], s->stream));
+    s->inflight[slot] = 1;
+    s->slot_ticket[slot] = s->next_ticket;
+    *ticket = s->next_ticket++;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* pts, uint64_t cap,
+                               uint64_t* n_points, double* background, rt3d_report* info) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    const int slot = (int)(ticket & 1u);
+    if (!s->cstream || !s->inflight[slot] || s->slot_ticket[slot] != ticket)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: ticket %llu is not in flight",
+                    (unsigned long long)ticket);
+    CUDA_TRY(cudaStreamWaitEvent(s->cstream, s->frame_done[slot], 0));
+    CUDA_TRY(cudaMemcpyAsync(s->h_res_ctl, s->res_ctl[slot].p, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                             s->cstream));
+    CUDA_TRY(cudaStreamSynchronize(s->cstream));
+    s->inflight[slot] = 0;
+    const Ctl& c = *s->h_res_ctl;
+    if (c.abort)
+        return fail(RT3D_ERR_CUDA, "rt3d: grid barrier watchdog aborted frame %llu",
+                    (unsigned long long)ticket);
+    if (n_points) *n_points = c.P;
+    if (pts && c.P > cap)
+        return fail(RT3D_ERR_OUT_OF_RANGE, "rt3d: %u points do not fit in %llu", c.P,
+                    (unsigned long long)cap);
+    const size_t npix = (size_t)s->rows * s->cols;
+    if (pts && c.P)
+        CUDA_TRY(cudaMemcpyAsync(pts, s->res_pts[slot].p, (size_t)c.P * sizeof(rt3d_point),
+                                 cudaMemcpyDeviceToHost, s->cstream));
+    if (background)
+        CUDA_TRY(cudaMemcpyAsync(background, s->res_bg[slot].p, npix * 8, cudaMemcpyDeviceToHost,
+                                 s->cstream));
+    CUDA_TRY(cudaStreamSynchronize(s->cstream));
+    if (info) {
+        std::memset(info, 0, sizeof *info);
+        info->iterations = c.iterations;
+        info->points = c.P;
+        info->init_nll = c.init_nll;
+        info->final_nll = c.iterations > 0 ? c.prev : c.init_nll;
+        const double init_s = (double)(c.t_init - c.t_start) * 1e-9;
+        const double tot_s = (double)(c.t_end - c.t_start) * 1e-9;
+        info->init_seconds = init_s;
+        info->iterate_seconds = tot_s - init_s;
+        info->total_seconds = tot_s;
+    }
+    return RT3D_OK;
 }
 
 rt3d_status rt3d_init_matched_filter(rt3d_session* s, const rt3d_init_params* p) {

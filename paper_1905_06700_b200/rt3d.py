@@ -63,6 +63,8 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
+    _bind(L, "rt3d_frame_submit", _st, [SS, P(Cube), P(ReconConfig), P(_u64)])
+    _bind(L, "rt3d_frame_collect", _st, [SS, _u64, P(Point), _u64, P(_u64), P(_dbl), P(Report)])
     _bind(L, "rt3d_report_info", _st, [SS, P(Report)])
     _bind(L, "rt3d_report_copy", _st, [SS, P(_dbl), P(StepDiag)])
     _bind(L, "rt3d_state_size", _st, [SS, P(_u64)])
@@ -99,7 +101,7 @@ EXPORTED = [
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube",
-    "rt3d_reconstruct", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
+    "rt3d_reconstruct", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
     "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
@@ -230,6 +232,38 @@ class Session:
         bg = np.zeros(self.scene.n_pixels)
         _check(lib().rt3d_state_copy(self.h, ptr(pts, Point), ptr(bg, _dbl)))
         return pts[: n.value].copy(), bg
+
+    # -- pipelined frames (rt3d_frame_submit / rt3d_frame_collect) ----------
+    def frame_submit(self, sc: Scene, cfg: Config) -> int:
+        """Enqueue H2D of sc's cube and its reconstruction; returns a ticket.
+        sc's arrays must stay alive until the frame is collected."""
+        cube, cfg_c = sc.cube_c(), cfg.to_c()
+        t = _u64()
+        _check(lib().rt3d_frame_submit(self.h, C.byref(cube), C.byref(cfg_c), C.byref(t)))
+        if not hasattr(self, "_inflight"):
+            self._inflight = {}
+        self._inflight[t.value] = (sc, cube, cfg_c)
+        return t.value
+
+    def frame_collect(self, ticket: int, points: np.ndarray = None, background: np.ndarray = None):
+        """Wait for a submitted frame; fills (or allocates) points / background.
+        Returns (points[:n], background, report dict)."""
+        sc, _, cfg_c = self._inflight[ticket]
+        if points is None:
+            cap = cfg_c.init.max_returns * sc.superres * sc.superres * sc.n_pixels
+            points = np.zeros(max(cap, 1), POINT_DTYPE)
+        if background is None:
+            background = np.zeros(sc.n_pixels)
+        n = _u64()
+        r = Report()
+        try:
+            _check(lib().rt3d_frame_collect(self.h, ticket, ptr(points, Point), len(points),
+                                            C.byref(n), ptr(background, _dbl), C.byref(r)))
+        finally:
+            self._inflight.pop(ticket, None)
+        rep = {"iterations": r.iterations, "points": int(r.points), "init_nll": r.init_nll,
+               "final_nll": r.final_nll, "total_seconds": r.total_seconds}
+        return points[: n.value], background, rep
 
     def reconstruct(self, cfg: Config) -> dict:
         self.reconstruct_async(cfg)
