@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
     }
 }
 
-__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
+__global__ void __launch_bounds__(kNbrBlock, 5) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);

@@ -1308,33 +1308,37 @@ __device__ __forceinline__ void for_each_pinned_neighbor(const Frame& F, int tc,
     }
 }
 
-constexpr int kMom = 25;        // APSS moments: wsum, mean(3), cov(6), M(15)
-constexpr int kRedStride = 21;  // APSS pass-B partials per lane (cov 6 + M 15)
+constexpr int kMom = 19;        // APSS moments: wsum, mean(3), M(15)
+constexpr int kRedStride = 15;  // APSS pass-B partials per lane (M, lower triangle)
 
-// covariance (denoise.hpp:190-195) and Pratt moments (denoise.hpp:73-80) of
-// one member, centred on the mean, into this lane's partials
+// Pratt moments of one member centred on the mean, (w d_r) d_c with
+// d = (1, y, |y|^2) (denoise.hpp:73-80), into this lane's partials.  The
+// weighted covariance of denoise.hpp:190-195 is (w y_r) y_c = M(r+1, c+1)
+// term by term, so it is read off M: members with w == 0 add signed zeros,
+// which leave a partial sum unchanged (partials start at +0 and are never
+// -0), hence including them here and skipping them in M (denoise.hpp:75)
+// give the same bits.
 __device__ __forceinline__ void apss_pass_b(double (&b)[kRedStride], double w, double x, double y,
                                             double z, double m0, double m1, double m2) {
-    const double d0 = x - m0, d1 = y - m1, d2 = z - m2;
-    double wr = w * d0;
-    b[0] += wr * d0;
-    wr = w * d1;
-    b[1] += wr * d0;
-    b[2] += wr * d1;
-    wr = w * d2;
-    b[3] += wr * d0;
-    b[4] += wr * d1;
-    b[5] += wr * d2;
-    if (w > 0.0) {
-        const double dv[5] = {1.0, d0, d1, d2, d0 * d0 + d1 * d1 + d2 * d2};
-        int e = 6;
+    const double y0 = x - m0, y1 = y - m1, y2 = z - m2;
+    const double dv[5] = {1.0, y0, y1, y2, y0 * y0 + y1 * y1 + y2 * y2};
+    int e = 0;
 #pragma unroll
-        for (int r = 0; r < 5; ++r) {
-            const double wa = w * dv[r];
+    for (int r = 0; r < 5; ++r) {
+        const double wa = w * dv[r];
 #pragma unroll
-            for (int c = 0; c <= r; ++c) b[e++] += wa * dv[c];
-        }
+        for (int c = 0; c <= r; ++c) b[e++] += wa * dv[c];
     }
+}
+
+// covariance (lower, row-major) from the Pratt moments
+__device__ __forceinline__ void cov_from_moments(const double* M, double wsum, double cv[6]) {
+    cv[0] = M[lt(1, 1)] / wsum;
+    cv[1] = M[lt(2, 1)] / wsum;
+    cv[2] = M[lt(2, 2)] / wsum;
+    cv[3] = M[lt(3, 1)] / wsum;
+    cv[4] = M[lt(3, 2)] / wsum;
+    cv[5] = M[lt(3, 3)] / wsum;
 }
 
 // the halving tree over 32 lane partials (column `col` of p[32][stride]):
@@ -1388,8 +1392,8 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
         ++c2;
     });
     double cv[6], M[15];
-    for (int e = 0; e < 6; ++e) cv[e] = halving_sum32(&pb[0][0], kRedStride, e) / wsum;
-    for (int e = 0; e < 15; ++e) M[e] = halving_sum32(&pb[0][0], kRedStride, 6 + e);
+    for (int e = 0; e < 15; ++e) M[e] = halving_sum32(&pb[0][0], kRedStride, e);
+    cov_from_moments(M, wsum, cv);
     double e0, e1, e2;
     sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
     if (e2 <= 0.0 || e1 <= 1e-12 * e2) {

@@ -37,7 +37,7 @@ struct ApssMember {
     double z, w;
     int32_t fi, fj;
 };
-constexpr int kApssList = 512;  // ball members kept per warp for the second pass
+constexpr int kApssList = 384;  // ball members kept per warp for the second pass
 struct ApssWarpSm {
     union {
         ApssMember list[kApssList];
@@ -163,8 +163,8 @@ __device__ __forceinline__ double warp_halving_sum(double v) {
 }
 
 // APSS moments over the current state: warp per point, results to F.amom
-// (SoA): [0] wsum (-1: isolated), [1..3] mean, [4..9] cov sums (lower,
-// row-major, not yet / wsum), [10..24] M (lower, row-major).
+// (SoA): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
+// the covariance is read off M, see apss_pass_b).
 __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ApssWarpSm& A = wsm[warp];
@@ -256,7 +256,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
             for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
                 for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
-            F.amom[(size_t)(4 + lane) * S + n] = v[0];
+            F.amom[(size_t)(4 + lane) * S + n] = v[0];  // M, lower row-major
         } else if (lane < kRedStride + 4) {
             const int e = lane - kRedStride;
             F.amom[(size_t)e * S + n] = e == 0 ? wsum : (e == 1 ? m0 : (e == 2 ? m1 : m2));
@@ -284,17 +284,15 @@ __device__ void apss_fit_threads(const Frame& F) {
             fl |= 4u;
         } else {
             const double* mo = F.amom + n;
-            const double c00 = mo[4 * (size_t)S] / wsum, c10 = mo[5 * (size_t)S] / wsum,
-                         c11 = mo[6 * (size_t)S] / wsum, c20 = mo[7 * (size_t)S] / wsum,
-                         c21 = mo[8 * (size_t)S] / wsum, c22 = mo[9 * (size_t)S] / wsum;
+            double M[15], cv[6];
+#pragma unroll
+            for (int k = 0; k < 15; ++k) M[k] = mo[(size_t)(4 + k) * S];
+            cov_from_moments(M, wsum, cv);
             double e0, e1, e2;
-            sym3_eigenvalues(c00, c10, c11, c20, c21, c22, e0, e1, e2);
+            sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
             if (e2 <= 0.0 || e1 <= 1e-12 * e2) {
                 fl |= 4u;
             } else {
-                double M[15];
-#pragma unroll
-                for (int k = 0; k < 15; ++k) M[k] = mo[(size_t)(10 + k) * S];
                 Sphere sp;
                 Pos o;
                 if (!sphere_from_moments(M, mo[S], mo[2 * (size_t)S], mo[3 * (size_t)S], sp) ||

@@ -4,7 +4,7 @@ import csv, io, subprocess, sys
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 kn = sys.argv[3] if len(sys.argv) > 3 else None
-out = subprocess.run(["ncu", "-i", rep] + (["--kernel-name", kn] if kn else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
+out = subprocess.run(["ncu", "-i", rep] + (kn.split() if kn else []) + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 res, cur_file, hdr = [], None, None
