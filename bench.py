@@ -290,7 +290,6 @@ def main():
           for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
-    sess.time_kernels(True)   # CUDA events around every launch, session stream
     with ClockSampler(local) as clocks:
         t_wall0 = time.perf_counter()
         with torch.cuda.stream(stream):
@@ -303,9 +302,24 @@ def main():
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     barrier(world)
+    frame_ms = [a.elapsed_time(b) for a, b in ev]
+    # second timed pass for the per-kernel breakdown: CUDA events around every
+    # launch on the session stream (the value pass replays each frame as one
+    # CUDA graph, inside which events cannot time kernels)
+    sess.time_kernels(True)
+    torch.cuda.synchronize()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    with torch.cuda.stream(stream):
+        for k in range(K):
+            flush.zero_()
+            ev2[k][0].record(stream)
+            sess.reconstruct_async(cfg)
+            ev2[k][1].record(stream)
+    stream.synchronize()
     ktimes = sess.kernel_times()
     sess.time_kernels(False)
-    frame_ms = [a.elapsed_time(b) for a, b in ev]
+    timed_ms = [a.elapsed_time(b) for a, b in ev2]
     dev_s = sum(frame_ms) / 1e3
     dev_s_max = barrier_max(dev_s, world, local)
     value = world * K / dev_s_max
@@ -342,8 +356,9 @@ def main():
     outs = [(torch.empty(P_cap * 64, dtype=torch.uint8, pin_memory=True).numpy().view(POINT_DTYPE),
              torch.empty(sc.n_pixels, dtype=torch.float64, pin_memory=True).numpy())
             for _ in range(2)]
-    tk = sess.frame_submit(sc_pin, cfg)   # warm the pipeline buffers
-    sess.frame_collect(tk, *outs[0])
+    for w in range(2):                      # warm both slots (buffers, graphs)
+        tk = sess.frame_submit(sc_pin, cfg)
+        sess.frame_collect(tk, *outs[w])
     barrier(world)
     t0 = time.perf_counter()
     d2h = 0
@@ -399,6 +414,8 @@ def main():
                 "vs_baseline_ref": "paper GPU 13 ms/frame on Titan Xp (BASELINE.md)",
                 "ms_per_frame_p50": statistics.median(frame_ms),
                 "ms_per_frame_min": min(frame_ms),
+                "ms_per_frame_direct_launch": sum(timed_ms) / K,
+                "frame_launch": "one CUDA graph per frame (captured once, replayed)",
             },
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
@@ -408,12 +425,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic_per_launch(dom),
                          "kernel": KERNEL_NAMES[dom],
-                         "share_of_frame": dc["ms_per_frame"] / (1e3 * dev_s / K),
+                         "share_of_frame": dc["ms_per_frame"] / (sum(timed_ms) / K),
                          "us_per_launch": dc["us_per_launch"],
                          "algorithmic_bytes_per_launch": dc["algorithmic_bytes_per_launch"],
                          "peak_source": peak_src,
                          "timing": "CUDA events on the session stream around every launch, "
-                                   "summed over the timed region"},
+                                   "summed over a second timed pass of K frames launched "
+                                   "directly (the value pass replays each frame as a CUDA "
+                                   "graph)"},
             "frame_roofline": {"achieved": fb / (dev_s / K) / 1e9, "unit": "GB/s",
                                "algorithmic_bytes_per_frame": fb},
             "kernel_classes": classes,

@@ -598,6 +598,15 @@ struct rt3d_session {
     std::vector<cudaEvent_t> ev_pool;
     double kt_ms[RT3D_KERNEL_CLASSES] = {};
     uint64_t kt_n[RT3D_KERNEL_CLASSES] = {};
+    // the last frame's launch sequence as a CUDA graph, replayed while the
+    // frame (its Frame bytes: buffers, config, toggles) and timing mode match
+    struct GraphCache {
+        bool valid = false;
+        Frame F;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t used = 0;
+    } gc[4];  // pipelined frames alternate two cube slots: two live graphs
+    uint64_t gc_clock = 0;
 };
 
 namespace {
@@ -852,10 +861,7 @@ rt3d_status timed_launch(rt3d_session* s, int cls, Fn&& fn) {
     return st;
 }
 
-rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
-    // no host staging: back-to-back async launches must not race on it
-    F.P0 = P_init;
-    F.prof_cap = F.prof ? (uint32_t)(s->prof.cap / 16) : 0u;
+rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
     CUDA_TRY(cudaMemsetAsync(F.ctl, 0, sizeof(Ctl), s->stream));
     CUDA_TRY(cudaMemsetAsync(F.diag, 0, sizeof(StepDiagDev) * std::max(F.cfg.max_iters, 1),
                              s->stream));
@@ -901,6 +907,56 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
             if ((st = stage(ST_TAIL, it))) return st;
         }
     }
+    return RT3D_OK;
+}
+
+static void graph_cache_drop(rt3d_session* s, int k) {
+    auto& g = s->gc[k];
+    if (!g.valid) return;
+    cudaStreamSynchronize(s->stream);
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.exec = nullptr;
+    g.valid = false;
+}
+
+// A frame is ~150 launches; replaying them as a CUDA graph removes the
+// per-launch host cost and most of the inter-kernel gaps.  Graphs are cached
+// by the Frame bytes (buffers, configuration, toggles), least recently used
+// out.  Kernel timing (CUDA events around every launch) and the in-kernel
+// profiler launch directly; so does RT3D_NO_GRAPH=1.
+rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
+    // no host staging: back-to-back async launches must not race on it
+    F.P0 = P_init;
+    F.prof_cap = F.prof ? (uint32_t)(s->prof.cap / 16) : 0u;
+    static const bool no_graph = getenv("RT3D_NO_GRAPH") != nullptr;
+    if (no_graph || F.prof || s->time_kernels) return launch_frame_direct(s, F);
+    const int nc = (int)(sizeof(s->gc) / sizeof(s->gc[0]));
+    int hit = -1, victim = 0;
+    for (int k = 0; k < nc; ++k) {
+        if (s->gc[k].valid && std::memcmp(&s->gc[k].F, &F, sizeof F) == 0) hit = k;
+        if (!s->gc[k].valid || (s->gc[victim].valid && s->gc[k].used < s->gc[victim].used)) victim = k;
+    }
+    if (hit < 0) {
+        hit = victim;
+        graph_cache_drop(s, hit);
+        auto& g = s->gc[hit];
+        CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+        const rt3d_status st = launch_frame_direct(s, F);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(s->stream, &graph);
+        if (st) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        if (ce != cudaSuccess) return fail(RT3D_ERR_CUDA, "CUDA: stream capture: %s", cudaGetErrorString(ce));
+        const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return fail(RT3D_ERR_CUDA, "CUDA: graph instantiate: %s", cudaGetErrorString(ie));
+        g.F = F;
+        g.valid = true;
+    }
+    s->gc[hit].used = ++s->gc_clock;
+    CUDA_TRY(cudaGraphLaunch(s->gc[hit].exec, s->stream));
     return RT3D_OK;
 }
 
@@ -1090,6 +1146,7 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     if (!s) return RT3D_OK;
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
+    for (int k = 0; k < (int)(sizeof(s->gc) / sizeof(s->gc[0])); ++k) graph_cache_drop(s, k);
     DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
                       &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk, &s->part,
                       &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
