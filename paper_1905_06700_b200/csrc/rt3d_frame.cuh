@@ -215,6 +215,13 @@ struct WarpSweepSmT {
     double vals[32];
 };
 constexpr int kTopMin = 1024;  // top-of-tree values always reducible in shared memory
+constexpr int kInitCap = 256;  // matched-filter candidate lags cached per warp
+struct InitWarpSm {
+    int lag[kInitCap];
+    double resp[kInitCap];
+    uint32_t pre[33];
+    int lo[32];
+};
 template <int G>
 struct SmemT {
     static constexpr int kEvc = SweepDims<G>::EVC;
@@ -225,6 +232,7 @@ struct SmemT {
             Warp w[kWarps];
         } sw;
         double top[kTopMin];
+        InitWarpSm init[kWarps];
     } u;
     double node[kWarps];
     double wmax[kWarps];
@@ -348,14 +356,22 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
         int taken[kMaxReturns];
         double tresp[kMaxReturns];
         int nt = 0;
-        for (int round = 0; round < K; ++round) {
-            double best_r = -INFINITY;
-            int best_l = 0x7fffffff;
-            for (uint32_t e = lane; e < m; e += 32) {
+        // candidate lags (reconstruct.hpp:141-148): per event the lags whose
+        // IRF support reaches it, minus the previous event's range, so the
+        // ranges are disjoint and increasing; one lane per candidate computes
+        // its response once, then K greedy rounds pick the best non-clashing
+        // candidate (= the reference's sorted greedy scan, :154-170)
+        InitWarpSm& I = sm.u.init[threadIdx.x >> 5];
+        uint32_t C = 0;
+        bool listed = true;
+        for (uint32_t eb = 0; eb < m; eb += 32) {
+            const uint32_t e = eb + lane;
+            int lo = 0, hi = -1;
+            if (e < m) {
                 const uint32_t bin = __ldg(&F.ev[e0 + e].x);
-                int lo = (int)ceil((double)bin - f.tau_max);
+                lo = (int)ceil((double)bin - f.tau_max);
                 lo = lo < 0 ? 0 : lo;
-                int hi = (int)floor((double)bin - f.tau_min);
+                hi = (int)floor((double)bin - f.tau_min);
                 hi = hi > T - 1 ? T - 1 : hi;
                 if (e > 0) {
                     const uint32_t pb = __ldg(&F.ev[e0 + e - 1].x);
@@ -363,17 +379,76 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
                     phi = phi > T - 1 ? T - 1 : phi;
                     if (phi + 1 > lo) lo = phi + 1;
                 }
-                for (int t0 = lo; t0 <= hi; ++t0) {
+            }
+            const uint32_t len = hi >= lo ? (uint32_t)(hi - lo + 1) : 0u;
+            uint32_t inc = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+            if (C + total > (uint32_t)kInitCap) {
+                listed = false;
+                break;
+            }
+            I.pre[lane] = inc - len;
+            I.lo[lane] = lo;
+            if (lane == 31) I.pre[32] = total;
+            __syncwarp();
+            int j = 0;
+            for (uint32_t c = lane; c < total; c += 32) {
+                while (I.pre[j + 1] <= c) ++j;
+                const int t0 = I.lo[j] + (int)(c - I.pre[j]);
+                I.lag[C + c] = t0;
+                I.resp[C + c] = mf_response(F.ev, e0, m, f, (double)t0);
+            }
+            C += total;
+            __syncwarp();
+        }
+        for (int round = 0; round < K; ++round) {
+            double best_r = -INFINITY;
+            int best_l = 0x7fffffff;
+            if (listed) {
+                for (uint32_t c = lane; c < C; c += 32) {
+                    const int t0 = I.lag[c];
                     bool clash = false;
                     for (int q = 0; q < nt; ++q) {
                         int dd = taken[q] - t0;
                         if ((dd < 0 ? -dd : dd) < sep) clash = true;
                     }
                     if (clash) continue;
-                    double rr = mf_response(F.ev, e0, m, f, (double)t0);
+                    const double rr = I.resp[c];
                     if (rr >= thr && (rr > best_r || (rr == best_r && t0 < best_l))) {
                         best_r = rr;
                         best_l = t0;
+                    }
+                }
+            } else {  // more candidates than the cache: recompute per round
+                for (uint32_t e = lane; e < m; e += 32) {
+                    const uint32_t bin = __ldg(&F.ev[e0 + e].x);
+                    int lo = (int)ceil((double)bin - f.tau_max);
+                    lo = lo < 0 ? 0 : lo;
+                    int hi = (int)floor((double)bin - f.tau_min);
+                    hi = hi > T - 1 ? T - 1 : hi;
+                    if (e > 0) {
+                        const uint32_t pb = __ldg(&F.ev[e0 + e - 1].x);
+                        int phi = (int)floor((double)pb - f.tau_min);
+                        phi = phi > T - 1 ? T - 1 : phi;
+                        if (phi + 1 > lo) lo = phi + 1;
+                    }
+                    for (int t0 = lo; t0 <= hi; ++t0) {
+                        bool clash = false;
+                        for (int q = 0; q < nt; ++q) {
+                            int dd = taken[q] - t0;
+                            if ((dd < 0 ? -dd : dd) < sep) clash = true;
+                        }
+                        if (clash) continue;
+                        double rr = mf_response(F.ev, e0, m, f, (double)t0);
+                        if (rr >= thr && (rr > best_r || (rr == best_r && t0 < best_l))) {
+                            best_r = rr;
+                            best_l = t0;
+                        }
                     }
                 }
             }
@@ -391,6 +466,7 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
             tresp[nt] = best_r;
             ++nt;
         }
+        __syncwarp();
         if (lane == 0) {
             double pt[kMaxReturns], pm[kMaxReturns], pr[kMaxReturns];
             for (int q = 0; q < nt; ++q) {
