@@ -460,10 +460,14 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
             }
             result = cnt == 0 ? rr[n] : acc / (double)tk;
         } else {
-            // mean over the selection in rank order (denoise.hpp:233-234)
+            // mean over the selection in rank order (denoise.hpp:233-234):
+            // the loads in parallel, the sum in rank order
             double acc = 0.0;
-            if (lane == 0)
-                for (int t = 0; t < taken; ++t) acc += rr[K.sel[t]];
+            for (int t0 = 0; t0 < taken; t0 += 32) {
+                const double v = t0 + lane < taken ? rr[K.sel[t0 + lane]] : 0.0;
+                const int nb = taken - t0 < 32 ? taken - t0 : 32;
+                for (int t = 0; t < nb; ++t) acc += __shfl_sync(0xffffffffu, v, t);
+            }
             result = taken == 0 ? rr[n] : acc / (double)taken;
         }
         if (lane == 0) F.r[rc ^ 1][n] = result;
