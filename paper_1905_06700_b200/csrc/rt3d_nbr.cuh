@@ -26,7 +26,7 @@ namespace rt3d {
 
 constexpr int kNbrBlock = 128;
 constexpr int kNbrWarps = kNbrBlock / 32;
-constexpr int kKnnCap = 512;     // per-warp ball list for the kNN selection
+constexpr int kKnnCap = 384;     // per-warp ball list for the kNN selection
 constexpr int kFitBlock = 128;
 
 struct RowTab {
