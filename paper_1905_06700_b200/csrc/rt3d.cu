@@ -57,22 +57,45 @@ __device__ __forceinline__ void stamp(const Frame& F, int phase) {
 }
 
 template <int KIND, int G>
-__device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc,
-                          int sc, int op, int it) {
+__device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, int sc, int op,
+                          int it) {
     // sm.c is this block's controller replica: every block sees the same
     // decisions after each sweep (tree_sweep_g ends with a block barrier)
+    // (the depth block backtracks about half the time on config B, the
+    // intensity block nearly always: two candidates pay for the latter)
+    const bool two = F.cfg.blocktree && ((KIND == K_CAND_R && (F.cfg.two_cand & 1)) ||
+                                         (KIND == K_CAND_T && (F.cfg.two_cand & 2)));
+    SweepCtx X;
+    X.cfloor = 1e-3 * sm.c.cmax + 1e-30;
+    X.tc = tc;
+    X.rc = rc;
+    X.bc = bc;
+    X.sc = sc;
+    X.apply_floor = 0;
+    X.mig_cached = 0;
     while (!sm.c.done) {
-        SweepCtx X;
         X.alpha = sm.c.alpha;
-        X.cfloor = 1e-3 * sm.c.cmax + 1e-30;
-        X.tc = tc;
-        X.rc = rc;
-        X.bc = bc;
-        X.sc = sc;
-        X.apply_floor = 0;
-        X.mig_cached = 0;
+        // two candidates per sweep (alpha, alpha * beta) while another
+        // backtrack is allowed; the controller consumes them in order
+        X.two = two && sm.c.bt + 1 < kMaxBacktracks;
+        X.alpha2 = X.alpha * F.cfg.beta;
         tree_sweep_g<KIND, G>(F, sm, X, op, it);
         stamp(F, KIND == K_CAND_T ? PH_CAND_T : KIND == K_CAND_R ? PH_CAND_R : PH_CAND_B);
+    }
+    if (two && sm.c.accept) {
+        // two-candidate sweeps do not store their candidates: write the
+        // accepted one for this block's own points (same expressions)
+        const double a = sm.c.alpha;
+        for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
+            uint32_t blo, bsz;
+            tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
+            const uint32_t n0 = F.bo[sc][blo], n1 = F.bo[sc][blo + bsz];
+            for (uint32_t n = n0 + threadIdx.x; n < n1; n += kBlock) {
+                if (KIND == K_CAND_T) F.t[tc ^ 1][n] = cand_t_value(F, X, n, F.t[tc][n], a);
+                else F.r[rc ^ 1][n] = cand_r_value(F, X, n, F.r[rc][n], a);
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -678,7 +701,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 32));
     F.nev = s->n_events;
     CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
-    CUDA_TRY(s->tblk.ensure((size_t)npix * 16 + 64));
+    CUDA_TRY(s->tblk.ensure((size_t)npix * 32 + 64));
     CUDA_TRY(s->tbmax.ensure((size_t)npix * 16 + 64));
     CUDA_TRY(s->part.ensure((size_t)npix * 8));
     F.part = s->part.as<double>();
@@ -745,6 +768,9 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
     F.cfg.blocktree = getenv("RT3D_TREE_OLD") ? 0 : 1;
+    // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND)
+    F.cfg.two_cand = getenv("RT3D_ONE_CAND") ? 0
+                     : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND")) : 1;
     {
         // first kNN window: about k fine pixels; no pruning on huge grids
         // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
@@ -790,6 +816,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         F.tblk[1] = F.tblk[0] + F.tb_nbn;
         F.tbmax[0] = s->tbmax.as<double>();
         F.tbmax[1] = F.tbmax[0] + F.tb_nbn;
+        F.tblk2[0] = F.tblk[0] + 2 * F.tb_nbn;
+        F.tblk2[1] = F.tblk[0] + 3 * F.tb_nbn;
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;

@@ -119,6 +119,7 @@ struct Cfg {
     int knn_w0;        // first kNN window half-width (see knn_warps)
     int set_oog_flags; // palm: OR out-of-gate into flags
     int blocktree;     // sweeps: block-node aligned phase 1 + replicated top tree
+    int two_cand;      // depth / intensity candidate sweeps evaluate alpha and alpha * beta
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };
 
@@ -170,6 +171,7 @@ struct Frame {
     uint32_t tb_nbn;
     double* tblk[2];
     double* tbmax[2];
+    double* tblk2[2];  // second-candidate block-node sums
     uint32_t* cnt;    // npix prefix scratch
     uint32_t* btot;   // gridDim block totals
     double* pk_t;
@@ -242,7 +244,9 @@ struct SmemT {
     int aborted;          // the frame was aborted by the barrier watchdog
     Ctl c;                // this block's replica of the controller state
     double bpart[kWarps * 32];  // blocktree: the block node's pixel partials
+    double bpart2[kWarps * 32]; // ... for the second candidate of two-candidate sweeps
     double node2[32];
+    double node2b[32];
     IrfDev irf0;
     double irf_tab[2 * kIrfSmem];
 };
@@ -615,6 +619,8 @@ __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
 // ---------------------------------------------------------------------------
 struct SweepCtx {
     double alpha;
+    double alpha2;   // two-candidate sweeps: the next backtracking step alpha * beta
+    int two;         // evaluate alpha2 as well (K_CAND_T / K_CAND_R, blocktree)
     double cfloor;   // 1e-3 * max(curv) + 1e-30 (reconstruct.hpp:315)
     int tc, rc, bc, sc;
     int apply_floor; // background floor of reconstruct.hpp:427 before the sweep
@@ -832,12 +838,27 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
     return part;
 }
 
+// candidate values of the depth / intensity steps (reconstruct.hpp:324-347,
+// 373-389): dir = grad, or grad / (curv + floor) for "auto" steps
+__device__ __forceinline__ double cand_t_value(const Frame& F, const SweepCtx& X, uint32_t n,
+                                               double t0, double alpha) {
+    double dir = F.gt[n];
+    if (F.cfg.step_auto[0]) dir = dir / (F.ct[n] + X.cfloor);
+    return std_clamp(t0 - alpha * dir, 0.0, F.tlim);
+}
+__device__ __forceinline__ double cand_r_value(const Frame& F, const SweepCtx& X, uint32_t n,
+                                               double r0, double alpha) {
+    double dir = F.gr[n];
+    if (F.cfg.step_auto[1]) dir = dir / (F.cr[n] + X.cfloor);
+    return std_max(0.0, r0 - alpha * dir);
+}
+
 // One warp processes tree node pixels [lo, lo+size): meta (lane per pixel),
 // then batches staged in shared memory, then lane groups per pixel.
 template <int KIND, int G>
 __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
                                            uint32_t lo, uint32_t size, double& cmax,
-                                           double* spart = nullptr) {
+                                           double* spart = nullptr, double* spart2 = nullptr) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     typename SmemT<G>::Warp& W = sm.u.sw.w[warp];
     constexpr int kEvc = SmemT<G>::kEvc, kPvc = SmemT<G>::kPvc;
@@ -892,6 +913,10 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
         const uint32_t E0 = W.me0[q0], N0 = W.mn0[q0];
         if (ev_smem)
             for (uint32_t k = lane; k < ne; k += 32) W.ev[k] = __ldg(&F.ev[E0 + k]);
+        const int ncand = ((KIND == K_CAND_T || KIND == K_CAND_R) && X.two) ? 2 : 1;
+        for (int cand = 0; cand < ncand; ++cand) {
+        const double alpha = cand ? X.alpha2 : X.alpha;
+        (void)alpha;
         // points: candidate values, support, mass_in_gate (lane per point)
         for (uint32_t k = lane; k < npt; k += 32) {
             const uint32_t n = N0 + k;
@@ -901,16 +926,12 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
             const IrfDev& f = pixel_irf(F, sm, lo + qk);
             double t = tcur[n], r = rcur[n];
             if (KIND == K_CAND_T) {
-                double dir = F.gt[n];
-                if (F.cfg.step_auto[0]) dir = dir / (F.ct[n] + X.cfloor);
-                t = std_clamp(t - X.alpha * dir, 0.0, F.tlim);
-                F.t[X.tc ^ 1][n] = t;
+                t = cand_t_value(F, X, n, t, alpha);
+                if (!X.two) F.t[X.tc ^ 1][n] = t;
             }
             if (KIND == K_CAND_R) {
-                double dir = F.gr[n];
-                if (F.cfg.step_auto[1]) dir = dir / (F.cr[n] + X.cfloor);
-                r = std_max(0.0, r - X.alpha * dir);
-                F.r[X.rc ^ 1][n] = r;
+                r = cand_r_value(F, X, n, r, alpha);
+                if (!X.two) F.r[X.rc ^ 1][n] = r;
             }
             int plo, phi;
             irf_support(f, t, F.bins, plo, phi);
@@ -957,7 +978,8 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
                                                                 T1, T2, W.mn0[q] - N0, gl, gmask,
                                                                 cmax);
                 if (gl == 0) {
-                    if (spart) spart[q] = part;
+                    double* sp = cand ? spart2 : spart;
+                    if (sp) sp[q] = part;
                     else F.part[lo + q] = part;
                     if (KIND == K_GRAD_B) {
                         F.gb[lo + q] = W.mb[q];
@@ -965,6 +987,8 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
                     }
                 }
             }
+        }
+        __syncwarp();
         }
         __syncwarp();
         if (w0t0) sub_stamp(F, 113);
@@ -1116,28 +1140,56 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
     return sm.aborted != 0;
 }
 
+// In-place perfect-tree reduction over v[0..w) (pairs (2q, 2q+1) at every
+// level) by the whole block: every level is read into registers before any
+// thread writes, so no thread reads an element another thread of the same
+// level has already overwritten.  w <= 8 * kBlock.
+__device__ __forceinline__ void block_tree_levels(double* v, uint32_t w) {
+    while (w > 1) {
+        const uint32_t h = w / 2;
+        double tmp[8];
+        int k = 0;
+        for (uint32_t q = threadIdx.x; q < h; q += kBlock) tmp[k++] = v[2 * q] + v[2 * q + 1];
+        __syncthreads();
+        k = 0;
+        for (uint32_t q = threadIdx.x; q < h; q += kBlock) v[q] = tmp[k++];
+        __syncthreads();
+        w = h;
+    }
+}
+__device__ __forceinline__ void block_tree_levels_g(double* v, uint32_t w) {
+    while (w > 1) {
+        const uint32_t h = w / 2;
+        for (uint32_t q0 = 0; q0 < h; q0 += 8u * kBlock) {
+            double tmp[8];
+            int k = 0;
+            const uint32_t qe = q0 + 8u * kBlock < h ? q0 + 8u * kBlock : h;
+            for (uint32_t q = q0 + threadIdx.x; q < qe; q += kBlock)
+                tmp[k++] = ld_cg(&v[2 * q]) + ld_cg(&v[2 * q + 1]);
+            __syncthreads();
+            k = 0;
+            for (uint32_t q = q0 + threadIdx.x; q < qe; q += kBlock) v[q] = tmp[k++];
+            __threadfence_block();
+            __syncthreads();
+        }
+        w = h;
+    }
+}
+
 // pairwise tree over the nbn block-node sums, in the last block
 template <class SM>
 __device__ double top_tree(const Frame& F, SM& sm) {
     const uint32_t nb = F.nbn;
     double* v = reinterpret_cast<double*>(&sm.u);
-    if (nb <= (uint32_t)(sizeof(sm.u) / sizeof(double))) {
+    if (nb <= (uint32_t)(sizeof(sm.u) / sizeof(double)) && nb <= 8u * kBlock) {
         for (uint32_t q = threadIdx.x; q < nb; q += kBlock) v[q] = ld_cg(&F.blk[q]);
         __syncthreads();
-        for (uint32_t w = nb; w > 1; w >>= 1) {
-            for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock) v[q] = v[2 * q] + v[2 * q + 1];
-            __syncthreads();
-        }
+        block_tree_levels(v, nb);
         double r = v[0];
         __syncthreads();
         return r;
     }
-    for (uint32_t w = nb; w > 1; w >>= 1) {
-        for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock)
-            F.blk[q] = ld_cg(&F.blk[2 * q]) + ld_cg(&F.blk[2 * q + 1]);
-        __threadfence_block();
-        __syncthreads();
-    }
+    block_tree_levels_g(F.blk, nb);
     double r = ld_cg(&F.blk[0]);
     __syncthreads();
     return r;
@@ -1148,42 +1200,102 @@ __device__ double top_tree(const Frame& F, SM& sm) {
 // both).  Up to kBlock values are loaded one per thread; above that each
 // thread first reduces a contiguous power-of-two run with the binary-counter
 // form of the same tree.
+// perfect binary tree over nb values (a power of two <= 32 * kWarps), two
+// arrays at once: warp w reduces values [32w, 32w + 32) with shuffles (pairs
+// (2q, 2q+1) at every level), then thread 0 combines the warp sums (only
+// thread 0's results are defined).
+template <class SM>
+__device__ void top_small(const double* vals, const double* vals2, const double* mx, uint32_t nb,
+                          SM& sm, double& total, double& total2, double& gm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t span = nb < 32u ? nb : 32u;
+    const uint32_t nw = nb / span;
+    if ((uint32_t)warp < nw) {
+        const uint32_t i = (uint32_t)warp * span + (uint32_t)lane;
+        const bool in = (uint32_t)lane < span;
+        double v = in ? ld_cg(&vals[i]) : 0.0;
+        double v2 = (vals2 && in) ? ld_cg(&vals2[i]) : 0.0;
+        double m = in ? ld_cg(&mx[i]) : 0.0;
+        for (uint32_t o = 1; o < span; o <<= 1) {
+            v = v + __shfl_down_sync(0xffffffffu, v, o);
+            v2 = v2 + __shfl_down_sync(0xffffffffu, v2, o);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = std_max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) {
+            sm.node[warp] = v;
+            sm.node2b[warp] = v2;
+            sm.wmax[warp] = m;
+        }
+    }
+    __syncthreads();
+    // the warp sums' tree by thread 0 (the caller's controller thread); the
+    // caller's closing block barrier orders the next reuse of sm.node
+    if (threadIdx.x == 0) {
+        double t[kWarps], t2[kWarps];
+        double g = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            t[w] = (uint32_t)w < nw ? sm.node[w] : 0.0;
+            t2[w] = (uint32_t)w < nw ? sm.node2b[w] : 0.0;
+            g = (uint32_t)w < nw ? std_max(g, sm.wmax[w]) : g;
+        }
+#pragma unroll
+        for (int w = kWarps; w > 1; w >>= 1)
+#pragma unroll
+            for (int q = 0; q < w / 2; ++q)
+                if ((uint32_t)(2 * q + 1) < nw) {
+                    t[q] = t[2 * q] + t[2 * q + 1];
+                    t2[q] = t2[2 * q] + t2[2 * q + 1];
+                } else if ((uint32_t)(2 * q) < nw) {
+                    t[q] = t[2 * q];
+                    t2[q] = t2[2 * q];
+                }
+        total = t[0];
+        total2 = t2[0];
+        gm = g;
+    }
+}
+
+// sum over a perfect binary tree (pairs (2q, 2q+1) at every level) of nb
+// values (a power of two) and their max, in every block (defined in thread 0,
+// which runs the controller).  Up to 32 * kWarps values: top_small; above that each thread first
+// reduces a contiguous power-of-two run with the binary-counter form of the
+// same tree, then the block reduces the thread sums.
 template <class SM>
 __device__ void top_all(const double* vals, const double* mx, uint32_t nb, SM& sm, double& total,
-                        double& gm) {
+                        double& gm, const double* vals2 = nullptr, double* total2 = nullptr) {
+    if (nb <= 32u * kWarps) {
+        double t2 = 0.0;
+        top_small(vals, vals2, mx, nb, sm, total, t2, gm);
+        if (total2) *total2 = t2;
+        return;
+    }
+    if (vals2) {
+        double g2;
+        top_all(vals2, mx, nb, sm, *total2, g2);
+    }
     double* v = reinterpret_cast<double*>(&sm.u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double m = 0.0;
-    uint32_t w = nb;
-    if (nb <= (uint32_t)kBlock) {
-        if (threadIdx.x < nb) {
-            v[threadIdx.x] = ld_cg(&vals[threadIdx.x]);
-            m = ld_cg(&mx[threadIdx.x]);
-        }
-    } else {
-        const uint32_t per = nb / kBlock;
-        double st[16];
-        const uint32_t base = threadIdx.x * per;
-        for (uint32_t j = 0; j < per; ++j) {
-            double x = ld_cg(&vals[base + j]);
-            m = std_max(m, ld_cg(&mx[base + j]));
-            int l = 0;
-            for (uint32_t bb = j; bb & 1u; bb >>= 1, ++l) x = st[l] + x;
-            st[l] = x;
-        }
-        int L = 0;
-        while ((1u << L) < per) ++L;
-        v[threadIdx.x] = st[L];
-        w = kBlock;
+    const uint32_t per = nb / kBlock;
+    double st[16];
+    const uint32_t base = threadIdx.x * per;
+    for (uint32_t j = 0; j < per; ++j) {
+        double x = ld_cg(&vals[base + j]);
+        m = std_max(m, ld_cg(&mx[base + j]));
+        int l = 0;
+        for (uint32_t bb = j; bb & 1u; bb >>= 1, ++l) x = st[l] + x;
+        st[l] = x;
     }
+    int L = 0;
+    while ((1u << L) < per) ++L;
+    v[threadIdx.x] = st[L];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = std_max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0) sm.wmax[warp] = m;
     __syncthreads();
-    for (; w > 1; w >>= 1) {
-        for (uint32_t q = threadIdx.x; q < w / 2; q += kBlock) v[q] = v[2 * q] + v[2 * q + 1];
-        __syncthreads();
-    }
+    block_tree_levels(v, kBlock);
     total = v[0];
     m = 0.0;
     for (int k = 0; k < kWarps; ++k) m = std_max(m, sm.wmax[k]);
@@ -1215,11 +1327,13 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
     if (threadIdx.x == 0 && F.dbg)
         F.dbg[64 + blockIdx.x] = ((unsigned long long)it << 40) | ((unsigned long long)op << 32) |
                                  (unsigned long long)sm.nsweep;
-    double total = 0.0, gm = 0.0;
+    double total = 0.0, gm = 0.0, total2 = 0.0;
     if (F.cfg.blocktree) {
         const uint32_t par = sm.nsweep & 1u;
         double* blk = F.tblk[par];
         double* bmx = F.tbmax[par];
+        double* blk2 = F.tblk2[par];
+        const bool two = (KIND == K_CAND_T || KIND == K_CAND_R) && X.two;
         const int dG = F.G - F.tb_G;
         for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
             uint32_t blo, bsz;
@@ -1229,7 +1343,8 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             for (uint32_t c = warp; c < nch; c += kWarps) {
                 const uint32_t lo = blo + c * NG;
                 const uint32_t size = blo + bsz - lo < NG ? blo + bsz - lo : NG;
-                sweep_node<KIND, G>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo));
+                sweep_node<KIND, G>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo),
+                                    two ? sm.bpart2 + (lo - blo) : nullptr);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cm = std_max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
@@ -1239,8 +1354,18 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
                 uint32_t lo, size;
                 tree_node_range(F.npix, F.G, (bn << dG) | threadIdx.x, lo, size);
                 sm.node2[threadIdx.x] = pw32(sm.bpart, (int)(lo - blo), (int)size);
+            } else if (two && threadIdx.x >= 32 && threadIdx.x - 32 < (1u << dG)) {
+                uint32_t lo, size;
+                tree_node_range(F.npix, F.G, (bn << dG) | (threadIdx.x - 32), lo, size);
+                sm.node2b[threadIdx.x - 32] = pw32(sm.bpart2, (int)(lo - blo), (int)size);
             }
             __syncthreads();
+            if (two && threadIdx.x == 32) {
+                for (uint32_t w = 1u << dG; w > 1; w >>= 1)
+                    for (uint32_t q = 0; q < w / 2; ++q)
+                        sm.node2b[q] = sm.node2b[2 * q] + sm.node2b[2 * q + 1];
+                blk2[bn] = sm.node2b[0];
+            }
             if (threadIdx.x == 0) {
                 for (uint32_t w = 1u << dG; w > 1; w >>= 1)
                     for (uint32_t q = 0; q < w / 2; ++q)
@@ -1259,7 +1384,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             return;
         }
         if (b0t0) sub_stamp(F, 102);
-        top_all(blk, bmx, F.tb_nbn, sm, total, gm);
+        top_all(blk, bmx, F.tb_nbn, sm, total, gm, two ? blk2 : nullptr, &total2);
     } else {
         double cmax = 0.0;
         {
@@ -1337,6 +1462,10 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
     }
     if (threadIdx.x == 0) {
         controller(F, &sm.c, blockIdx.x == 0, op, it, total, gm);
+        // the second candidate is the next backtracking step: taken exactly
+        // when the first was rejected and the search goes on
+        if ((KIND == K_CAND_T || KIND == K_CAND_R) && X.two && F.cfg.blocktree && !sm.c.done)
+            controller(F, &sm.c, blockIdx.x == 0, op, it, total2, gm);
         sm.nsweep += 1u;
     }
     if (b0t0) sub_stamp(F, 103);

@@ -260,3 +260,26 @@ def test_pipelined_frames_match_reconstruct(gpu):
     # the resident-state API still works after pipelined frames
     again = gpu.reconstruct(cfg)
     assert np.array_equal(again["points"], ref["points"])
+
+
+@pytest.mark.parametrize("name", G.SCENE_NAMES + ["config_b"])
+def test_two_candidate_sweeps_agree(gpu, name):
+    """Depth / intensity candidate sweeps that evaluate alpha and alpha*beta
+    together (default) take exactly the decisions of one-candidate sweeps."""
+    if name == "config_b":
+        import sys
+        from pathlib import Path
+        sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+        import bench
+        from paper_1905_06700_b200.scene import simulate
+        spec, seed, cfg, _ = bench.config_b()
+        cfg.max_iters = 6
+        sc = simulate(spec, seed)
+    else:
+        sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_ONE_CAND": "1"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
+    assert np.array_equal(a["steps"], b["steps"])
