@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parents[1]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 CLASS = {"stage_kernel<0,": "stage_first", "stage_kernel<1,": "stage_depth",
          "stage_kernel<2,": "stage_intensity", "stage_kernel<3,": "stage_tail",
-         "apss_kernel": "apss", "knn_kernel": "knn"}
+         "apss_kernel": "apss", "apss_fit_kernel": "apss_fit", "knn_kernel": "knn"}
 
 
 def kclass(name):
@@ -94,7 +94,7 @@ def main():
     (prof / f"{tag}_ncu_full.md").write_text(
         f"# {tag}: ncu --set full (key metrics per captured launch)\n\n"
         "`ncu --set full --clock-control none --import-source on -k "
-        "regex:\"apss_kernel|knn_kernel|stage_kernel\" -s 10 -c 10 python tools/profile_frame.py 1`\n\n"
+        "regex:\"apss_kernel|apss_fit|knn_kernel|stage_kernel\" -s 7 -c 7 python tools/profile_frame.py 1`\n\n"
         + "\n".join(f) + "\n")
     traffic["_source"] = f"{fpath} ({tag}), dram__bytes_read.sum + dram__bytes_write.sum"
     (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
