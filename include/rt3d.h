@@ -185,6 +185,10 @@ int rt3d_device_count(void);
 rt3d_status rt3d_session_create(int device, rt3d_session** out);
 rt3d_status rt3d_session_destroy(rt3d_session* s);
 rt3d_status rt3d_session_synchronize(rt3d_session* s);
+/* Size the session's cooperative grids so that n_sessions sessions can run
+ * frames concurrently on the device (one per stream, e.g. alternate frames
+ * of a video): each gets 1/n of the co-resident stage blocks.  Default 1. */
+rt3d_status rt3d_session_set_sharing(rt3d_session* s, int n_sessions);
 /* The session's CUDA stream (a cudaStream_t), for callers that time the
  * stream-ordered entry points with their own CUDA events. */
 void* rt3d_session_stream(rt3d_session* s);

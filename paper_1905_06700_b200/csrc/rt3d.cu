@@ -562,6 +562,9 @@ struct rt3d_session {
     cudaStream_t stream = nullptr;
     int grid_frame = 0;      // max over the configs (per-block scratch sizing)
     int grid_frame_c[3] = {0, 0, 0};  // cooperative grid of stage_kernel per lane-group config
+    int per_sm_c[3] = {0, 0, 0};      // co-resident stage blocks per SM per config
+    int want_per_sm = 2;              // RT3D_BLOCKS_PER_SM
+    int sharing = 1;                  // sessions running frames concurrently on the device
     int grid_apss = 0, grid_knn = 0, grid_fit = 0;
     int grid_fft = 0;
     // sensor
@@ -1098,6 +1101,33 @@ int rt3d_device_count(void) {
     return n;
 }
 
+// cooperative stage grids: `sharing` sessions running frames concurrently
+// must fit on the device together (each cooperative grid co-resident)
+static void set_frame_grids(rt3d_session* s) {
+    s->grid_frame = 0;
+    for (int c = 0; c < 3; ++c) {
+        const int per = std::max(1, std::min(s->per_sm_c[c], s->want_per_sm) / std::max(1, s->sharing));
+        s->grid_frame_c[c] = s->nsm * per;
+        s->grid_frame = std::max(s->grid_frame, s->grid_frame_c[c]);
+    }
+}
+
+rt3d_status rt3d_session_set_sharing(rt3d_session* s, int n_sessions) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (n_sessions < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "sharing must be >= 1");
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    for (int k = 0; k < (int)(sizeof(s->gc) / sizeof(s->gc[0])); ++k) graph_cache_drop(s, k);
+    const int old = s->grid_frame;
+    s->sharing = n_sessions;
+    set_frame_grids(s);
+    if (s->grid_frame > old) {  // per-block scratch sized by the grid
+        CUDA_TRY(s->bmax.ensure((size_t)s->grid_frame * 8));
+        CUDA_TRY(s->btot.ensure((size_t)s->grid_frame * 4));
+    }
+    return RT3D_OK;
+}
+
 rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     if (!out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null out");
     *out = nullptr;
@@ -1149,10 +1179,9 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     const char* env = getenv("RT3D_BLOCKS_PER_SM");
     int want = env ? atoi(env) : 2;
     if (want < 1) want = 1;
-    for (int c = 0; c < kNumCfg; ++c) {
-        s->grid_frame_c[c] = s->nsm * std::min(per_sm_c[c], want);
-        s->grid_frame = std::max(s->grid_frame, s->grid_frame_c[c]);
-    }
+    s->want_per_sm = want;
+    for (int c = 0; c < kNumCfg; ++c) s->per_sm_c[c] = per_sm_c[c];
+    set_frame_grids(s);
     int per_sm_fft = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock, 0));
     s->grid_fft = s->nsm * std::max(1, per_sm_fft);

@@ -54,6 +54,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_session_create", _st, [C.c_int, P(SS)])
     _bind(L, "rt3d_session_destroy", _st, [SS])
     _bind(L, "rt3d_session_synchronize", _st, [SS])
+    _bind(L, "rt3d_session_set_sharing", _st, [SS, C.c_int])
     _bind(L, "rt3d_session_stream", C.c_void_p, [SS])
     _bind(L, "rt3d_session_profile", _st, [SS, C.c_int])
     _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
@@ -98,7 +99,7 @@ def _check(status: int):
 
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
-    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
+    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube",
     "rt3d_reconstruct", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
@@ -212,6 +213,10 @@ class Session:
 
     def synchronize(self):
         _check(lib().rt3d_session_synchronize(self.h))
+
+    def set_sharing(self, n_sessions: int):
+        """Size the cooperative grids so n sessions can run frames concurrently."""
+        _check(lib().rt3d_session_set_sharing(self.h, int(n_sessions)))
 
     def report(self) -> dict:
         r = Report()

@@ -283,3 +283,32 @@ def test_two_candidate_sweeps_agree(gpu, name):
     assert np.array_equal(a["background"], b["background"])
     assert np.array_equal(a["trace"], b["trace"])
     assert np.array_equal(a["steps"], b["steps"])
+
+
+def test_concurrent_sessions_match_sequential(gpu):
+    """Two sessions sized to share the device (rt3d_session_set_sharing)
+    reconstructing alternate frames concurrently give the sequential results."""
+    from paper_1905_06700_b200.rt3d import Session
+    sc, cfg, _ = G.scene("two_surface_24")
+    gpu.set_scene(sc)
+    ref = gpu.reconstruct(cfg)
+    ss = [Session(0), Session(0)]
+    try:
+        for s in ss:
+            s.set_scene(sc)
+            s.set_sharing(2)
+        pend = []
+        for k in range(8):
+            s = ss[k % 2]
+            pend.append((s, s.frame_submit(sc, cfg)))
+            if len(pend) == 4:
+                ps, pt = pend.pop(0)
+                pts, bg, _ = ps.frame_collect(pt)
+                assert np.array_equal(pts, ref["points"])
+                assert np.array_equal(bg, ref["background"])
+        for ps, pt in pend:
+            pts, bg, _ = ps.frame_collect(pt)
+            assert np.array_equal(pts, ref["points"])
+    finally:
+        for s in ss:
+            s.close()
