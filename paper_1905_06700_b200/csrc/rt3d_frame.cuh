@@ -98,6 +98,10 @@ struct Ctl {
     unsigned int abort_count, abort_nsweep;
 };
 constexpr unsigned long long kBarrierTimeoutNs = 2000000000ull;
+#ifndef RT3D_BARRIER_SLEEP_NS
+#define RT3D_BARRIER_SLEEP_NS 32
+#endif
+constexpr unsigned int kBarrierSleepNs = RT3D_BARRIER_SLEEP_NS;
 
 struct Cfg {
     int program;
@@ -1116,6 +1120,9 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
         const unsigned long long t0 = globaltimer();
         unsigned int spins = 0;
         while (((ld_volatile(&c->bar_count) ^ old) & 0x80000000u) == 0u) {
+            // back off once the wait is long: the poll loop's issue slots
+            // belong to the other warps on the SM (and to concurrent frames)
+            if (spins > 32u) __nanosleep(kBarrierSleepNs);
             if (((++spins) & 255u) == 0u) {
                 if (ld_volatile(&c->abort)) {
                     sm.aborted = 1;
