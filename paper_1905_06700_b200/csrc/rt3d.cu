@@ -565,6 +565,7 @@ struct rt3d_session {
     int per_sm_c[3] = {0, 0, 0};      // co-resident stage blocks per SM per config
     int want_per_sm = 2;              // RT3D_BLOCKS_PER_SM
     int sharing = 1;                  // sessions running frames concurrently on the device
+    int occ_apss = 1, occ_knn = 1, occ_fit = 1;  // co-resident blocks per SM
     int grid_apss = 0, grid_knn = 0, grid_fit = 0;
     int grid_fft = 0;
     // sensor
@@ -821,6 +822,13 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         F.tbmax[1] = F.tbmax[0] + F.tb_nbn;
         F.tblk2[0] = F.tblk[0] + 2 * F.tb_nbn;
         F.tblk2[1] = F.tblk[0] + 3 * F.tb_nbn;
+    }
+    {
+        const int cfgi = F.cfg.gsz == 4 ? 0 : F.cfg.gsz == 32 ? 1 : 2;
+        if (std::min(s->per_sm_c[cfgi], s->want_per_sm) < s->sharing)
+            return fail(RT3D_ERR_UNSUPPORTED,
+                        "rt3d: this frame's stage kernels do not fit %d sessions per device",
+                        s->sharing);
     }
     F.tc0 = s->tc;
     F.rc0 = s->rc;
@@ -1104,6 +1112,11 @@ int rt3d_device_count(void) {
 // cooperative stage grids: `sharing` sessions running frames concurrently
 // must fit on the device together (each cooperative grid co-resident)
 static void set_frame_grids(rt3d_session* s) {
+    // the neighbour kernels keep their full grids (grid-stride, no barrier):
+    // halving them under sharing measured slower
+    s->grid_apss = s->nsm * s->occ_apss;
+    s->grid_knn = s->nsm * s->occ_knn;
+    s->grid_fit = s->nsm * s->occ_fit;
     s->grid_frame = 0;
     for (int c = 0; c < 3; ++c) {
         const int per = std::max(1, std::min(s->per_sm_c[c], s->want_per_sm) / std::max(1, s->sharing));
@@ -1116,6 +1129,11 @@ rt3d_status rt3d_session_set_sharing(rt3d_session* s, int n_sessions) {
     rt3d_status st = require_device(s);
     if (st) return st;
     if (n_sessions < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "sharing must be >= 1");
+    for (int c = 0; c < 3; c += 2)  // lane-group configs (a warp per pixel: see build_frame)
+        if (std::min(s->per_sm_c[c], s->want_per_sm) < n_sessions)
+            return fail(RT3D_ERR_UNSUPPORTED,
+                        "rt3d: %d sessions cannot share the device (%d stage blocks per SM)",
+                        n_sessions, std::min(s->per_sm_c[c], s->want_per_sm));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     for (int k = 0; k < (int)(sizeof(s->gc) / sizeof(s->gc[0])); ++k) graph_cache_drop(s, k);
     const int old = s->grid_frame;
@@ -1166,11 +1184,11 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
                                                                sizeof(ApssWarpSm) * kNbrWarps));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k, knn_kernel, kNbrBlock,
                                                                sizeof(KnnWarpSm) * kNbrWarps));
-        s->grid_apss = prop.multiProcessorCount * std::max(a, 1);
         int f = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, apss_fit_kernel, kFitBlock, 0));
-        s->grid_fit = prop.multiProcessorCount * std::max(f, 1);
-        s->grid_knn = prop.multiProcessorCount * std::max(k, 1);
+        s->occ_apss = std::max(a, 1);
+        s->occ_knn = std::max(k, 1);
+        s->occ_fit = std::max(f, 1);
     }
     if (per_sm < 1) {
         delete s;
