@@ -88,7 +88,10 @@ __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab
             const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
             const double rem = lim2 - (double)dmin * (double)dmin;
             if (rem >= 0.0) {
-                int wj = (int)floor(sqrt(rem)) + 1;
+                // a member at column offset b has (b pitch)^2 <= R^2 - (a pitch)^2
+                // up to rounding far below the 1e-9 margin of lim2, so
+                // |b| <= floor(sqrt(rem)) bounds every member of this row
+                int wj = (int)floor(sqrt(rem));
                 wj = wj > W ? W : wj;
                 int b0 = fj - wj, b1 = fj + wj;
                 b0 = b0 < 0 ? 0 : b0;
@@ -163,7 +166,7 @@ __device__ __forceinline__ double warp_halving_sum(double v) {
 }
 
 // APSS moments over the current state: warp per point, results to F.amom
-// (SoA): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
+// (kMom doubles per point, one coalesced store per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
 // the covariance is read off M, see apss_pass_b).
 __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -173,7 +176,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
     const int tc = ld_cg(&ctl->tc), sc = ld_cg(&ctl->sc);
     const uint32_t gw = blockIdx.x * kNbrWarps + warp, nw = gridDim.x * kNbrWarps;
     const double R = F.cfg.R, r2 = R * R;
-    const uint32_t S = F.amom_stride;
+    (void)F.amom_stride;
     for (uint32_t n = gw; n < P; n += nw) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
         const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
@@ -207,7 +210,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
         const double wsum = warp_halving_sum(a0);
         double m0 = warp_halving_sum(a1), m1 = warp_halving_sum(a2), m2 = warp_halving_sum(a3);
         if (cnt < (unsigned int)F.cfg.min_nbrs || wsum <= 0.0) {
-            if (lane == 0) F.amom[n] = cnt < (unsigned int)F.cfg.min_nbrs ? -1.0 : wsum;
+            if (lane == 0) F.amom[(size_t)n * kMom] = cnt < (unsigned int)F.cfg.min_nbrs ? -1.0 : wsum;
             __syncwarp();
             continue;
         }
@@ -256,10 +259,10 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
             for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
                 for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
-            F.amom[(size_t)(4 + lane) * S + n] = v[0];  // M, lower row-major
+            F.amom[(size_t)n * kMom + 4 + lane] = v[0];  // M, lower row-major
         } else if (lane < kRedStride + 4) {
             const int e = lane - kRedStride;
-            F.amom[(size_t)e * S + n] = e == 0 ? wsum : (e == 1 ? m0 : (e == 2 ? m1 : m2));
+            F.amom[(size_t)n * kMom + e] = e == 0 ? wsum : (e == 1 ? m0 : (e == 2 ? m1 : m2));
         }
         __syncwarp();
     }
@@ -271,22 +274,22 @@ __device__ void apss_fit_threads(const Frame& F) {
     const Ctl* ctl = F.ctl;
     const uint32_t P = ld_cg(&ctl->P);
     const int tc = ld_cg(&ctl->tc), sc = ld_cg(&ctl->sc);
-    const uint32_t S = F.amom_stride;
+    (void)F.amom_stride;
     for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < P; n += gridDim.x * blockDim.x) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
         const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
         uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
         double z = q.z;
-        const double wsum = F.amom[n];
+        const double* mo = F.amom + (size_t)n * kMom;
+        const double wsum = mo[0];
         if (wsum < 0.0) {
             fl |= 1u;  // isolated
         } else if (wsum <= 0.0) {
             fl |= 4u;
         } else {
-            const double* mo = F.amom + n;
             double M[15], cv[6];
 #pragma unroll
-            for (int k = 0; k < 15; ++k) M[k] = mo[(size_t)(4 + k) * S];
+            for (int k = 0; k < 15; ++k) M[k] = mo[4 + k];
             cov_from_moments(M, wsum, cv);
             double e0, e1, e2;
             sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
@@ -295,7 +298,7 @@ __device__ void apss_fit_threads(const Frame& F) {
             } else {
                 Sphere sp;
                 Pos o;
-                if (!sphere_from_moments(M, mo[S], mo[2 * (size_t)S], mo[3 * (size_t)S], sp) ||
+                if (!sphere_from_moments(M, mo[1], mo[2], mo[3], sp) ||
                     !project_sphere(sp, F.cfg.eps, q.x, q.y, q.z, o.x, o.y, o.z))
                     fl |= 4u;
                 else
