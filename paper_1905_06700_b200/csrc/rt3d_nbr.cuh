@@ -45,6 +45,7 @@ struct ApssWarpSm {
     } u;
     double chunk[32][4];  // the current scan chunk's members (w, x, y, z)
     RowTab rt;
+    RowTab rtn[2];  // single-batch windows: this point's and the next point's rows
 };
 struct KnnWarpSm {
     double d2[kKnnCap];
@@ -60,100 +61,132 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
-// Ball of q over the window; visit(rank, mm, pos, d2, fi, fj) on member lanes,
-// flush(n_members) once per chunk (warp-synchronous).
+// Window rows of point (fi, fj): coarse rows ci0..ci1 (fine window of
+// half-width W, clipped).
+__device__ __forceinline__ void window_rows(const Frame& F, int fi, int W, int& ci0, int& ci1) {
+    int a0 = fi - W, a1 = fi + W;
+    a0 = a0 < 0 ? 0 : a0;
+    a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
+    ci0 = a0 / F.s;
+    ci1 = a1 / F.s;
+}
+
+// Candidate range of window row ci = rb + lane (disc-culled columns): the
+// global loads of a row batch, kept in registers until rows_finish.
+__device__ __forceinline__ void rows_load(const Frame& F, int sc, int fi, int fj, int W, int rb,
+                                          int ci1, uint32_t& m0, uint32_t& len) {
+    const int lane = threadIdx.x & 31, s = F.s;
+    const double rw = F.cfg.R / F.pitch;
+    const double lim2 = rw * rw * (1.0 + 1e-9);
+    const int ci = rb + lane;
+    m0 = 0;
+    len = 0;
+    if (ci <= ci1) {
+        const int r_lo = ci * s, r_hi = r_lo + s - 1;
+        const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
+        const double rem = lim2 - (double)dmin * (double)dmin;
+        if (rem >= 0.0) {
+            // a member at column offset b has (b pitch)^2 <= R^2 - (a pitch)^2
+            // up to rounding far below the 1e-9 margin of lim2, so
+            // |b| <= floor(sqrt(rem)) bounds every member of this row
+            int wj = (int)floor(sqrt(rem));
+            wj = wj > W ? W : wj;
+            int b0 = fj - wj, b1 = fj + wj;
+            b0 = b0 < 0 ? 0 : b0;
+            b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
+            const uint32_t prow = (uint32_t)ci * F.cols;
+            const uint32_t* bo = F.bo[sc];
+            m0 = bo[prow + b0 / s];
+            len = bo[prow + b1 / s + 1] - m0;
+        }
+    }
+}
+
+// prefix of the row batch into rt; returns the batch's candidate count
+__device__ __forceinline__ uint32_t rows_finish(RowTab& rt, uint32_t m0, uint32_t len) {
+    const int lane = threadIdx.x & 31;
+    uint32_t inc = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    rt.pre[lane] = inc - len;
+    rt.m0[lane] = m0;
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    if (lane == 31) rt.pre[32] = total;
+    __syncwarp();
+    return total;
+}
+
+// The candidates of one row batch (rt, total) against q: visit(rank, mm,
+// pos, d2, fi, fj) on member lanes, flush(n_members) once per chunk of 32
+// candidates (warp-synchronous); the next chunk's loads are issued before the
+// current chunk is processed.
+template <typename Visit, typename Flush>
+__device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const RowTab& rt,
+                                          uint32_t total, const Pos& q, double r2, Visit visit,
+                                          Flush flush) {
+    const int lane = threadIdx.x & 31;
+    const double* tt = F.t[tc];
+    const int32_t* FI = F.fi[sc];
+    const int32_t* FJ = F.fj[sc];
+    int j = 0;
+    auto locate = [&](uint32_t f) -> uint32_t {
+        while (rt.pre[j + 1] <= f) ++j;
+        return rt.m0[j] + (f - rt.pre[j]);
+    };
+    bool v = (uint32_t)lane < total;
+    uint32_t mm = v ? locate(lane) : 0u;
+    int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
+    double ctt = v ? tt[mm] : 0.0;
+    for (uint32_t fb = 0; fb < total; fb += 32) {
+        const uint32_t f2 = fb + 32 + lane;
+        const bool v2 = f2 < total;
+        const uint32_t mm2 = v2 ? locate(f2) : 0u;
+        const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
+        const double ntt = v2 ? tt[mm2] : 0.0;
+        bool ok = false;
+        Pos o;
+        double d2 = 0.0;
+        if (v) {
+            o.x = (cfi + 0.5) * F.pitch;
+            o.y = (cfj + 0.5) * F.pitch;
+            o.z = ctt * F.bres;
+            const double dx = o.x - q.x, dy = o.y - q.y, dz = o.z - q.z;
+            d2 = dx * dx + dy * dy + dz * dz;
+            ok = d2 <= r2;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+        if (bal) {
+            if (ok) visit(__popc(bal & lanemask_lt()), mm, o, d2, cfi, cfj);
+            __syncwarp();
+            flush(__popc(bal));
+            __syncwarp();
+        }
+        v = v2;
+        mm = mm2;
+        cfi = nfi;
+        cfj = nfj;
+        ctt = ntt;
+    }
+    __syncwarp();
+}
+
+// Ball of q over the window, all row batches.
 template <typename Visit, typename Flush>
 __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab& rt, int fi,
                                           int fj, const Pos& q, double r2, Visit visit,
                                           Flush flush, int Wq = -1) {
-    const int lane = threadIdx.x & 31;
     // Wq < W restricts the scan to the fine window of half-width Wq (kNN)
-    const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W, s = F.s;
-    const double rw = F.cfg.R / F.pitch;
-    const double lim2 = rw * rw * (1.0 + 1e-9);
-    int a0 = fi - W, a1 = fi + W;
-    a0 = a0 < 0 ? 0 : a0;
-    a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
-    const int ci0 = a0 / s, ci1 = a1 / s;
-    const uint32_t* bo = F.bo[sc];
-    const double* tt = F.t[tc];
-    const int32_t* FI = F.fi[sc];
-    const int32_t* FJ = F.fj[sc];
+    const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W;
+    int ci0, ci1;
+    window_rows(F, fi, W, ci0, ci1);
     for (int rb = ci0; rb <= ci1; rb += 32) {
-        // one window row per lane: its candidate range (disc-culled columns)
-        const int ci = rb + lane;
-        uint32_t m0 = 0, len = 0;
-        if (ci <= ci1) {
-            const int r_lo = ci * s, r_hi = r_lo + s - 1;
-            const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
-            const double rem = lim2 - (double)dmin * (double)dmin;
-            if (rem >= 0.0) {
-                // a member at column offset b has (b pitch)^2 <= R^2 - (a pitch)^2
-                // up to rounding far below the 1e-9 margin of lim2, so
-                // |b| <= floor(sqrt(rem)) bounds every member of this row
-                int wj = (int)floor(sqrt(rem));
-                wj = wj > W ? W : wj;
-                int b0 = fj - wj, b1 = fj + wj;
-                b0 = b0 < 0 ? 0 : b0;
-                b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
-                const uint32_t prow = (uint32_t)ci * F.cols;
-                m0 = bo[prow + b0 / s];
-                len = bo[prow + b1 / s + 1] - m0;
-            }
-        }
-        uint32_t inc = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        rt.pre[lane] = inc - len;
-        rt.m0[lane] = m0;
-        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-        if (lane == 31) rt.pre[32] = total;
-        __syncwarp();
-        // chunks of 32 candidates; the next chunk's loads are issued before
-        // the current chunk is processed (software pipelining)
-        int j = 0;
-        auto locate = [&](uint32_t f) -> uint32_t {
-            while (rt.pre[j + 1] <= f) ++j;
-            return rt.m0[j] + (f - rt.pre[j]);
-        };
-        bool v = (uint32_t)lane < total;
-        uint32_t mm = v ? locate(lane) : 0u;
-        int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
-        double ctt = v ? tt[mm] : 0.0;
-        for (uint32_t fb = 0; fb < total; fb += 32) {
-            const uint32_t f2 = fb + 32 + lane;
-            const bool v2 = f2 < total;
-            const uint32_t mm2 = v2 ? locate(f2) : 0u;
-            const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
-            const double ntt = v2 ? tt[mm2] : 0.0;
-            bool ok = false;
-            Pos o;
-            double d2 = 0.0;
-            if (v) {
-                o.x = (cfi + 0.5) * F.pitch;
-                o.y = (cfj + 0.5) * F.pitch;
-                o.z = ctt * F.bres;
-                const double dx = o.x - q.x, dy = o.y - q.y, dz = o.z - q.z;
-                d2 = dx * dx + dy * dy + dz * dz;
-                ok = d2 <= r2;
-            }
-            const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-            if (bal) {
-                if (ok) visit(__popc(bal & lanemask_lt()), mm, o, d2, cfi, cfj);
-                __syncwarp();
-                flush(__popc(bal));
-                __syncwarp();
-            }
-            v = v2;
-            mm = mm2;
-            cfi = nfi;
-            cfj = nfj;
-            ctt = ntt;
-        }
-        __syncwarp();
+        uint32_t m0, len;
+        rows_load(F, sc, fi, fj, W, rb, ci1, m0, len);
+        const uint32_t total = rows_finish(rt, m0, len);
+        rows_scan(F, tc, sc, rt, total, q, r2, visit, flush);
     }
 }
 
@@ -177,41 +210,102 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
     const uint32_t gw = blockIdx.x * kNbrWarps + warp, nw = gridDim.x * kNbrWarps;
     const double R = F.cfg.R, r2 = R * R;
     (void)F.amom_stride;
-    for (uint32_t n = gw; n < P; n += nw) {
-        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
-        const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
+    const int W = F.cfg.W;
+    // the warp's points n_j = gw + j nw: positions preloaded 32 at a time (lane
+    // j holds point j's), and a single-batch window's rows are loaded for the
+    // next point while this point's second pass computes
+    int pfi = 0, pfj = 0;
+    double pt = 0.0;
+    uint32_t jbase = 0xffffffffu;
+    auto point = [&](uint32_t j, int& fi, int& fj, double& t) {
+        if ((j & ~31u) != jbase) {
+            jbase = j & ~31u;
+            const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
+            if (nl < P) {
+                pfi = F.fi[sc][nl];
+                pfj = F.fj[sc][nl];
+                pt = F.t[tc][nl];
+            }
+        }
+        fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
+        fj = __shfl_sync(0xffffffffu, pfj, (int)(j & 31u));
+        t = __shfl_sync(0xffffffffu, pt, (int)(j & 31u));
+    };
+    uint32_t ntot = 0;     // rows of the current point when single_cur
+    bool single_cur = false;
+    {
+        if (gw < P) {
+            int fi, fj;
+            double t;
+            point(0, fi, fj, t);
+            int ci0, ci1;
+            window_rows(F, fi, W, ci0, ci1);
+            single_cur = ci1 - ci0 < 32;
+            if (single_cur) {
+                uint32_t m0r, lenr;
+                rows_load(F, sc, fi, fj, W, ci0, ci1, m0r, lenr);
+                ntot = rows_finish(A.rtn[0], m0r, lenr);
+            }
+        }
+    }
+    uint32_t j = 0;
+    for (uint32_t n = gw; n < P; n += nw, ++j) {
+        int fi, fj;
+        double tq;
+        point(j, fi, fj, tq);
+        const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, tq * F.bres};
+        RowTab& rcur = A.rtn[j & 1u];
+        const bool single = single_cur;
+        const uint32_t total = ntot;
+        // next point: positions and (single batch) row loads, finished after pass B
+        const bool has_next = n + nw < P;
+        int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
+        double ntq = 0.0;
+        bool single_next = false;
+        uint32_t nm0 = 0, nlen = 0;
+        if (has_next) {
+            point(j + 1, nfi, nfj, ntq);
+            window_rows(F, nfi, W, nci0, nci1);
+            single_next = nci1 - nci0 < 32;
+        }
         // pass A: ball size, weights, wsum and weighted mean (denoise.hpp:172-186)
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         unsigned int cnt = 0;
-        ball_scan(
-            F, tc, sc, A.rt, fi, fj, q, r2,
-            [&](int rank, uint32_t, const Pos& o, double d2, int mfi, int mfj) {
-                const double w = apss_weight(R, sqrt(d2));
-                double* c = A.chunk[rank];
-                c[0] = w;
-                c[1] = o.x;
-                c[2] = o.y;
-                c[3] = o.z;
-                const unsigned int g = cnt + (unsigned int)rank;
-                if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, w, mfi, mfj};
-            },
-            [&](int nm) {
-                const int r = (lane - (int)cnt) & 31;  // member cnt + r has lane (cnt + r) mod 32
-                if (r < nm) {
-                    const double* c = A.chunk[r];
-                    const double w = c[0];
-                    a0 += w;
-                    a1 += w * c[1];
-                    a2 += w * c[2];
-                    a3 += w * c[3];
-                }
-                cnt += (unsigned int)nm;
-            });
+        auto visitA = [&](int rank, uint32_t, const Pos& o, double d2, int mfi, int mfj) {
+            const double w = apss_weight(R, sqrt(d2));
+            double* c = A.chunk[rank];
+            c[0] = w;
+            c[1] = o.x;
+            c[2] = o.y;
+            c[3] = o.z;
+            const unsigned int g = cnt + (unsigned int)rank;
+            if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, w, mfi, mfj};
+        };
+        auto flushA = [&](int nm) {
+            const int r = (lane - (int)cnt) & 31;  // member cnt + r has lane (cnt + r) mod 32
+            if (r < nm) {
+                const double* c = A.chunk[r];
+                const double w = c[0];
+                a0 += w;
+                a1 += w * c[1];
+                a2 += w * c[2];
+                a3 += w * c[3];
+            }
+            cnt += (unsigned int)nm;
+        };
+        if (single) rows_scan(F, tc, sc, rcur, total, q, r2, visitA, flushA);
+        else ball_scan(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
+        if (has_next && single_next) rows_load(F, sc, nfi, nfj, W, nci0, nci1, nm0, nlen);
+        auto advance = [&]() {
+            single_cur = single_next;
+            if (has_next && single_next) ntot = rows_finish(A.rtn[(j + 1) & 1u], nm0, nlen);
+        };
         const double wsum = warp_halving_sum(a0);
         double m0 = warp_halving_sum(a1), m1 = warp_halving_sum(a2), m2 = warp_halving_sum(a3);
         if (cnt < (unsigned int)F.cfg.min_nbrs || wsum <= 0.0) {
             if (lane == 0) F.amom[(size_t)n * kMom] = cnt < (unsigned int)F.cfg.min_nbrs ? -1.0 : wsum;
             __syncwarp();
+            advance();
             continue;
         }
         m0 /= wsum;
@@ -265,6 +359,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
             F.amom[(size_t)n * kMom + e] = e == 0 ? wsum : (e == 1 ? m0 : (e == 2 ? m1 : m2));
         }
         __syncwarp();
+        advance();
     }
 }
 
