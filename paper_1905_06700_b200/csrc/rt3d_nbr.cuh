@@ -53,6 +53,7 @@ struct KnnWarpSm {
     uint32_t sel[kKnnCap];  // the selection in rank order
     double kth;
     RowTab rt;
+    RowTab rtn[2];  // first-window rows of this point and the next
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -488,26 +489,81 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
     const double* rr = F.r[rc];
     const int k = F.cfg.knn_k, Wfull = F.cfg.W;
     const double pitch = F.pitch;
-    for (uint32_t n = gw; n < P; n += nw) {
-        const int fi = F.fi[sc][n], fj = F.fj[sc][n];
-        const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, F.t[tc][n] * F.bres};
-        int w = F.cfg.knn_w0 < Wfull ? F.cfg.knn_w0 : Wfull;
+    const int w0 = F.cfg.knn_w0 < Wfull ? F.cfg.knn_w0 : Wfull;
+    // positions preloaded 32 points at a time (lane j holds point j's); the
+    // next point's first-window rows are loaded during this point's selection
+    int pfi = 0, pfj = 0;
+    double pt = 0.0;
+    uint32_t jbase = 0xffffffffu;
+    auto point = [&](uint32_t j, int& fi, int& fj, double& t) {
+        if ((j & ~31u) != jbase) {
+            jbase = j & ~31u;
+            const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
+            if (nl < P) {
+                pfi = F.fi[sc][nl];
+                pfj = F.fj[sc][nl];
+                pt = F.t[tc][nl];
+            }
+        }
+        fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
+        fj = __shfl_sync(0xffffffffu, pfj, (int)(j & 31u));
+        t = __shfl_sync(0xffffffffu, pt, (int)(j & 31u));
+    };
+    bool single_cur = false;
+    uint32_t ntot = 0;
+    if (gw < P) {
+        int fi, fj;
+        double t;
+        point(0, fi, fj, t);
+        int ci0, ci1;
+        window_rows(F, fi, w0, ci0, ci1);
+        single_cur = ci1 - ci0 < 32;
+        if (single_cur) {
+            uint32_t m0r, lenr;
+            rows_load(F, sc, fi, fj, w0, ci0, ci1, m0r, lenr);
+            ntot = rows_finish(K.rtn[0], m0r, lenr);
+        }
+    }
+    uint32_t jj = 0;
+    for (uint32_t n = gw; n < P; n += nw, ++jj) {
+        int fi, fj;
+        double tq;
+        point(jj, fi, fj, tq);
+        const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, tq * F.bres};
+        const bool first_single = single_cur;
+        const uint32_t first_total = ntot;
+        const bool has_next = n + nw < P;
+        int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
+        double ntq = 0.0;
+        bool single_next = false;
+        uint32_t nm0 = 0, nlen = 0;
+        if (has_next) {
+            point(jj + 1, nfi, nfj, ntq);
+            window_rows(F, nfi, w0, nci0, nci1);
+            single_next = nci1 - nci0 < 32;
+        }
+        bool next_loaded = false;
+        int w = w0;
         double kth = 0.0;
         int taken = 0;
         unsigned int cnt;
         for (;;) {
             cnt = 0;
-            ball_scan(
-                F, tc, sc, K.rt, fi, fj, q, r2,
-                [&](int rank, uint32_t mm, const Pos&, double d2, int, int) {
-                    const unsigned int slot = cnt + (unsigned int)rank;
-                    if (slot < (unsigned int)kKnnCap) {
-                        K.d2[slot] = d2;
-                        K.idx[slot] = mm;
-                    }
-                },
-                [&](int nm) { cnt += (unsigned int)nm; }, w);
+            auto visitK = [&](int rank, uint32_t mm, const Pos&, double d2, int, int) {
+                const unsigned int slot = cnt + (unsigned int)rank;
+                if (slot < (unsigned int)kKnnCap) {
+                    K.d2[slot] = d2;
+                    K.idx[slot] = mm;
+                }
+            };
+            auto flushK = [&](int nm) { cnt += (unsigned int)nm; };
+            if (w == w0 && first_single) rows_scan(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
+            else ball_scan(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
             __syncwarp();
+            if (!next_loaded && has_next && single_next) {
+                rows_load(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
+                next_loaded = true;
+            }
             if (cnt > (unsigned int)kKnnCap) break;  // overflow: exact rescan below
             taken = knn_select(K, cnt, k, kth);
             if (w >= Wfull) break;
@@ -570,6 +626,11 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
         }
         if (lane == 0) F.r[rc ^ 1][n] = result;
         __syncwarp();
+        single_cur = single_next;
+        if (has_next && single_next) {
+            if (!next_loaded) rows_load(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
+            ntot = rows_finish(K.rtn[(jj + 1) & 1u], nm0, nlen);
+        }
     }
 }
 
