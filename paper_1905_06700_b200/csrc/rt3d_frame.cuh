@@ -278,6 +278,21 @@ __device__ __forceinline__ void sub_stamp(const Frame& F, int id) {
     }
 }
 
+// sweep sub-phase stamps (tools/sweep_profile.py), compiled in with
+// -DRT3D_SWEEP_PROF only: they cost registers in the hot loops
+#ifdef RT3D_SWEEP_PROF
+#define SWEEP_STAMP(who, id) \
+    do {                     \
+        if (who) sub_stamp(F, id); \
+    } while (0)
+#else
+#define SWEEP_STAMP(who, id) \
+    do {                     \
+        (void)(who);         \
+    } while (0)
+#endif
+
+
 
 template <class SM>
 __device__ __forceinline__ const IrfDev& pixel_irf(const Frame& F, const SM& sm, uint32_t p) {
@@ -870,7 +885,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
     constexpr int NG = 32 / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
     const bool w0t0 = blockIdx.x == 0 && threadIdx.x == 0;
-    if (w0t0) sub_stamp(F, 110);
+    SWEEP_STAMP(w0t0, 110);
     // ---- meta, lane per pixel
     if ((uint32_t)lane < size) {
         const uint32_t p = lo + lane;
@@ -900,7 +915,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
         W.mdead[lane] = dead ? 1u : 0u;
     }
     __syncwarp();
-    if (w0t0) sub_stamp(F, 111);
+    SWEEP_STAMP(w0t0, 111);
     const double* tcur = F.t[X.tc];
     const double* rcur = F.r[X.rc];
     for (uint32_t q0 = 0; q0 < size;) {
@@ -956,7 +971,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
             W.pmig[k] = mg;
         }
         __syncwarp();
-        if (w0t0) sub_stamp(F, 112);
+        SWEEP_STAMP(w0t0, 112);
         for (uint32_t qb = q0; qb < q1; qb += NG) {
             const uint32_t q = qb + grp;
             if (q < q1) {
@@ -995,7 +1010,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
         __syncwarp();
         }
         __syncwarp();
-        if (w0t0) sub_stamp(F, 113);
+        SWEEP_STAMP(w0t0, 113);
         q0 = q1;
     }
 }
@@ -1330,7 +1345,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t NG = 32 / G;
     const bool b0t0 = blockIdx.x == 0 && threadIdx.x == 0;
-    if (b0t0) sub_stamp(F, 100);
+    SWEEP_STAMP(b0t0, 100);
     if (threadIdx.x == 0 && F.dbg)
         F.dbg[64 + blockIdx.x] = ((unsigned long long)it << 40) | ((unsigned long long)op << 32) |
                                  (unsigned long long)sm.nsweep;
@@ -1384,13 +1399,13 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             }
             __syncthreads();
         }
-        if (b0t0) sub_stamp(F, 101);
+        SWEEP_STAMP(b0t0, 101);
         if (gbar(F, sm, op, it)) {
             if (threadIdx.x == 0) sm.c.done = 1;
             __syncthreads();
             return;
         }
-        if (b0t0) sub_stamp(F, 102);
+        SWEEP_STAMP(b0t0, 102);
         top_all(blk, bmx, F.tb_nbn, sm, total, gm, two ? blk2 : nullptr, &total2);
     } else {
         double cmax = 0.0;
@@ -1475,7 +1490,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             controller(F, &sm.c, blockIdx.x == 0, op, it, total2, gm);
         sm.nsweep += 1u;
     }
-    if (b0t0) sub_stamp(F, 103);
+    SWEEP_STAMP(b0t0, 103);
     __syncthreads();
 }
 

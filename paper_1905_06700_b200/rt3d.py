@@ -18,7 +18,7 @@ from .abi import (
     Peak, Point, ReconConfig, Report, Scene, Sensor, StateView, StepDiag, Config, ptr,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "librt3d.so"
+LIB_PATH = Path(os.environ.get("RT3D_LIB", Path(__file__).resolve().parent / "librt3d.so"))
 
 P = C.POINTER
 _dbl, _u64, _u8, _i32, _st = C.c_double, C.c_uint64, C.c_uint8, C.c_int32, C.c_int

@@ -1,6 +1,7 @@
 """Per-transition timing of the in-kernel profile stamps of one config-B
 frame (sweep sub-phases 100..106 included when compiled in).
-usage: python tools/sweep_profile.py"""
+usage: python tools/sweep_profile.py  (sub-phases 100..113 need a build with
+  make -C paper_1905_06700_b200/csrc EXTRA=-DRT3D_SWEEP_PROF)"""
 import sys
 from collections import defaultdict
 from pathlib import Path
