@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
     }
 }
 
-__global__ void __launch_bounds__(kNbrBlock, 5) apss_kernel(Frame F) {
+__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(Frame F) {
     apss_fit_threads(F);
 }
 
-__global__ void __launch_bounds__(kNbrBlock, 8) knn_kernel(Frame F) {
+__global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
