@@ -222,6 +222,10 @@ rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches);
  * (sensor.hpp:138-148) and PhotonCube::validate (cube.hpp:84-112). */
 rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* sensor);
 rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* cube);
+/* decode_cube / read_cube (io.hpp:116-150) from an SPCB byte buffer straight
+ * into the session's device CSR (the file's bytes, e.g. read or mmapped by the
+ * caller).  Same errors as the reference (RT3D_ERR_FORMAT with its messages). */
+rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_bytes);
 
 /* ---- hot path ----------------------------------------------------------- */
 /* splidar::reconstruct (reconstruct.hpp:457-489): matched-filter init + PALM

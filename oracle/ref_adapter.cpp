@@ -32,6 +32,7 @@
 #include <fftw3.h>
 #define private public
 #include "splidar/splidar.hpp"
+#include "splidar/io.hpp"
 #include "splidar/report_json.hpp"
 #undef private
 
@@ -210,6 +211,26 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 void ref_set_threads(unsigned n) { set_thread_count(n); }
+
+// encode_cube (io.hpp:99-114): the SPCB bytes of a cube
+int ref_encode_cube(const rt3d_cube* c, uint8_t* out, uint64_t cap, uint64_t* n) {
+    return guarded([&] {
+        const std::string b = encode_cube(make_cube(c));
+        *n = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    });
+}
+
+// decode_cube (io.hpp:116-145): 0 and the CSR, or 1 and the exception text
+int ref_decode_cube(const uint8_t* bytes, uint64_t n, uint64_t* offsets, rt3d_event* events,
+                    uint64_t cap) {
+    return guarded([&] {
+        PhotonCube cube = decode_cube(std::string(reinterpret_cast<const char*>(bytes), n));
+        if (offsets) std::memcpy(offsets, cube.offsets.data(), cube.offsets.size() * 8);
+        if (events && cap >= cube.events.size())
+            std::memcpy(events, cube.events.data(), cube.events.size() * 8);
+    });
+}
 
 int ref_matched_filter_peaks(const rt3d_event* ev, uint64_t n, const rt3d_irf* irf, int n_bins,
                              int k, double thr, int min_sep, rt3d_peak* out) {

@@ -447,6 +447,31 @@ __global__ void fft_kernel(const double* img, double* out, double* re, double* i
 // SoA state -> AoS rt3d_point (cloud order), positions per world_from_lidar
 // (sensor.hpp:200-203) or the baseline's coarse-centre placement
 // (eval.hpp:116-118).
+// SPCB events of pixel p (io.hpp:131-140) into the device CSR, with
+// PhotonCube::validate's per-event checks (cube.hpp:94-106); the first error
+// in pixel order is kept as (pixel << 2 | kind) in *err.  Pixel p's record
+// starts after the 28-byte header, p + 1 count words and off[p] events.
+__global__ void spcb_gather_kernel(const uint32_t* words, const uint32_t* off, uint32_t npix,
+                                   uint32_t n_bins, uint2* ev, unsigned long long* err) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += gridDim.x * blockDim.x) {
+        const uint32_t e0 = off[p], e1 = off[p + 1];
+        const uint64_t w0 = 7ull + (uint64_t)(p + 1) + 2ull * e0;  // first event word
+        uint32_t prev = 0;
+        unsigned kind = 0;
+        for (uint32_t k = 0; k < e1 - e0; ++k) {
+            const uint32_t bin = words[w0 + 2ull * k], count = words[w0 + 2ull * k + 1];
+            if (!kind) {
+                if (bin >= n_bins) kind = 1;
+                else if (count < 1) kind = 2;
+                else if (k > 0 && bin <= prev) kind = 3;
+            }
+            prev = bin;
+            ev[e0 + k] = make_uint2(bin, count);
+        }
+        if (kind) atomicMin(err, ((unsigned long long)p << 2) | kind);
+    }
+}
+
 // end-of-frame copy for pipelined frames: the cloud (AoS), the background
 // and the controller state into a result slot; P and the buffer toggles are
 // read on the device, so nothing waits for the frame on the host
@@ -1468,6 +1493,91 @@ rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
     s->c_cols = c->n_cols;
     s->c_bins = c->n_bins;
     s->n_events = c->n_events;
+    return RT3D_OK;
+}
+
+// decode_cube (io.hpp:116-145) straight into the session's device CSR: the
+// host walks the per-pixel record headers only (O(pixels)); the events are
+// copied once as raw bytes and gathered + validated on the device.
+rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_bytes) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!bytes) return fail(RT3D_ERR_INVALID_ARGUMENT, "null SPCB buffer");
+    const unsigned char* b = static_cast<const unsigned char*>(bytes);
+    uint64_t pos = 0;
+    auto u32 = [&](const char* what, uint32_t& v) -> bool {
+        if (n_bytes - pos < 4) {
+            fail(RT3D_ERR_FORMAT, "SPCB: truncated while reading %s", what);
+            return false;
+        }
+        v = (uint32_t)b[pos] | ((uint32_t)b[pos + 1] << 8) | ((uint32_t)b[pos + 2] << 16) |
+            ((uint32_t)b[pos + 3] << 24);
+        pos += 4;
+        return true;
+    };
+    if (n_bytes < 4) return fail(RT3D_ERR_FORMAT, "SPCB: truncated while reading magic");
+    if (std::memcmp(b, "SPCB", 4) != 0) return fail(RT3D_ERR_FORMAT, "SPCB: bad magic");
+    pos = 4;
+    uint32_t version, rows, cols, bins;
+    if (!u32("version", version)) return RT3D_ERR_FORMAT;
+    if (version != 1) return fail(RT3D_ERR_FORMAT, "SPCB: unsupported version %u", version);
+    if (!u32("n_rows", rows) || !u32("n_cols", cols) || !u32("n_bins", bins)) return RT3D_ERR_FORMAT;
+    if (n_bytes - pos < 8) return fail(RT3D_ERR_FORMAT, "SPCB: truncated while reading bin_width");
+    double bin_width;
+    std::memcpy(&bin_width, b + pos, 8);  // little-endian host
+    pos += 8;
+    if (rows == 0 || cols == 0 || bins == 0) return fail(RT3D_ERR_FORMAT, "SPCB: zero dimension");
+    if (rows > 0x7fffffffu || cols > 0x7fffffffu || bins > 0x7fffffffu)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: SPCB dimensions above 2^31");
+    const uint64_t npix = (uint64_t)rows * cols;
+    if (npix >= (1ull << 31)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: too many pixels");
+    std::vector<uint32_t> off32(npix + 1);
+    uint64_t ne = 0;
+    for (uint64_t p = 0; p < npix; ++p) {
+        uint32_t n;
+        if (!u32("event count", n)) return RT3D_ERR_FORMAT;
+        const uint64_t need = 8ull * n, have = n_bytes - pos;
+        if (have < need)
+            return fail(RT3D_ERR_FORMAT, "SPCB: truncated while reading %s",
+                        (have % 8) >= 4 ? "event value" : "event bin");
+        off32[p] = (uint32_t)ne;
+        ne += n;
+        if (ne >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: >= 2^32 events");
+        pos += need;
+    }
+    off32[npix] = (uint32_t)ne;
+    if (pos != n_bytes) return fail(RT3D_ERR_FORMAT, "SPCB: trailing bytes");
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->cube_slot = 0;
+    CUDA_TRY(s->off.ensure((npix + 1) * 4));
+    CUDA_TRY(s->ev.ensure(std::max<uint64_t>(ne, 1) * 8));
+    const uint64_t eo = (n_bytes + 7) & ~7ull;  // the error word after the bytes
+    CUDA_TRY(s->misc.ensure(eo + 8));
+    CUDA_TRY(cudaMemcpyAsync(s->misc.p, b, n_bytes, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->off.p, off32.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+    unsigned long long* err =
+        reinterpret_cast<unsigned long long*>(static_cast<char*>(s->misc.p) + eo);
+    CUDA_TRY(cudaMemsetAsync(err, 0xff, 8, s->stream));
+    spcb_gather_kernel<<<s->nsm * 8, 256, 0, s->stream>>>(
+        s->misc.as<uint32_t>(), s->off.as<uint32_t>(), (uint32_t)npix, bins, s->ev.as<uint2>(), err);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long herr = 0;
+    CUDA_TRY(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (herr != ~0ull) {
+        const unsigned long long p = herr >> 2;
+        const unsigned kind = (unsigned)(herr & 3u);
+        s->have_cube = false;
+        return fail(RT3D_ERR_FORMAT, kind == 1   ? "cube: bin out of range at pixel %llu"
+                                     : kind == 2 ? "cube: zero count at pixel %llu"
+                                                 : "cube: bins not strictly increasing at pixel %llu",
+                    p);
+    }
+    s->have_cube = true;
+    s->c_rows = (int)rows;
+    s->c_cols = (int)cols;
+    s->c_bins = (int)bins;
+    s->n_events = ne;
     return RT3D_OK;
 }
 

@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_debug_buffer", C.c_void_p, [SS])
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
+    _bind(L, "rt3d_set_cube_spcb", _st, [SS, C.c_void_p, _u64])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
     _bind(L, "rt3d_frame_submit", _st, [SS, P(Cube), P(ReconConfig), P(_u64)])
     _bind(L, "rt3d_frame_collect", _st, [SS, _u64, P(Point), _u64, P(_u64), P(_dbl), P(Report)])
@@ -101,7 +102,7 @@ EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
-    "rt3d_set_sensor", "rt3d_set_cube",
+    "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
     "rt3d_reconstruct", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
@@ -149,6 +150,12 @@ class Session:
     def set_cube(self, sc: Scene):
         self._cube = sc.cube_c()
         _check(lib().rt3d_set_cube(self.h, C.byref(self._cube)))
+
+    def set_cube_spcb(self, data):
+        """decode_cube (io.hpp:116-145) of SPCB bytes into the device CSR."""
+        buf = np.frombuffer(bytes(data), np.uint8) if not isinstance(data, np.ndarray) else data
+        buf = np.ascontiguousarray(buf, np.uint8)
+        _check(lib().rt3d_set_cube_spcb(self.h, buf.ctypes.data if len(buf) else None, len(buf)))
 
     def upload_state(self, points: np.ndarray, background: np.ndarray):
         from .abi import buckets

@@ -138,3 +138,27 @@ def simulate(spec: SceneSpec, seed: int, threads: int = 0) -> Scene:
     sc.truth = truth[: nt.value].copy()
     sc.signal_photons, sc.background_photons = int(meta[3]), int(meta[4])
     return sc
+
+
+def encode_spcb(sc) -> bytes:
+    """encode_cube (io.hpp:99-114): 'SPCB', version 1, rows, cols, bins (u32
+    little-endian), bin width (f64), then per pixel its event count and
+    (bin, count) pairs."""
+    import struct
+    out = [b"SPCB", struct.pack("<4I", 1, sc.n_rows, sc.n_cols, sc.n_bins),
+           struct.pack("<d", float(sc.bin_width_s))]
+    off = np.asarray(sc.offsets, np.uint64)
+    ev = np.ascontiguousarray(sc.events)
+    counts = np.diff(off).astype(np.uint32)
+    words = np.empty(len(counts) + 2 * len(ev), np.uint32)
+    # record p at word (p + 2 off[p]): count, then its events
+    pos = np.arange(len(counts), dtype=np.uint64) + 2 * off[:-1]
+    words[pos.astype(np.int64)] = counts
+    if len(ev):
+        pix = np.repeat(np.arange(len(counts)), counts.astype(np.int64))
+        k = np.arange(len(ev), dtype=np.uint64) - off[pix]
+        w = (pos[pix] + 1 + 2 * k).astype(np.int64)
+        words[w] = ev["bin"]
+        words[w + 1] = ev["count"]
+    out.append(words.astype("<u4").tobytes())
+    return b"".join(out)
