@@ -312,3 +312,19 @@ def test_concurrent_sessions_match_sequential(gpu):
     finally:
         for s in ss:
             s.close()
+
+
+@pytest.mark.parametrize("name", ["small_s3", "two_surface_24", "dense_12"])
+def test_reconstruct_fft_background_matches_oracle(gpu, name):
+    """background_mode = fft (reconstruct.hpp:405-429, denoise.hpp:267-319):
+    the device FFT low-pass inside the tail stage against the oracle's direct
+    DFT (<= 1e-9), through a whole reconstruction."""
+    import dataclasses
+    sc, cfg, _ = G.scene(name)
+    cfg = dataclasses.replace(cfg, background_mode=1, fft_cutoff=0.4)
+    gpu.set_scene(sc)
+    rep = gpu.reconstruct(cfg)
+    ref = O.reconstruct(sc, cfg, "oracle")
+    assert rep["iterations"] == ref["iterations"]
+    _assert_recon_parity(rep, ref, name + "/fft")
+    np.testing.assert_allclose(rep["background"], ref["background"], rtol=1e-7, atol=1e-12)
