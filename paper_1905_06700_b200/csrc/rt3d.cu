@@ -248,11 +248,19 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
             rc ^= 1;
             phase_prune_a(F, sm, rc, sc);
             gsync(sm, F, PH_PRUNE_A);
-            phase_prune_b(F, sm, tc, rc, sc);
-            gsync(sm, F, PH_PRUNE_B);
-            tc ^= 1;
-            rc ^= 1;
-            sc ^= 1;
+            // survivors over all blocks (every block sums the block totals):
+            // when nothing is pruned the compaction is the identity, so the
+            // buffers stay where they are
+            unsigned int keep = 0;
+            for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) keep += ld_cg(&F.btot[b]);
+            keep = block_sum_u32(keep, sm);
+            if (keep != P) {
+                phase_prune_b(F, sm, tc, rc, sc);
+                gsync(sm, F, PH_PRUNE_B);
+                tc ^= 1;
+                rc ^= 1;
+                sc ^= 1;
+            }
             X.tc = tc;
             X.rc = rc;
             X.bc = bc;

@@ -585,6 +585,14 @@ __device__ unsigned int scan_stage_b_base(const Frame& F, SM& sm, unsigned int* 
     return tot;
 }
 
+// block-wide sum of one u32 per thread, returned to every thread
+template <class SM>
+__device__ __forceinline__ unsigned int block_sum_u32(unsigned int v, SM& sm) {
+    unsigned int tot;
+    (void)block_exclusive_scan(v, sm, tot);
+    return tot;
+}
+
 // spawn points of init_matched_filter (reconstruct.hpp:219-237, 245-247)
 template <class SM>
 __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
