@@ -246,15 +246,11 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
         SweepCtx X = X0;
         if (P > 0) {
             rc ^= 1;
-            phase_prune_a(F, sm, rc, sc);
-            gsync(sm, F, PH_PRUNE_A);
-            // survivors over all blocks (every block sums the block totals):
-            // when nothing is pruned the compaction is the identity, so the
-            // buffers stay where they are
-            unsigned int keep = 0;
-            for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) keep += ld_cg(&F.btot[b]);
-            keep = block_sum_u32(keep, sm);
-            if (keep != P) {
+            // the kNN kernel counted the points at r >= r_min: when prune keeps
+            // them all the compaction is the identity and the buffers stay
+            if (ld_cg(&F.ctl->keep) != P) {
+                phase_prune_a(F, sm, rc, sc);
+                gsync(sm, F, PH_PRUNE_A);
                 phase_prune_b(F, sm, tc, rc, sc);
                 gsync(sm, F, PH_PRUNE_B);
                 tc ^= 1;
@@ -316,6 +312,7 @@ __global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, 
         c->result = sm.c.result;
         c->alpha = sm.c.alpha;
         c->cmax = sm.c.cmax;
+        c->keep = 0;  // the next kNN pass counts from zero
         F.ctl->tc = tc;
         F.ctl->rc = rc;
         F.ctl->bc = bc;

@@ -94,6 +94,7 @@ struct Ctl {
     // grid barrier (gbar) and its watchdog: a barrier that waits longer than
     // kBarrierTimeoutNs aborts the frame instead of hanging the device
     unsigned int bar_count, bar_gen, abort, abort_block;
+    unsigned int keep, pad1_;  // points the kNN filter left at r >= r_min (prune skip test)
     int abort_op, abort_it;
     unsigned int abort_count, abort_nsweep;
 };

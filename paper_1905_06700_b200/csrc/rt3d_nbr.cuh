@@ -525,6 +525,7 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
         }
     }
     uint32_t jj = 0;
+    unsigned int kept = 0;
     for (uint32_t n = gw; n < P; n += nw, ++jj) {
         int fi, fj;
         double tq;
@@ -624,7 +625,10 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
             }
             result = taken == 0 ? rr[n] : acc / (double)taken;
         }
-        if (lane == 0) F.r[rc ^ 1][n] = result;
+        if (lane == 0) {
+            F.r[rc ^ 1][n] = result;
+            kept += (result >= F.cfg.r_min) ? 1u : 0u;  // prune's test (denoise.hpp:246)
+        }
         __syncwarp();
         single_cur = single_next;
         if (has_next && single_next) {
@@ -632,6 +636,8 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
             ntot = rows_finish(K.rtn[(jj + 1) & 1u], nm0, nlen);
         }
     }
+    // survivors of the coming prune, one integer atomic per warp (exact, any order)
+    if (lane == 0 && kept) atomicAdd(&F.ctl->keep, kept);
 }
 
 }  // namespace rt3d
