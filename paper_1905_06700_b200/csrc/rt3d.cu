@@ -840,9 +840,13 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     {
         // blocktree block nodes: the shallowest depth <= G whose nodes hold at
         // most one chunk per warp (ceil(npix / 2^d) <= kWarps * 32/gsz)
+        // Depths below G stay nodes of pairwise_sum's recursion while their
+        // parents split (every parent has more than 8 pixels).
         const uint64_t cap = (uint64_t)kWarps * (uint64_t)(32 / F.cfg.gsz);
+        int dmax = F.G;
+        while (((uint64_t)npix >> dmax) > 8) ++dmax;  // depth dmax+1's parents would hold <= 8
         int d = 0;
-        while (d < F.G && (((uint64_t)npix + (1ull << d) - 1) >> d) > cap) ++d;
+        while (d < dmax && (((uint64_t)npix + (1ull << d) - 1) >> d) > cap) ++d;
         if (const char* e = getenv("RT3D_TBG")) d = std::max(d, std::min(atoi(e), F.G));
         F.tb_G = d;
         F.tb_nbn = 1u << d;

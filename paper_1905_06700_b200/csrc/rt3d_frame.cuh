@@ -1365,7 +1365,11 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         double* bmx = F.tbmax[par];
         double* blk2 = F.tblk2[par];
         const bool two = (KIND == K_CAND_T || KIND == K_CAND_R) && X.two;
-        const int dG = F.G - F.tb_G;
+        // block nodes above depth G hold 2^dG depth-G nodes; at or below it
+        // (small dense frames) a block node is itself a node of pairwise_sum's
+        // recursion of <= 32 pixels
+        const int dG = F.G > F.tb_G ? F.G - F.tb_G : 0;
+        const bool sub = F.tb_G >= F.G;
         for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
@@ -1382,12 +1386,12 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             if (lane == 0) sm.wmax[warp] = cm;
             __syncthreads();
             if (threadIdx.x < (1u << dG)) {
-                uint32_t lo, size;
-                tree_node_range(F.npix, F.G, (bn << dG) | threadIdx.x, lo, size);
+                uint32_t lo = blo, size = bsz;
+                if (!sub) tree_node_range(F.npix, F.G, (bn << dG) | threadIdx.x, lo, size);
                 sm.node2[threadIdx.x] = pw32(sm.bpart, (int)(lo - blo), (int)size);
             } else if (two && threadIdx.x >= 32 && threadIdx.x - 32 < (1u << dG)) {
-                uint32_t lo, size;
-                tree_node_range(F.npix, F.G, (bn << dG) | (threadIdx.x - 32), lo, size);
+                uint32_t lo = blo, size = bsz;
+                if (!sub) tree_node_range(F.npix, F.G, (bn << dG) | (threadIdx.x - 32), lo, size);
                 sm.node2b[threadIdx.x - 32] = pw32(sm.bpart2, (int)(lo - blo), (int)size);
             }
             __syncthreads();
