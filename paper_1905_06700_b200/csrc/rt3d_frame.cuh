@@ -1271,17 +1271,16 @@ __device__ void top_small(const double* vals, const double* vals2, const double*
             t2[w] = (uint32_t)w < nw ? sm.node2b[w] : 0.0;
             g = (uint32_t)w < nw ? std_max(g, sm.wmax[w]) : g;
         }
+        // the perfect tree over the nw (a power of two) warp sums
 #pragma unroll
         for (int w = kWarps; w > 1; w >>= 1)
+            if ((uint32_t)w <= nw) {
 #pragma unroll
-            for (int q = 0; q < w / 2; ++q)
-                if ((uint32_t)(2 * q + 1) < nw) {
+                for (int q = 0; q < w / 2; ++q) {
                     t[q] = t[2 * q] + t[2 * q + 1];
                     t2[q] = t2[2 * q] + t2[2 * q + 1];
-                } else if ((uint32_t)(2 * q) < nw) {
-                    t[q] = t[2 * q];
-                    t2[q] = t2[2 * q];
                 }
+            }
         total = t[0];
         total2 = t2[0];
         gm = g;
