@@ -102,14 +102,14 @@ __device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, 
 enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
 
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it);
+__global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it);
 
 // One stage of a frame: a cooperative kernel whose phases are separated by
 // grid barriers.  Buffer toggles live in Ctl between kernels; every block
 // reads them at entry, the leader writes them back at exit (after at least
 // one barrier, so no block still reads them).
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, G < 32 ? 2 : 1) stage_kernel(Frame F, int it) {
+__global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);

@@ -207,7 +207,7 @@ struct Frame {
 // 32.  The smaller footprint lets two 256-thread blocks share an SM.
 template <int G>
 struct SweepDims {
-    static constexpr int EVC = G >= 32 ? 256 : 64;
+    static constexpr int EVC = G >= 32 ? 192 : 64;
     static constexpr int PVC = G >= 32 ? 128 : 32;
 };
 template <int EVC, int PVC>
