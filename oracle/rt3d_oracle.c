@@ -924,7 +924,9 @@ int oracle_pratt_smallest(const double mflat[25], double u[5]) {
             pencil_shift(m, mid, a);
             if (pd5(a)) lo = mid;
             else hi = mid;
-            if (hi - lo <= 1e-14 * hi) break;
+            /* bracket to 1e-9 relative: the inverse iteration below converges
+             * from there (ratio ~1e-9 / gap per step) */
+            if (hi - lo <= 1e-9 * hi) break;
         }
         sigma = lo;
     } else {

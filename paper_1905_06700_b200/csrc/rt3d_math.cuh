@@ -225,7 +225,9 @@ __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
             if (!(mid > lo && mid < hi)) break;
             if (pd5_shift(m, mid)) lo = mid;
             else hi = mid;
-            if (hi - lo <= 1e-14 * hi) break;
+            // bracket to 1e-9 relative (as the oracle): the inverse iteration
+            // converges from there
+            if (hi - lo <= 1e-9 * hi) break;
         }
         sigma = lo;
     } else {
