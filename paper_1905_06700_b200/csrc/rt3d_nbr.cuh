@@ -68,8 +68,10 @@ __device__ __forceinline__ void window_rows(const Frame& F, int fi, int W, int& 
     int a0 = fi - W, a1 = fi + W;
     a0 = a0 < 0 ? 0 : a0;
     a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
-    ci0 = a0 / F.s;
-    ci1 = a1 / F.s;
+    // (integer division by the runtime superres factor is slow; s == 1 is
+    // the common case)
+    ci0 = F.s == 1 ? a0 : a0 / F.s;
+    ci1 = F.s == 1 ? a1 : a1 / F.s;
 }
 
 // Candidate range of window row ci = rb + lane (disc-culled columns): the
@@ -97,8 +99,9 @@ __device__ __forceinline__ void rows_load(const Frame& F, int sc, int fi, int fj
             b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
             const uint32_t prow = (uint32_t)ci * F.cols;
             const uint32_t* bo = F.bo[sc];
-            m0 = bo[prow + b0 / s];
-            len = bo[prow + b1 / s + 1] - m0;
+            const int c0 = s == 1 ? b0 : b0 / s, c1 = s == 1 ? b1 : b1 / s;
+            m0 = bo[prow + c0];
+            len = bo[prow + c1 + 1] - m0;
         }
     }
 }
