@@ -58,17 +58,17 @@ def config_b():
 
 
 KERNEL_NAMES = {
-    "stage_first": "rt3d::stage_kernel<ST_FIRST> (init peaks, spawn, first nll+grad sweep)",
+    "stage_first": "rt3d::stage_kernel<ST_FIRST> (init peaks, spawn, first nll+grad sweep, depth block 0)",
     "stage_depth": "rt3d::stage_kernel<ST_DEPTH> (depth candidates + backtracking)",
     "apss": "rt3d::apss_kernel (APSS ball moments, warp per point)",
     "apss_fit": "rt3d::apss_fit_kernel (sphere fit, projection, pinning)",
     "stage_intensity": "rt3d::stage_kernel<ST_INTENSITY> (intensity grad + candidates)",
     "knn": "rt3d::knn_kernel (kNN intensity filter)",
-    "stage_tail": "rt3d::stage_kernel<ST_TAIL> (prune, background block, nll)",
+    "stage_tail": "rt3d::stage_kernel<ST_TAIL> (prune, background block, nll, next depth block)",
 }
 
 
-def class_bytes(sc, rep) -> dict:
+def class_bytes(sc, rep, fused_depth: bool = True) -> dict:
     """Algorithmic HBM bytes of one frame per kernel class (DESIGN.md §4,
     SURVEY.md §8d): every likelihood sweep reads the CSR cube (8 B/event),
     per-pixel offsets/bucket/background/gain/dead (29 B/px) and t, r, bucket
@@ -85,10 +85,13 @@ def class_bytes(sc, rep) -> dict:
     b = dict.fromkeys(KERNEL_NAMES, 0.0)
     P0 = int(steps[0]["points_before"]) if len(steps) else 0
     b["stage_first"] = 8.0 * E + 29.0 * npix + 33.0 * P0 + sweep(P0, 16.0 * P0)
-    for st in steps:
+    for k, st in enumerate(steps):
         P, P1 = int(st["points_before"]), int(st["points_after"])
         if P > 0:
-            b["stage_depth"] += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
+            # the depth block runs at the end of the kernel that computed its
+            # gradients (ST_FIRST for iteration 0, else the previous ST_TAIL)
+            dk = "stage_depth" if not fused_depth else ("stage_first" if k == 0 else "stage_tail")
+            b[dk] += (1 + int(st["depth_backtracks"])) * sweep(P, 8.0 * P)
             b["apss"] += 8.0 * P          # t in (neighbours are L2/SMEM reuse)
             b["apss_fit"] += 9.0 * P      # t out + flags
             b["stage_intensity"] += sweep(P, 16.0 * P) + \
@@ -386,7 +389,7 @@ def main():
     h2d = sc.offsets.nbytes + sc.events.nbytes
 
     peak, peak_src = load_measured_peaks()
-    cb = class_bytes(sc, rep)
+    cb = class_bytes(sc, rep, fused_depth=ktimes["stage_depth"][1] == 0)
     fb = sum(cb.values())
     classes = {}
     for cls, (ms, n) in ktimes.items():

@@ -101,6 +101,29 @@ __device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, 
 
 enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
 
+// depth block of iteration it, reconstruct.hpp:320-350: safeguarded gradient
+// step; returns the new t toggle.  Runs at the end of the stage kernel that
+// computed the depth gradients (ST_FIRST for iteration 0, ST_TAIL for the
+// next iteration), so it needs no launch of its own.
+template <int G>
+__device__ int depth_block(const Frame& F, SmemT<G>& sm, int it, int tc, int rc, int bc, int sc) {
+    const uint32_t P = ld_cg(&F.ctl->P);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        StepDiagDev& d = F.diag[it];
+        d.nll_before = sm.c.nll_cur;
+        d.points_before = P;
+        if (P == 0) {
+            d.blk[0].nll_after_grad = d.blk[0].nll_after_denoise = d.nll_before;
+            d.blk[1].nll_after_grad = d.blk[1].nll_after_denoise = d.nll_before;
+        }
+    }
+    if (P > 0) {
+        cand_loop<K_CAND_T, G>(F, sm, tc, rc, bc, sc, OP_CAND_T, it);
+        if (sm.c.accept) tc ^= 1;
+    }
+    return tc;
+}
+
 template <int STAGE, int G>
 __global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it);
 
@@ -207,23 +230,10 @@ __global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
             // nll at the initial state + depth gradients (reconstruct.hpp:466)
             tree_sweep_g<K_GRAD_T, G>(F, sm, X0, OP_GRAD_T_FIRST, 0);
             stamp(F, PH_GRAD_T);
+            if (F.cfg.fuse_depth) tc = depth_block<G>(F, sm, 0, tc, rc, bc, sc);
         }
     } else if constexpr (STAGE == ST_DEPTH) {
-        // depth block, reconstruct.hpp:320-350: safeguarded gradient step
-        const uint32_t P = ld_cg(&F.ctl->P);
-        if (leader) {
-            StepDiagDev& d = F.diag[it];
-            d.nll_before = sm.c.nll_cur;
-            d.points_before = P;
-            if (P == 0) {
-                d.blk[0].nll_after_grad = d.blk[0].nll_after_denoise = d.nll_before;
-                d.blk[1].nll_after_grad = d.blk[1].nll_after_denoise = d.nll_before;
-            }
-        }
-        if (P > 0) {
-            cand_loop<K_CAND_T, G>(F, sm, tc, rc, bc, sc, OP_CAND_T, it);
-            if (sm.c.accept) tc ^= 1;
-        }
+        tc = depth_block<G>(F, sm, it, tc, rc, bc, sc);
     } else if constexpr (STAGE == ST_INTENSITY) {
         // APSS wrote t[tc^1] (apss_kernel); intensity block, :371-392
         const uint32_t P = ld_cg(&F.ctl->P);
@@ -297,6 +307,9 @@ __global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
         X.mig_cached = ld_cg(&F.ctl->P) > 0 ? 1 : 0;
         tree_sweep_g<K_GRAD_T, G>(F, sm, X, OP_GRAD_T_END, it);
         stamp(F, PH_GRAD_T);
+        // the next iteration's depth block (skipped by the stop rule)
+        if (F.cfg.fuse_depth && it + 1 < F.cfg.max_iters && !sm.c.stop)
+            tc = depth_block<G>(F, sm, it + 1, tc, rc, bc, sc);
     }
     if (leader && !sm.aborted) {
         // the controller replica back to F.ctl for the next kernel and the host
@@ -802,6 +815,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.trace = s->trace.as<double>();
     F.cfg = cfg;
     F.cfg.blocktree = getenv("RT3D_TREE_OLD") ? 0 : 1;
+    F.cfg.fuse_depth = getenv("RT3D_DEPTH_KERNEL") ? 0 : 1;
     // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND)
     F.cfg.two_cand = getenv("RT3D_ONE_CAND") ? 0
                      : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND")) : 1;
@@ -957,7 +971,7 @@ rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
     const int prog = F.cfg.program;
     if (prog == PROG_RECON || prog == PROG_PALM) {
         for (int it = 0; it < F.cfg.max_iters; ++it) {
-            if ((st = stage(ST_DEPTH, it))) return st;
+            if (!F.cfg.fuse_depth && (st = stage(ST_DEPTH, it))) return st;
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
                 apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
                 CUDA_TRY(cudaGetLastError());

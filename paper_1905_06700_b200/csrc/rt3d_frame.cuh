@@ -125,6 +125,7 @@ struct Cfg {
     int set_oog_flags; // palm: OR out-of-gate into flags
     int blocktree;     // sweeps: block-node aligned phase 1 + replicated top tree
     int two_cand;      // depth / intensity candidate sweeps evaluate alpha and alpha * beta
+    int fuse_depth;    // depth block at the end of ST_FIRST / ST_TAIL (no ST_DEPTH launch)
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };
 

@@ -328,3 +328,15 @@ def test_reconstruct_fft_background_matches_oracle(gpu, name):
     assert rep["iterations"] == ref["iterations"]
     _assert_recon_parity(rep, ref, name + "/fft")
     np.testing.assert_allclose(rep["background"], ref["background"], rtol=1e-7, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", G.SCENE_NAMES)
+def test_fused_and_separate_depth_block_agree(gpu, name):
+    """The depth block run at the end of the previous stage kernel and as its
+    own kernel give the same bits (reconstruct and palm_step flows)."""
+    sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_DEPTH_KERNEL": "1"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["trace"], b["trace"])
+    assert np.array_equal(a["steps"], b["steps"])

@@ -8,5 +8,7 @@ import json
 d = json.loads(open("gpurun_out/bench.json").read())
 print("value", round(d["value"], 2), "e2e", round(d["e2e"]["value"], 2), "ms", round(d["ms_per_step"], 3))
 for c, v in d["kernel_classes"].items():
+    if v["us_per_launch"] is None:
+        continue
     print(f'{c:16s} {v["ms_per_frame"]:.3f} ms/frame  {v["us_per_launch"]:.1f} us/launch')
 PY
