@@ -209,7 +209,8 @@ enum {
     RT3D_KC_KNN = 4,             /* kNN intensity filter (denoise.hpp:223)   */
     RT3D_KC_STAGE_TAIL = 5,      /* prune, background block, stop rule       */
     RT3D_KC_APSS_FIT = 6,        /* APSS sphere fit + projection + pinning   */
-    RT3D_KERNEL_CLASSES = 7
+    RT3D_KC_ITER = 7,            /* a whole PALM iteration in one launch     */
+    RT3D_KERNEL_CLASSES = 8
 };
 rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable);
 /* Debug aid (RT3D_DEBUG set at session creation): mapped host memory with

@@ -99,7 +99,7 @@ __device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, 
     }
 }
 
-enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3 };
+enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3, ST_ITER = 4 };
 
 // depth block of iteration it, reconstruct.hpp:320-350: safeguarded gradient
 // step; returns the new t toggle.  Runs at the end of the stage kernel that
@@ -234,8 +234,21 @@ __global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
         }
     } else if constexpr (STAGE == ST_DEPTH) {
         tc = depth_block<G>(F, sm, it, tc, rc, bc, sc);
-    } else if constexpr (STAGE == ST_INTENSITY) {
-        // APSS wrote t[tc^1] (apss_kernel); intensity block, :371-392
+    }
+    if constexpr (STAGE == ST_ITER) {
+        // a whole iteration in one launch: the APSS moments and fit as grid
+        // phases between barriers (same device functions as apss_kernel /
+        // apss_fit_kernel, warp scratch in the stage union)
+        const uint32_t P = ld_cg(&F.ctl->P);
+        if (P > 0) {
+            apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(sm.u.nbr), P, tc, sc);
+            gsync(sm, F, PH_APSS);
+            apss_fit_threads(F, P, tc, sc);
+            gsync(sm, F, PH_APSS_FIT);
+        }
+    }
+    if constexpr (STAGE == ST_INTENSITY || STAGE == ST_ITER) {
+        // APSS wrote t[tc^1]; intensity block, :371-392
         const uint32_t P = ld_cg(&F.ctl->P);
         if (P > 0) {
             tc ^= 1;
@@ -249,7 +262,19 @@ __global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
             cand_loop<K_CAND_R, G>(F, sm, tc, rc, bc, sc, OP_CAND_R, it);
             if (sm.c.accept) rc ^= 1;
         }
-    } else if constexpr (STAGE == ST_TAIL) {
+    }
+    if constexpr (STAGE == ST_ITER) {
+        // the kNN filter as a grid phase (knn_kernel's device function); it
+        // counts the points prune will keep into ctl->keep (reset by the
+        // previous kernel's write-back)
+        const uint32_t P = ld_cg(&F.ctl->P);
+        if (P > 0) {
+            gsync(sm, F, PH_GRAD_R);  // the accepted intensity candidates of every block
+            knn_warps(F, reinterpret_cast<KnnWarpSm*>(sm.u.nbr), P, tc, rc, sc);
+            gsync(sm, F, PH_KNN);
+        }
+    }
+    if constexpr (STAGE == ST_TAIL || STAGE == ST_ITER) {
         // kNN wrote r[rc^1] (knn_kernel); prune + refresh (:395-397), then
         // the background block (:405-429) and the nll that ends the iteration
         const uint32_t P = ld_cg(&F.ctl->P);
@@ -338,20 +363,22 @@ __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
-    apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw));
+    apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw), ld_cg(&F.ctl->P),
+                      ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
 }
 
 __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(Frame F) {
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS_FIT);
-    apss_fit_threads(F);
+    apss_fit_threads(F, ld_cg(&F.ctl->P), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
 }
 
 __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
-    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw));
+    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->P), ld_cg(&F.ctl->tc),
+              ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
 }
 
 // ---------------------------------------------------------------------------
@@ -816,6 +843,9 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.cfg = cfg;
     F.cfg.blocktree = getenv("RT3D_TREE_OLD") ? 0 : 1;
     F.cfg.fuse_depth = getenv("RT3D_DEPTH_KERNEL") ? 0 : 1;
+    // opt-in (RT3D_FUSED_ITER=1): measured slower on config B, the neighbour
+    // phases run at the stage kernels' occupancy
+    F.cfg.fused_iter = (F.cfg.fuse_depth && getenv("RT3D_FUSED_ITER")) ? 1 : 0;
     // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND)
     F.cfg.two_cand = getenv("RT3D_ONE_CAND") ? 0
                      : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND")) : 1;
@@ -894,13 +924,13 @@ static size_t stage_smem(int cfgi) {
 }
 // [config][stage]
 static StageFn stage_fn(int cfgi, int st) {
-    static StageFn tab[kNumCfg][4] = {
+    static StageFn tab[kNumCfg][5] = {
         {stage_kernel<ST_FIRST, 4>, stage_kernel<ST_DEPTH, 4>, stage_kernel<ST_INTENSITY, 4>,
-         stage_kernel<ST_TAIL, 4>},
+         stage_kernel<ST_TAIL, 4>, stage_kernel<ST_ITER, 4>},
         {stage_kernel<ST_FIRST, 32>, stage_kernel<ST_DEPTH, 32>, stage_kernel<ST_INTENSITY, 32>,
-         stage_kernel<ST_TAIL, 32>},
+         stage_kernel<ST_TAIL, 32>, stage_kernel<ST_ITER, 32>},
         {stage_kernel<ST_FIRST, 3>, stage_kernel<ST_DEPTH, 3>, stage_kernel<ST_INTENSITY, 3>,
-         stage_kernel<ST_TAIL, 3>},
+         stage_kernel<ST_TAIL, 3>, stage_kernel<ST_ITER, 3>},
     };
     return tab[cfgi][st];
 }
@@ -955,8 +985,8 @@ rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
     // the frame as a stream-ordered kernel sequence; every decision stays on
     // the device (Ctl), so nothing here waits for the GPU
     const int cfgi = F.cfg.gsz == 4 ? 0 : F.cfg.gsz == 32 ? 1 : 2;
-    static const int stage_cls[4] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
-                                     RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL};
+    static const int stage_cls[5] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
+                                     RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL, RT3D_KC_ITER};
     auto stage = [&](int st, int it) -> rt3d_status {
         return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
             void* args[] = {&F, &it};
@@ -971,6 +1001,10 @@ rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
     const int prog = F.cfg.program;
     if (prog == PROG_RECON || prog == PROG_PALM) {
         for (int it = 0; it < F.cfg.max_iters; ++it) {
+            if (F.cfg.fused_iter) {  // the whole iteration in one cooperative launch
+                if ((st = stage(ST_ITER, it))) return st;
+                continue;
+            }
             if (!F.cfg.fuse_depth && (st = stage(ST_DEPTH, it))) return st;
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
                 apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
@@ -1212,7 +1246,7 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     int per_sm_c[kNumCfg] = {1 << 30, 1 << 30, 1 << 30};
     for (int c = 0; c < kNumCfg; ++c)
-        for (int st = 0; st < 4; ++st) {
+        for (int st = 0; st < 5; ++st) {
             int b = 0;
             const size_t sz = stage_smem(c);
             CUDA_TRY(cudaFuncSetAttribute((const void*)stage_fn(c, st),

@@ -126,6 +126,7 @@ struct Cfg {
     int blocktree;     // sweeps: block-node aligned phase 1 + replicated top tree
     int two_cand;      // depth / intensity candidate sweeps evaluate alpha and alpha * beta
     int fuse_depth;    // depth block at the end of ST_FIRST / ST_TAIL (no ST_DEPTH launch)
+    int fused_iter;    // one ST_ITER launch per iteration (APSS, fit, kNN as grid phases)
     int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
 };
 
@@ -224,6 +225,7 @@ struct WarpSweepSmT {
 };
 constexpr int kTopMin = 1024;  // top-of-tree values always reducible in shared memory
 constexpr int kInitCap = 256;  // matched-filter candidate lags cached per warp
+constexpr int kNbrWarpBytes = 11264;  // APSS / kNN warp scratch inside the stage kernels (ST_ITER)
 struct InitWarpSm {
     int lag[kInitCap];
     double resp[kInitCap];
@@ -241,6 +243,7 @@ struct SmemT {
         } sw;
         double top[kTopMin];
         InitWarpSm init[kWarps];
+        alignas(16) unsigned char nbr[kWarps * kNbrWarpBytes];  // APSS / kNN phases of ST_ITER
     } u;
     double node[kWarps];
     double wmax[kWarps];

@@ -205,13 +205,11 @@ __device__ __forceinline__ double warp_halving_sum(double v) {
 // APSS moments over the current state: warp per point, results to F.amom
 // (kMom doubles per point, one coalesced store per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
 // the covariance is read off M, see apss_pass_b).
-__device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
+__device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t P, int tc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ApssWarpSm& A = wsm[warp];
-    const Ctl* ctl = F.ctl;
-    const uint32_t P = ld_cg(&ctl->P);
-    const int tc = ld_cg(&ctl->tc), sc = ld_cg(&ctl->sc);
-    const uint32_t gw = blockIdx.x * kNbrWarps + warp, nw = gridDim.x * kNbrWarps;
+    const uint32_t wpb = blockDim.x >> 5;
+    const uint32_t gw = blockIdx.x * wpb + warp, nw = gridDim.x * wpb;
     const double R = F.cfg.R, r2 = R * R;
     (void)F.amom_stride;
     const int W = F.cfg.W;
@@ -369,10 +367,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm) {
 
 // sphere fit, projection and pinning, one thread per point
 // (denoise.hpp:186-214, reconstruct.hpp:352-363); writes t[tc^1] and flags
-__device__ void apss_fit_threads(const Frame& F) {
-    const Ctl* ctl = F.ctl;
-    const uint32_t P = ld_cg(&ctl->P);
-    const int tc = ld_cg(&ctl->tc), sc = ld_cg(&ctl->sc);
+__device__ void apss_fit_threads(const Frame& F, uint32_t P, int tc, int sc) {
     (void)F.amom_stride;
     for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < P; n += gridDim.x * blockDim.x) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
@@ -481,13 +476,11 @@ __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k,
 // the next ring, no member outside can enter the top k and the selection is
 // final; otherwise the window grows to the first ring whose bound exceeds
 // the k-th key (at most W, the full ball).
-__device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
+__device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int tc, int rc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KnnWarpSm& K = wsm[warp];
-    const Ctl* ctl = F.ctl;
-    const uint32_t P = ld_cg(&ctl->P);
-    const int tc = ld_cg(&ctl->tc), rc = ld_cg(&ctl->rc), sc = ld_cg(&ctl->sc);
-    const uint32_t gw = blockIdx.x * kNbrWarps + warp, nw = gridDim.x * kNbrWarps;
+    const uint32_t wpb = blockDim.x >> 5;
+    const uint32_t gw = blockIdx.x * wpb + warp, nw = gridDim.x * wpb;
     const double R = F.cfg.R, r2 = R * R;
     const double* rr = F.r[rc];
     const int k = F.cfg.knn_k, Wfull = F.cfg.W;
@@ -642,5 +635,8 @@ __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm) {
     // survivors of the coming prune, one integer atomic per warp (exact, any order)
     if (lane == 0 && kept) atomicAdd(&F.ctl->keep, kept);
 }
+
+static_assert(sizeof(ApssWarpSm) <= (size_t)kNbrWarpBytes, "APSS warp scratch exceeds the stage union");
+static_assert(sizeof(KnnWarpSm) <= (size_t)kNbrWarpBytes, "kNN warp scratch exceeds the stage union");
 
 }  // namespace rt3d

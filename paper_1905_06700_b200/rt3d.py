@@ -205,7 +205,7 @@ class Session:
         return out
 
     KERNEL_CLASSES = ("stage_first", "stage_depth", "apss", "stage_intensity", "knn", "stage_tail",
-                      "apss_fit")
+                      "apss_fit", "iteration")
 
     def time_kernels(self, enable: bool = True):
         """CUDA events around every launch on the session stream (resets totals)."""

@@ -340,3 +340,16 @@ def test_fused_and_separate_depth_block_agree(gpu, name):
     assert np.array_equal(a["points"], b["points"])
     assert np.array_equal(a["trace"], b["trace"])
     assert np.array_equal(a["steps"], b["steps"])
+
+
+@pytest.mark.parametrize("name", G.SCENE_NAMES)
+def test_one_launch_iteration_matches_kernel_sequence(gpu, name):
+    """A PALM iteration as one cooperative launch (APSS, fit and kNN as grid
+    phases) and as the kernel sequence give the same bits."""
+    sc, cfg, _ = G.scene(name)
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_FUSED_ITER": "1"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
+    assert np.array_equal(a["steps"], b["steps"])
