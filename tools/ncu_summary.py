@@ -94,7 +94,7 @@ def main():
     (prof / f"{tag}_ncu_full.md").write_text(
         f"# {tag}: ncu --set full (key metrics per captured launch)\n\n"
         "`ncu --set full --clock-control none --import-source on -k "
-        "regex:\"apss_kernel|apss_fit|knn_kernel|stage_kernel\" -s 7 -c 7 python tools/profile_frame.py 1`\n\n"
+        "regex:\"apss_kernel|apss_fit|knn_kernel|stage_kernel\" -s 6 -c 6 python tools/profile_frame.py 1`\n\n"
         + "\n".join(f) + "\n")
     traffic["_source"] = f"{fpath} ({tag}), dram__bytes_read.sum + dram__bytes_write.sum"
     (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
