@@ -855,6 +855,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         int w0 = (int)std::ceil(std::sqrt((double)std::max(cfg.knn_k, 1)) / 2.0);
         w0 = std::max(w0, 1);
         if (F.frows >= (1 << 20) || F.fcols >= (1 << 20) || getenv("RT3D_KNN_NO_PRUNE")) w0 = cfg.W;
+        if (const char* e = getenv("RT3D_KNN_W0")) w0 = std::max(1, atoi(e));
         F.cfg.knn_w0 = w0;
     }
     F.cfg.max_iters = max_iters;
