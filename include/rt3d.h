@@ -176,6 +176,17 @@ typedef struct rt3d_report {
     double total_seconds;
 } rt3d_report;
 
+/* EvalResult (eval.hpp:20-28) */
+typedef struct rt3d_eval {
+    double recall;
+    double false_point_rate;
+    double depth_rmse;
+    double intensity_mae;
+    uint64_t n_truth;
+    uint64_t n_est;
+    uint64_t n_matched;
+} rt3d_eval;
+
 typedef struct rt3d_session rt3d_session;
 
 /* ---- library / session ------------------------------------------------ */
@@ -298,6 +309,15 @@ rt3d_status rt3d_prune(rt3d_session* s, const rt3d_point* cloud, uint64_t n, dou
 rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t rows,
                                     int32_t cols, double cutoff, int32_t clamp_nonneg,
                                     double* out);
+
+/* evaluate (eval.hpp:33-87): points grouped into transverse columns of the
+ * given pitch (floor(x / pitch), floor(y / pitch)), matched one-to-one per
+ * column greedily by (|dz|, truth index, estimate index) within tau.  Columns
+ * and matches on the device; the error sums in the reference's order on the
+ * host, so the result is bit-identical. */
+rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est,
+                          const rt3d_point* truth, uint64_t n_truth, double tau, double pitch,
+                          rt3d_eval* out);
 
 #ifdef __cplusplus
 }

@@ -212,6 +212,21 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 void ref_set_threads(unsigned n) { set_thread_count(n); }
 
+// evaluate (eval.hpp:33-87)
+int ref_evaluate(const rt3d_point* est, uint64_t n_est, const rt3d_point* truth, uint64_t n_truth,
+                 double tau, double pitch, double* out7) {
+    return guarded([&] {
+        EvalResult r = evaluate(make_cloud(est, n_est), make_cloud(truth, n_truth), tau, pitch);
+        out7[0] = r.recall;
+        out7[1] = r.false_point_rate;
+        out7[2] = r.depth_rmse;
+        out7[3] = r.intensity_mae;
+        out7[4] = (double)r.n_truth;
+        out7[5] = (double)r.n_est;
+        out7[6] = (double)r.n_matched;
+    });
+}
+
 // encode_cube (io.hpp:99-114): the SPCB bytes of a cube
 int ref_encode_cube(const rt3d_cube* c, uint8_t* out, uint64_t cap, uint64_t* n) {
     return guarded([&] {

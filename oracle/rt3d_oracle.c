@@ -1606,3 +1606,96 @@ int oracle_baseline_xcorr(const rt3d_cube* cube, const rt3d_sensor* sensor, rt3d
     sensor_free(&sn);
     return 0;
 }
+
+/* ---- evaluate (eval.hpp:33-87) ----------------------------------------
+   Points go into transverse columns (floor(x/pitch), floor(y/pitch))
+   (eval.hpp:39-43); columns are visited in (cx, cy) order like the
+   reference's std::map (:44-48, :54).  Inside a column every (est, truth)
+   pair within tau is a candidate (:60-65); candidates are taken greedily in
+   (err, truth, est) order, each point at most once (:66-79).  The depth and
+   intensity sums run in that same order. */
+typedef struct {
+    int64_t cx, cy;
+    uint32_t id; /* est ids first, then n_est + truth id */
+} ev_item;
+
+static int ev_item_cmp(const void* a, const void* b) {
+    const ev_item* p = (const ev_item*)a;
+    const ev_item* q = (const ev_item*)b;
+    if (p->cx != q->cx) return p->cx < q->cx ? -1 : 1;
+    if (p->cy != q->cy) return p->cy < q->cy ? -1 : 1;
+    return p->id < q->id ? -1 : (p->id > q->id);
+}
+
+typedef struct {
+    double err;
+    uint32_t e, t;
+} ev_pair;
+
+static int ev_pair_cmp(const void* a, const void* b) {
+    const ev_pair* p = (const ev_pair*)a;
+    const ev_pair* q = (const ev_pair*)b;
+    if (p->err != q->err) return p->err < q->err ? -1 : 1;
+    if (p->t != q->t) return p->t < q->t ? -1 : 1;
+    return p->e < q->e ? -1 : (p->e > q->e);
+}
+
+int oracle_evaluate(const rt3d_point* est, uint64_t n_est, const rt3d_point* truth, uint64_t n_truth,
+                    double tau, double pitch, double* out7) {
+    if (tau <= 0.0 || pitch <= 0.0) return 1;
+    const uint64_t n = n_est + n_truth;
+    ev_item* it = (ev_item*)malloc((n ? n : 1) * sizeof *it);
+    for (uint64_t q = 0; q < n; ++q) {
+        const rt3d_point* p = q < n_est ? &est[q] : &truth[q - n_est];
+        it[q].cx = (int64_t)floor(p->x / pitch);
+        it[q].cy = (int64_t)floor(p->y / pitch);
+        it[q].id = (uint32_t)q;
+    }
+    qsort(it, n, sizeof *it, ev_item_cmp);
+    uint8_t* e_used = (uint8_t*)calloc(n_est ? n_est : 1, 1);
+    uint8_t* t_used = (uint8_t*)calloc(n_truth ? n_truth : 1, 1);
+    double sq_depth = 0.0, abs_intensity = 0.0;
+    uint64_t matched = 0;
+    for (uint64_t a = 0; a < n;) {
+        uint64_t b = a, ne = 0;
+        while (b < n && it[b].cx == it[a].cx && it[b].cy == it[a].cy) {
+            ne += it[b].id < n_est;
+            ++b;
+        }
+        const uint64_t nt = (b - a) - ne;
+        ev_pair* pr = (ev_pair*)malloc((ne * nt ? ne * nt : 1) * sizeof *pr);
+        uint64_t np = 0;
+        for (uint64_t i = a; i < a + ne; ++i)
+            for (uint64_t j = a + ne; j < b; ++j) {
+                const uint32_t e = it[i].id, t = it[j].id - (uint32_t)n_est;
+                const double err = fabs(est[e].z - truth[t].z);
+                if (err <= tau) {
+                    pr[np].err = err;
+                    pr[np].e = e;
+                    pr[np].t = t;
+                    ++np;
+                }
+            }
+        qsort(pr, np, sizeof *pr, ev_pair_cmp);
+        for (uint64_t k = 0; k < np; ++k) {
+            if (e_used[pr[k].e] || t_used[pr[k].t]) continue;
+            e_used[pr[k].e] = t_used[pr[k].t] = 1;
+            ++matched;
+            sq_depth += pr[k].err * pr[k].err;
+            abs_intensity += fabs(est[pr[k].e].intensity - truth[pr[k].t].intensity);
+        }
+        free(pr);
+        a = b;
+    }
+    free(it);
+    free(e_used);
+    free(t_used);
+    out7[0] = n_truth ? (double)matched / (double)n_truth : 1.0;
+    out7[1] = n_est ? (double)(n_est - matched) / (double)n_est : 0.0;
+    out7[2] = matched ? sqrt(sq_depth / (double)matched) : 0.0;
+    out7[3] = matched ? abs_intensity / (double)matched : 0.0;
+    out7[4] = (double)n_truth;
+    out7[5] = (double)n_est;
+    out7[6] = (double)matched;
+    return 0;
+}

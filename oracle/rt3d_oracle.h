@@ -80,6 +80,10 @@ int oracle_knn_intensity_filter(const rt3d_point* cloud, uint64_t n, int k,
                                 double radius, rt3d_point* out);
 /* denoise.hpp:241-248; returns survivors. */
 uint64_t oracle_prune(const rt3d_point* cloud, uint64_t n, double r_min, rt3d_point* out);
+/* evaluate (eval.hpp:33-87); out7 = recall, false_point_rate, depth_rmse,
+   intensity_mae, n_truth, n_est, n_matched; returns 0, or 1 for tau/pitch <= 0 */
+int oracle_evaluate(const rt3d_point* est, uint64_t n_est, const rt3d_point* truth, uint64_t n_truth,
+                    double tau, double pitch, double* out7);
 /* denoise.hpp:254-319 (direct DFT instead of FFTW). */
 int oracle_fft_lowpass_filter(const double* img, int rows, int cols, double cutoff,
                               int clamp_nonneg, double* out);

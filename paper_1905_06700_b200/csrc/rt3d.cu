@@ -7,6 +7,7 @@
 // barriers, so a frame is one launch with no host round trip.  The same
 // device phases serve the fine-grained operators (nll, gradients, init,
 // palm_step) through the program switch.
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -517,6 +518,80 @@ __global__ void spcb_gather_kernel(const uint32_t* words, const uint32_t* off, u
     }
 }
 
+// evaluate (eval.hpp:33-87): column key of every estimate / truth point
+// (est first, then truth) -> (key, id); key order = std::map's (cx, cy) order
+__global__ void eval_keys_kernel(const rt3d_point* pts, uint32_t n, double pitch,
+                                 unsigned long long* keys, uint32_t* ids, unsigned int* bad) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double fx = floor(pts[i].x / pitch), fy = floor(pts[i].y / pitch);
+        const long long cx = (long long)fx, cy = (long long)fy;
+        if (!(fabs(fx) < 2147483648.0) || !(fabs(fy) < 2147483648.0)) atomicOr(bad, 1u);
+        keys[i] = ((unsigned long long)(cx + 2147483648ll) << 32) |
+                  (unsigned long long)(cy + 2147483648ll);
+        ids[i] = i;
+    }
+}
+
+// one thread per column (segment of equal keys): greedy one-to-one matching by
+// (err, truth, est) within tau (eval.hpp:51-77); the k-th match of the column
+// starting at sorted position p goes to out[p + k] = (err^2, |dr|), its count
+// to cnt[p]
+constexpr int kEvalCap = 64;
+__global__ void eval_match_kernel(const rt3d_point* pts, uint32_t n_est, uint32_t n,
+                                  const unsigned long long* keys, const uint32_t* ids, double tau,
+                                  double2* out, uint32_t* cnt, unsigned int* bad) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+        cnt[p] = 0;
+        if (p > 0 && keys[p - 1] == keys[p]) continue;
+        uint32_t q = p;
+        while (q < n && keys[q] == keys[p]) ++q;
+        uint32_t es[kEvalCap], ts[kEvalCap];
+        int ne = 0, nt = 0;
+        for (uint32_t k = p; k < q; ++k) {
+            const uint32_t id = ids[k];
+            if (id < n_est) {
+                if (ne < kEvalCap) es[ne] = id;
+                ++ne;
+            } else {
+                if (nt < kEvalCap) ts[nt] = id - n_est;
+                ++nt;
+            }
+        }
+        if (ne > kEvalCap || nt > kEvalCap) {
+            atomicOr(bad, 2u);
+            continue;
+        }
+        uint64_t eu = 0, tu = 0;  // used flags
+        uint32_t m = 0;
+        for (;;) {
+            double be = INFINITY;
+            uint32_t bt = 0xffffffffu, bs = 0xffffffffu;
+            int bi = -1, bj = -1;
+            for (int i = 0; i < ne; ++i) {
+                if ((eu >> i) & 1u) continue;
+                for (int j = 0; j < nt; ++j) {
+                    if ((tu >> j) & 1u) continue;
+                    const double err = fabs(pts[es[i]].z - pts[n_est + ts[j]].z);
+                    if (!(err <= tau)) continue;
+                    if (err < be || (err == be && (ts[j] < bt || (ts[j] == bt && es[i] < bs)))) {
+                        be = err;
+                        bt = ts[j];
+                        bs = es[i];
+                        bi = i;
+                        bj = j;
+                    }
+                }
+            }
+            if (bi < 0) break;
+            eu |= 1ull << bi;
+            tu |= 1ull << bj;
+            out[p + m] = make_double2(be * be, fabs(pts[bs].intensity - pts[n_est + bt].intensity));
+            ++m;
+        }
+        cnt[p] = m;
+    }
+}
+
 // end-of-frame copy for pipelined frames: the cloud (AoS), the background
 // and the controller state into a result slot; P and the buffer toggles are
 // read on the device, so nothing waits for the frame on the host
@@ -652,6 +727,7 @@ struct rt3d_session {
     // pipelined frames (rt3d_frame_submit / rt3d_frame_collect): a second
     // cube slot, a copy stream, result slots
     DevBuf off2, ev2;
+    DevBuf eval_pts, eval_k[2], eval_v[2], eval_out, eval_cnt, eval_tmp;  // rt3d_evaluate
     int cube_slot = 0;
     cudaStream_t cstream = nullptr;
     uint32_t* h_off[2] = {nullptr, nullptr};
@@ -2266,3 +2342,78 @@ rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t 
 }
 
 }  // extern "C"
+
+rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est,
+                          const rt3d_point* truth, uint64_t n_truth, double tau, double pitch,
+                          rt3d_eval* out) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null result");
+    if (!(tau > 0.0)) return fail(RT3D_ERR_INVALID_ARGUMENT, "evaluate: tau must be positive");
+    if (!(pitch > 0.0)) return fail(RT3D_ERR_INVALID_ARGUMENT, "evaluate: pitch must be positive");
+    if ((n_est && !est) || (n_truth && !truth)) return fail(RT3D_ERR_INVALID_ARGUMENT, "null points");
+    const uint64_t n = n_est + n_truth;
+    if (n >= (1ull << 31)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: too many points");
+    std::memset(out, 0, sizeof *out);
+    out->n_est = n_est;
+    out->n_truth = n_truth;
+    if (n == 0 || n_est == 0 || n_truth == 0) {
+        out->recall = n_truth ? 0.0 : 1.0;
+        out->false_point_rate = n_est ? 1.0 : 0.0;
+        return RT3D_OK;
+    }
+    CUDA_TRY(s->eval_pts.ensure(n * sizeof(rt3d_point)));
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(s->eval_k[k].ensure(n * 8));
+        CUDA_TRY(s->eval_v[k].ensure(n * 4));
+    }
+    CUDA_TRY(s->eval_out.ensure(n * 16));
+    CUDA_TRY(s->eval_cnt.ensure(n * 4 + 16));
+    rt3d_point* dp = s->eval_pts.as<rt3d_point>();
+    CUDA_TRY(cudaMemcpyAsync(dp, est, n_est * sizeof(rt3d_point), cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(dp + n_est, truth, n_truth * sizeof(rt3d_point), cudaMemcpyHostToDevice,
+                             s->stream));
+    unsigned int* bad = reinterpret_cast<unsigned int*>(s->eval_cnt.as<uint32_t>() + n);
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s->stream));
+    const int grid = s->nsm * 4;
+    eval_keys_kernel<<<grid, 256, 0, s->stream>>>(dp, (uint32_t)n, pitch,
+                                                 s->eval_k[0].as<unsigned long long>(),
+                                                 s->eval_v[0].as<uint32_t>(), bad);
+    CUDA_TRY(cudaGetLastError());
+    cub::DoubleBuffer<unsigned long long> kb(s->eval_k[0].as<unsigned long long>(),
+                                             s->eval_k[1].as<unsigned long long>());
+    cub::DoubleBuffer<uint32_t> vb(s->eval_v[0].as<uint32_t>(), s->eval_v[1].as<uint32_t>());
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, (int)n, 0, 64, s->stream));
+    CUDA_TRY(s->eval_tmp.ensure(tmp + 16));
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(s->eval_tmp.p, tmp, kb, vb, (int)n, 0, 64, s->stream));
+    eval_match_kernel<<<grid, 128, 0, s->stream>>>(dp, (uint32_t)n_est, (uint32_t)n, kb.Current(),
+                                                  vb.Current(), tau, s->eval_out.as<double2>(),
+                                                  s->eval_cnt.as<uint32_t>(), bad);
+    CUDA_TRY(cudaGetLastError());
+    std::vector<uint32_t> cnt(n + 1);
+    std::vector<double2> val(n);
+    CUDA_TRY(cudaMemcpyAsync(cnt.data(), s->eval_cnt.p, n * 4 + 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(val.data(), s->eval_out.p, n * 16, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (cnt[n] & 1u) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: evaluate column index beyond 2^31");
+    if (cnt[n] & 2u)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: evaluate column with more than %d points of a kind",
+                    kEvalCap);
+    // the sums in the reference's order: columns in key order, matches in order
+    double sq_depth = 0.0, abs_intensity = 0.0;
+    uint64_t matched = 0;
+    for (uint64_t p = 0; p < n; ++p)
+        for (uint32_t k = 0; k < cnt[p]; ++k) {
+            sq_depth += val[p + k].x;
+            abs_intensity += val[p + k].y;
+            ++matched;
+        }
+    out->n_matched = matched;
+    out->recall = (double)matched / (double)n_truth;
+    out->false_point_rate = (double)(n_est - matched) / (double)n_est;
+    out->depth_rmse = matched ? std::sqrt(sq_depth / (double)matched) : 0.0;
+    out->intensity_mae = matched ? abs_intensity / (double)matched : 0.0;
+    return RT3D_OK;
+}
+

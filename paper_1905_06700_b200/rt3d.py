@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_knn_intensity_filter", _st,
           [SS, P(Point), _u64, _i32, P(Point), _u64, _dbl, _dbl, P(Point)])
     _bind(L, "rt3d_prune", _st, [SS, P(Point), _u64, _dbl, P(Point), P(_u64)])
+    _bind(L, "rt3d_evaluate", _st, [SS, P(Point), _u64, P(Point), _u64, _dbl, _dbl, P(Eval)])
     _bind(L, "rt3d_fft_lowpass_filter", _st,
           [SS, P(_dbl), _i32, _i32, _dbl, _i32, P(_dbl)])
     _lib = L
@@ -108,7 +109,15 @@ EXPORTED = [
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
     "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
     "rt3d_apss_project", "rt3d_knn_intensity_filter", "rt3d_prune", "rt3d_fft_lowpass_filter",
+    "rt3d_evaluate",
 ]
+
+
+class Eval(C.Structure):
+    """rt3d_eval (include/rt3d.h) = splidar::EvalResult (eval.hpp:21-29)."""
+    _fields_ = [("recall", C.c_double), ("false_point_rate", C.c_double),
+                ("depth_rmse", C.c_double), ("intensity_mae", C.c_double),
+                ("n_truth", C.c_uint64), ("n_est", C.c_uint64), ("n_matched", C.c_uint64)]
 
 
 class Session:
@@ -357,6 +366,16 @@ class Session:
                                                radius if cell is None else cell, radius,
                                                ptr(out, Point)))
         return out
+
+    def evaluate(self, est, truth, tau: float, pitch: float) -> dict:
+        """evaluate (eval.hpp:33-87): recall / false-point rate / depth RMSE /
+        intensity MAE of `est` against `truth`, matched per column of `pitch`."""
+        est = np.ascontiguousarray(est, POINT_DTYPE)
+        truth = np.ascontiguousarray(truth, POINT_DTYPE)
+        e = Eval()
+        _check(lib().rt3d_evaluate(self.h, ptr(est, Point), len(est), ptr(truth, Point),
+                                   len(truth), tau, pitch, C.byref(e)))
+        return {k: getattr(e, k) for k, _ in Eval._fields_}
 
     def prune(self, points, r_min):
         points = np.ascontiguousarray(points, POINT_DTYPE)

@@ -118,8 +118,64 @@ def scene_arrays(sc, prefix=""):
     return {prefix + k: np.asarray(v) for k, v in d.items()}
 
 
+def evaluate_cases():
+    """(name, est, truth, tau, pitch) for evaluate (eval.hpp:33-87): clouds with
+    shared columns, equal depth errors (ties), negative coordinates, empties."""
+    from paper_1905_06700_b200.abi import POINT_DTYPE
+    rng = np.random.default_rng(1905)
+
+    def cloud(n, span, zq=None, shift=0.0):
+        c = np.zeros(n, POINT_DTYPE)
+        c["x"] = rng.uniform(-span, span, n) + shift
+        c["y"] = rng.uniform(-span, span, n)
+        z = rng.uniform(1.0, 3.0, n)
+        c["z"] = np.round(z / zq) * zq if zq else z
+        c["intensity"] = rng.uniform(0.1, 5.0, n)
+        return c
+
+    cases = []
+    sc = np.load(HERE / "scene_two_surface_24.npz")
+    est = sc["rec_points"]
+    truth = est.copy()
+    truth["z"] += rng.normal(0, 0.01, len(truth))
+    truth["intensity"] *= rng.uniform(0.8, 1.2, len(truth))
+    keep = rng.random(len(truth)) > 0.1
+    truth = np.concatenate([truth[keep], cloud(40, 0.2)])
+    cases.append(("scene", est, truth, 0.02, float(sc["pitch"])))
+    t = cloud(600, 0.05, zq=0.01)
+    e = cloud(700, 0.05, zq=0.01)
+    cases.append(("ties", e, t, 0.02, 0.01))
+    cases.append(("ties_wide", e, t, 0.5, 0.02))
+    e2 = cloud(300, 1.0, shift=-0.5)
+    t2 = e2.copy()
+    t2["z"] += rng.uniform(-0.05, 0.05, len(t2))
+    cases.append(("negative", e2, t2, 0.03, 0.1))
+    cases.append(("empty_est", e2[:0], t2, 0.03, 0.1))
+    cases.append(("empty_truth", e2, t2[:0], 0.03, 0.1))
+    cases.append(("empty_both", e2[:0], t2[:0], 0.03, 0.1))
+    cases.append(("tiny_tau", e2, t2, 1e-12, 0.1))
+    return cases
+
+
+def make_evaluate():
+    out = {}
+    names = []
+    for name, e, t, tau, pitch in evaluate_cases():
+        r, rc = L.evaluate(e, t, tau, pitch, "ref")
+        assert rc == 0, L.ref().ref_last_error()
+        names.append(name)
+        out[name + "_est"], out[name + "_truth"] = e, t
+        out[name + "_tp"] = np.array([tau, pitch])
+        out[name + "_out"] = r
+    np.savez_compressed(HERE / "evaluate.npz", names=np.array(names), **out)
+    print("evaluate cases", names)
+
+
 def main():
     assert L.ref_available(), "oracle/_ref/libref.so missing: make -C oracle"
+    if sys.argv[1:] == ["evaluate"]:
+        make_evaluate()
+        return
     # 1) random instances + reference likelihood outputs
     rnd = {}
     for seed in list(range(0, 40)) + [77, 9001, 1001, 1013]:
@@ -205,6 +261,7 @@ def main():
     den["img_fft04"] = L.fft_lowpass(img, 0.4, impl="ref")
     den["img_fft04_clamp"] = L.fft_lowpass(img, 0.4, clamp=True, impl="ref")
     np.savez_compressed(HERE / "denoise.npz", **den)
+    make_evaluate()
     print("done")
 
 

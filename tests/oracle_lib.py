@@ -74,6 +74,7 @@ def oracle() -> C.CDLL:
         _bind(lib, "oracle_knn_intensity_filter", C.c_int,
               [P(Point), _u64, C.c_int, P(Point), _u64, _dbl, _dbl, P(Point)])
         _bind(lib, "oracle_prune", _u64, [P(Point), _u64, _dbl, P(Point)])
+        _bind(lib, "oracle_evaluate", C.c_int, [P(Point), _u64, P(Point), _u64, _dbl, _dbl, P(_dbl)])
         _bind(lib, "oracle_fft_lowpass_filter", C.c_int,
               [P(_dbl), C.c_int, C.c_int, _dbl, C.c_int, P(_dbl)])
         _bind(lib, "oracle_palm_step", C.c_int,
@@ -119,6 +120,7 @@ def ref() -> C.CDLL:
                P(StepDiag), P(C.c_int)])
         _bind(lib, "ref_reconstruct", C.c_int,
               [P(Cube), P(Sensor), P(ReconConfig), P(_u64), P(C.c_int), P(_dbl)])
+        _bind(lib, "ref_evaluate", C.c_int, [P(Point), _u64, P(Point), _u64, _dbl, _dbl, P(_dbl)])
         _bind(lib, "ref_baseline_xcorr", C.c_int, [P(Cube), P(Sensor), P(Point), P(_u64)])
         _bind(lib, "ref_simulate", C.c_int,
               [C.c_char_p, _u64, P(C.c_int), P(_u64), P(_u64)])
@@ -329,3 +331,14 @@ def irf_gaussian(sigma=1.5, nsig=4.0, dtau=0.25):
     tmin = _dbl()
     n = oracle().oracle_irf_gaussian(sigma, nsig, dtau, ptr(buf, _dbl), len(buf), C.byref(tmin))
     return buf[:n].copy(), tmin.value
+
+
+def evaluate(est, truth, tau: float, pitch: float, impl="oracle"):
+    """eval.hpp:33-87 -> (7 doubles, status): recall, false_point_rate, depth_rmse,
+    intensity_mae, n_truth, n_est, n_matched."""
+    est = np.ascontiguousarray(est, POINT_DTYPE)
+    truth = np.ascontiguousarray(truth, POINT_DTYPE)
+    out = np.zeros(7)
+    rc = getattr(_lib(impl), _name(impl, "evaluate"))(ptr(est, Point), len(est), ptr(truth, Point),
+                                                       len(truth), tau, pitch, ptr(out, _dbl))
+    return out, rc
