@@ -18,6 +18,7 @@
 //   splidar::b200::prune              <- denoise.hpp:241-248
 //   splidar::b200::fft_lowpass_filter / fft_background_denoise <- denoise.hpp:267-319
 //   splidar::b200::baseline_xcorr     <- splidar::baseline_xcorr     eval.hpp:91-126
+//   splidar::b200::evaluate           <- splidar::evaluate           eval.hpp:33-87
 //
 // The neighbour-search operators take the indexed cloud explicitly: the
 // reference's SpatialIndex keeps its cloud private, and every reference call
@@ -293,6 +294,22 @@ inline PointCloud baseline_xcorr(const PhotonCube& cube, const SensorModel& sens
     BackgroundImage bg;
     detail::download(s, sensor.n_rows, sensor.n_cols, cloud, bg);
     return cloud;
+}
+
+inline EvalResult evaluate(const PointCloud& est, const PointCloud& truth, double tau,
+                           double pitch, Session& s = default_session()) {
+    const std::vector<rt3d_point> e = detail::to_c(est), t = detail::to_c(truth);
+    rt3d_eval r{};
+    check(rt3d_evaluate(s.get(), e.data(), e.size(), t.data(), t.size(), tau, pitch, &r));
+    EvalResult out;
+    out.recall = r.recall;
+    out.false_point_rate = r.false_point_rate;
+    out.depth_rmse = r.depth_rmse;
+    out.intensity_mae = r.intensity_mae;
+    out.n_truth = r.n_truth;
+    out.n_est = r.n_est;
+    out.n_matched = r.n_matched;
+    return out;
 }
 
 inline std::vector<splidar::detail::Peak> matched_filter_peaks(

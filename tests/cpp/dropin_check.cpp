@@ -114,6 +114,18 @@ int main() {
     CHECK(same_cloud(s0.cloud, s1.cloud), "init cloud");
     CHECK(s0.background == s1.background, "init background");
     CHECK(same_cloud(baseline_xcorr(cube, sensor), b200::baseline_xcorr(cube, sensor)), "baseline");
+    {
+        const PointCloud bl = baseline_xcorr(cube, sensor);
+        for (double tau : {0.01, 0.05, 0.3}) {
+            const EvalResult e0 = evaluate(s0.cloud, bl, tau, sensor.pixel_pitch);
+            const EvalResult e1 = b200::evaluate(s0.cloud, bl, tau, sensor.pixel_pitch);
+            CHECK(same(e0.recall, e1.recall) && same(e0.false_point_rate, e1.false_point_rate) &&
+                      same(e0.depth_rmse, e1.depth_rmse) &&
+                      same(e0.intensity_mae, e1.intensity_mae) && e0.n_matched == e1.n_matched &&
+                      e0.n_truth == e1.n_truth && e0.n_est == e1.n_est,
+                  "evaluate tau %g", tau);
+        }
+    }
     for (int i = 0; i < cube.n_rows; ++i) {
         auto [eb, ee] = cube.pixel(i, i);
         auto p0 = splidar::detail::matched_filter_peaks(eb, ee, sensor.irf_shared, cube.n_bins, 3,
