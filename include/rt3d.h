@@ -319,6 +319,36 @@ rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est
                           const rt3d_point* truth, uint64_t n_truth, double tau, double pitch,
                           rt3d_eval* out);
 
+/* ---- forward simulator (device) ----------------------------------------- */
+/* simulate_cube's photon sampling (simulate.hpp:181-205: rate_profile,
+ * likelihood.hpp:80-95, and CounterRng::next_poisson keyed by (seed, pixel,
+ * bin, stream), rng.hpp:11-98) on the device, into the session's resident
+ * cube (as if rt3d_set_cube had been called).  `truth` is the scene's truth
+ * cloud after the reflectivity scaling (simulate.hpp:145-159; i, j, t and
+ * intensity are read), `background` the true background per pixel and bin
+ * (simulate.hpp:172-177).  Uses the session's sensor (IRF, gain, dead).
+ * photons[2] receives {signal, background} photon totals.  Sampled events
+ * must stay below 2^32. */
+rt3d_status rt3d_simulate_cube(rt3d_session* s, const rt3d_point* truth, uint64_t n_truth,
+                               const double* background, uint64_t seed, uint64_t* n_events,
+                               uint64_t* photons);
+/* The session's resident cube (CSR, cube.hpp:24-40) back to the host:
+ * offsets u64[rows*cols+1], events[n_events] (n_events from
+ * rt3d_simulate_cube or the cube that was set).  Either pointer may be NULL. */
+rt3d_status rt3d_cube_copy(rt3d_session* s, uint64_t* offsets, rt3d_event* events);
+
+/* ---- output formats (host only, no session) ---------------------------- */
+/* encode_ply (io.hpp:162-179): ASCII PLY of a cloud (e.g. from
+ * rt3d_state_copy / rt3d_frame_collect), byte-identical to the reference's;
+ * has_pixel_pitch != 0 adds the "comment pixel_pitch" line.  Two calls: with
+ * buf NULL (or cap too small) only *n_bytes is set. */
+rt3d_status rt3d_encode_ply(const rt3d_point* points, uint64_t n, int32_t has_pixel_pitch,
+                            double pixel_pitch, char* buf, uint64_t cap, uint64_t* n_bytes);
+/* The background CSV of `splidar reconstruct --background-out`
+ * (tools/splidar_main.cpp:204-212): rows lines of cols "%.9g" values. */
+rt3d_status rt3d_encode_background_csv(const double* background, int32_t rows, int32_t cols,
+                                       char* buf, uint64_t cap, uint64_t* n_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,8 @@ void rt3d_scene_sizes(const rt3d_scene* s, uint64_t* n_events, uint64_t* n_truth
  * signal_photons, background_photons}. */
 void rt3d_scene_copy(const rt3d_scene* s, uint64_t* offsets, rt3d_event* events,
                      double* irf_samples, rt3d_point* truth, uint8_t* dead, double* meta);
+/* background_truth (simulate.hpp:172-177): ambient + hot pixels, f64[rows*cols] */
+void rt3d_scene_background(const rt3d_scene* s, double* out);
 void rt3d_scene_free(rt3d_scene* s);
 
 #ifdef __cplusplus

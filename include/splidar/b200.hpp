@@ -19,6 +19,8 @@
 //   splidar::b200::fft_lowpass_filter / fft_background_denoise <- denoise.hpp:267-319
 //   splidar::b200::baseline_xcorr     <- splidar::baseline_xcorr     eval.hpp:91-126
 //   splidar::b200::evaluate           <- splidar::evaluate           eval.hpp:33-87
+//   splidar::b200::encode_ply         <- splidar::encode_ply         io.hpp:162-179
+//   splidar::b200::simulate_photons   <- simulate_cube's sampling    simulate.hpp:181-205
 //
 // The neighbour-search operators take the indexed cloud explicitly: the
 // reference's SpatialIndex keeps its cloud private, and every reference call
@@ -41,6 +43,7 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -453,6 +456,42 @@ inline BackgroundImage fft_background_denoise(const BackgroundImage& b, double c
     check(rt3d_fft_lowpass_filter(s.get(), b.data.data(), b.rows, b.cols, cutoff, 1,
                                   out.data.data()));
     return out;
+}
+
+// ---- around the path: output and the forward simulator ----------------------
+
+/// encode_ply (io.hpp:162-179), byte-identical; formatted on all host threads.
+inline std::string encode_ply(const PointCloud& cloud, std::optional<double> pixel_pitch = {}) {
+    const std::vector<rt3d_point> pts = detail::to_c(cloud);
+    std::uint64_t n = 0;
+    check(rt3d_encode_ply(pts.data(), pts.size(), pixel_pitch ? 1 : 0, pixel_pitch.value_or(0.0),
+                          nullptr, 0, &n));
+    std::string out(n, '\0');
+    check(rt3d_encode_ply(pts.data(), pts.size(), pixel_pitch ? 1 : 0, pixel_pitch.value_or(0.0),
+                          out.data(), n, &n));
+    return out;
+}
+
+/// simulate_cube's photon sampling (simulate.hpp:181-205) on the device:
+/// `truth` after the reflectivity scaling (SimReport::truth), `background`
+/// = SimReport::background_truth.  The cube stays resident in `s` as well.
+inline PhotonCube simulate_photons(const PointCloud& truth, const BackgroundImage& background,
+                                   const SensorModel& sensor, std::uint64_t seed,
+                                   Session& s = default_session()) {
+    detail::SensorView sv(sensor);
+    check(rt3d_set_sensor(s.get(), &sv.c));
+    const std::vector<rt3d_point> pts = detail::to_c(truth);
+    std::uint64_t n = 0, ph[2] = {0, 0};
+    check(rt3d_simulate_cube(s.get(), pts.data(), pts.size(), background.data.data(), seed, &n,
+                             ph));
+    PhotonCube c(sensor.n_rows, sensor.n_cols, sensor.n_bins,
+                 2.0 * sensor.bin_resolution / kSpeedOfLight);
+    c.events.resize(n);
+    static_assert(sizeof(Event) == sizeof(rt3d_event), "Event layout");
+    check(rt3d_cube_copy(s.get(), c.offsets.data(),
+                         reinterpret_cast<rt3d_event*>(c.events.data())));
+    c.recount();
+    return c;
 }
 
 }  // namespace splidar::b200

@@ -236,6 +236,17 @@ int ref_encode_cube(const rt3d_cube* c, uint8_t* out, uint64_t cap, uint64_t* n)
     });
 }
 
+// encode_ply (io.hpp:162-179): the reference's PLY text of a cloud
+int ref_encode_ply(const rt3d_point* pts, uint64_t n, int has_pitch, double pitch, char* out,
+                   uint64_t cap, uint64_t* nb) {
+    return guarded([&] {
+        const std::string b = has_pitch ? encode_ply(make_cloud(pts, n), pitch)
+                                        : encode_ply(make_cloud(pts, n));
+        *nb = b.size();
+        if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    });
+}
+
 // decode_cube (io.hpp:116-145): 0 and the CSR, or 1 and the exception text
 int ref_decode_cube(const uint8_t* bytes, uint64_t n, uint64_t* offsets, rt3d_event* events,
                     uint64_t cap) {

@@ -21,6 +21,7 @@
 #include "../../include/rt3d.h"
 #include "rt3d_frame.cuh"
 #include "rt3d_nbr.cuh"
+#include "rt3d_sim.cuh"
 
 using namespace rt3d;
 
@@ -728,6 +729,7 @@ struct rt3d_session {
     // cube slot, a copy stream, result slots
     DevBuf off2, ev2;
     DevBuf eval_pts, eval_k[2], eval_v[2], eval_out, eval_cnt, eval_tmp;  // rt3d_evaluate
+    DevBuf sim_boff, sim_bpts, sim_t, sim_r, sim_bg, sim_cnt, sim_tmp, sim_ph;  // rt3d_simulate_cube
     int cube_slot = 0;
     cudaStream_t cstream = nullptr;
     uint32_t* h_off[2] = {nullptr, nullptr};
@@ -2417,3 +2419,110 @@ rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est
     return RT3D_OK;
 }
 
+
+// simulate_cube's photon sampling (simulate.hpp:181-205) into the session's
+// resident cube.  The truth buckets are a stable counting sort by coarse
+// pixel (SceneState::refresh, likelihood.hpp:38-55) done on the host; the
+// sampling, the offset scan and the event gather run on the device
+// (rt3d_sim.cu).
+rt3d_status rt3d_simulate_cube(rt3d_session* s, const rt3d_point* truth, uint64_t n_truth,
+                               const double* background, uint64_t seed, uint64_t* n_events,
+                               uint64_t* photons) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!s->have_sensor) return fail(RT3D_ERR_INVALID_ARGUMENT, "simulate: no sensor set");
+    if ((n_truth && !truth) || !background)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "simulate: null truth / background");
+    if (n_truth >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: >= 2^32 truth points");
+    const size_t npix = (size_t)s->rows * s->cols;
+    std::vector<uint32_t> boff(npix + 1, 0), bpts(std::max<uint64_t>(n_truth, 1));
+    std::vector<double> tt(std::max<uint64_t>(n_truth, 1)), rr(std::max<uint64_t>(n_truth, 1));
+    for (uint64_t k = 0; k < n_truth; ++k) {
+        const rt3d_point& q = truth[k];
+        if (q.i < 0 || q.i >= s->rows || q.j < 0 || q.j >= s->cols)
+            return fail(RT3D_ERR_OUT_OF_RANGE, "simulate: truth point %llu outside the sensor",
+                        (unsigned long long)k);
+        ++boff[(size_t)q.i * s->cols + q.j + 1];
+        tt[k] = q.t;
+        rr[k] = q.intensity;
+    }
+    for (size_t p = 0; p < npix; ++p) boff[p + 1] += boff[p];
+    {
+        std::vector<uint32_t> cur(boff.begin(), boff.end() - 1);
+        for (uint64_t k = 0; k < n_truth; ++k)
+            bpts[cur[(size_t)truth[k].i * s->cols + truth[k].j]++] = (uint32_t)k;
+    }
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    CUDA_TRY(s->sim_boff.ensure((npix + 1) * 4));
+    CUDA_TRY(s->sim_bpts.ensure(bpts.size() * 4));
+    CUDA_TRY(s->sim_t.ensure(tt.size() * 8));
+    CUDA_TRY(s->sim_r.ensure(rr.size() * 8));
+    CUDA_TRY(s->sim_bg.ensure(npix * 8));
+    CUDA_TRY(s->sim_cnt.ensure((npix + 1) * 4));
+    CUDA_TRY(s->sim_ph.ensure(16));
+    CUDA_TRY(s->off.ensure((npix + 1) * 4));
+    CUDA_TRY(cudaMemcpyAsync(s->sim_boff.p, boff.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->sim_bpts.p, bpts.data(), bpts.size() * 4, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->sim_t.p, tt.data(), tt.size() * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->sim_r.p, rr.data(), rr.size() * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(s->sim_bg.p, background, npix * 8, cudaMemcpyHostToDevice, s->stream));
+    SimArgs a;
+    a.irfs = s->irfs.as<IrfDev>();
+    a.irf_of_pix = s->per_pixel_irf ? s->irf_of_pix.as<uint32_t>() : nullptr;
+    a.gain = s->gain.as<double>();
+    a.dead = s->dead.as<uint8_t>();
+    a.background = s->sim_bg.as<double>();
+    a.boff = s->sim_boff.as<uint32_t>();
+    a.bpts = s->sim_bpts.as<uint32_t>();
+    a.pt_t = s->sim_t.as<double>();
+    a.pt_r = s->sim_r.as<double>();
+    a.rows = s->rows;
+    a.cols = s->cols;
+    a.bins = s->bins;
+    a.seed = seed;
+    size_t tmp = 0;
+    CUDA_TRY(sim_count(a, s->sim_cnt.as<uint32_t>(), s->off.as<uint32_t>(), nullptr, nullptr, &tmp,
+                       s->stream));
+    CUDA_TRY(s->sim_tmp.ensure(std::max<size_t>(tmp, 16)));
+    CUDA_TRY(sim_count(a, s->sim_cnt.as<uint32_t>(), s->off.as<uint32_t>(),
+                       s->sim_ph.as<unsigned long long>(), s->sim_tmp.p, &tmp, s->stream));
+    uint32_t total = 0;
+    unsigned long long ph[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(&total, s->off.as<uint32_t>() + npix, 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(ph, s->sim_ph.p, 16, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    CUDA_TRY(s->ev.ensure(std::max<uint64_t>(total, 1) * 8));
+    CUDA_TRY(sim_write(a, s->off.as<uint32_t>(), s->ev.as<uint2>(), s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    s->cube_slot = 0;
+    s->have_cube = true;
+    s->c_rows = s->rows;
+    s->c_cols = s->cols;
+    s->c_bins = s->bins;
+    s->n_events = total;
+    if (n_events) *n_events = total;
+    if (photons) {
+        photons[0] = ph[0];
+        photons[1] = ph[1];
+    }
+    return RT3D_OK;
+}
+
+// The session's resident cube back to the host (PhotonCube CSR, cube.hpp:24-40).
+rt3d_status rt3d_cube_copy(rt3d_session* s, uint64_t* offsets, rt3d_event* events) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!s->have_cube) return fail(RT3D_ERR_INVALID_ARGUMENT, "no cube set");
+    const size_t npix = (size_t)s->c_rows * s->c_cols;
+    const DevBuf& off = s->cube_slot ? s->off2 : s->off;
+    const DevBuf& ev = s->cube_slot ? s->ev2 : s->ev;
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (offsets) {
+        std::vector<uint32_t> o(npix + 1);
+        CUDA_TRY(cudaMemcpy(o.data(), off.p, (npix + 1) * 4, cudaMemcpyDeviceToHost));
+        for (size_t p = 0; p <= npix; ++p) offsets[p] = o[p];
+    }
+    if (events && s->n_events)
+        CUDA_TRY(cudaMemcpy(events, ev.p, s->n_events * 8, cudaMemcpyDeviceToHost));
+    return RT3D_OK;
+}

@@ -159,6 +159,7 @@ struct rt3d_scene {
     uint8_t* dead;
     double bin_width_s;
     uint64_t sig, bgp;
+    double* bg; /* background_truth, simulate.hpp:172-177 */
 };
 
 /* SurfaceSpec::depth_at, simulate.hpp:37-41 */
@@ -399,7 +400,7 @@ int rt3d_scene_simulate(const rt3d_scene_spec* spec, uint64_t seed, int threads,
     free(nev);
     free(jobs);
     free(th);
-    free(bgimg);
+    sc->bg = bgimg;
     free(boff);
     free(bpts);
     *out = sc;
@@ -437,5 +438,10 @@ void rt3d_scene_free(rt3d_scene* s) {
     free(s->events);
     free(s->truth);
     free(s->dead);
+    free(s->bg);
     free(s);
+}
+
+void rt3d_scene_background(const rt3d_scene* s, double* out) {
+    if (s->bg) memcpy(out, s->bg, sizeof(double) * (size_t)s->rows * s->cols);
 }

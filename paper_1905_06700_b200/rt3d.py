@@ -14,7 +14,7 @@ from typing import Optional
 import numpy as np
 
 from .abi import (
-    POINT_DTYPE, PEAK_DTYPE, STEP_DIAG_DTYPE, STATUS, ApssParams, Cube, Event, InitParams, Irf,
+    EVENT_DTYPE, POINT_DTYPE, PEAK_DTYPE, STEP_DIAG_DTYPE, STATUS, ApssParams, Cube, Event, InitParams, Irf,
     Peak, Point, ReconConfig, Report, Scene, Sensor, StateView, StepDiag, Config, ptr,
 )
 
@@ -90,6 +90,10 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_evaluate", _st, [SS, P(Point), _u64, P(Point), _u64, _dbl, _dbl, P(Eval)])
     _bind(L, "rt3d_fft_lowpass_filter", _st,
           [SS, P(_dbl), _i32, _i32, _dbl, _i32, P(_dbl)])
+    _bind(L, "rt3d_simulate_cube", _st, [SS, P(Point), _u64, P(_dbl), _u64, P(_u64), P(_u64)])
+    _bind(L, "rt3d_cube_copy", _st, [SS, P(_u64), P(Event)])
+    _bind(L, "rt3d_encode_ply", _st, [P(Point), _u64, _i32, _dbl, C.c_char_p, _u64, P(_u64)])
+    _bind(L, "rt3d_encode_background_csv", _st, [P(_dbl), _i32, _i32, C.c_char_p, _u64, P(_u64)])
     _lib = L
     return L
 
@@ -109,8 +113,31 @@ EXPORTED = [
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
     "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
     "rt3d_apss_project", "rt3d_knn_intensity_filter", "rt3d_prune", "rt3d_fft_lowpass_filter",
-    "rt3d_evaluate",
+    "rt3d_evaluate", "rt3d_encode_ply", "rt3d_encode_background_csv",
+    "rt3d_simulate_cube", "rt3d_cube_copy",
 ]
+
+
+def _two_call(fn, *args) -> bytes:
+    n = _u64()
+    _check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    _check(fn(*args, buf, n.value, C.byref(n)))
+    return buf.raw[: n.value]
+
+
+def encode_ply(points, pixel_pitch=None) -> bytes:
+    """encode_ply (io.hpp:162-179): the reference's ASCII PLY bytes."""
+    points = np.ascontiguousarray(points, POINT_DTYPE)
+    return _two_call(lib().rt3d_encode_ply, ptr(points, Point), len(points),
+                     int(pixel_pitch is not None), float(pixel_pitch or 0.0))
+
+
+def encode_background_csv(background) -> bytes:
+    """`splidar reconstruct --background-out` CSV (tools/splidar_main.cpp:204-212)."""
+    bg = np.ascontiguousarray(background, np.float64)
+    rows, cols = bg.shape
+    return _two_call(lib().rt3d_encode_background_csv, ptr(bg, _dbl), rows, cols)
 
 
 class Eval(C.Structure):
@@ -376,6 +403,25 @@ class Session:
         _check(lib().rt3d_evaluate(self.h, ptr(est, Point), len(est), ptr(truth, Point),
                                    len(truth), tau, pitch, C.byref(e)))
         return {k: getattr(e, k) for k, _ in Eval._fields_}
+
+    def simulate_cube(self, truth, background, seed: int):
+        """simulate_cube's sampling (simulate.hpp:181-205) on the device into
+        the session cube (sensor must be set).  Returns (n_events, signal
+        photons, background photons)."""
+        truth = np.ascontiguousarray(truth, POINT_DTYPE)
+        bg = np.ascontiguousarray(background, np.float64)
+        n = _u64()
+        ph = (_u64 * 2)()
+        _check(lib().rt3d_simulate_cube(self.h, ptr(truth, Point), len(truth), ptr(bg, _dbl),
+                                        seed, C.byref(n), ph))
+        return n.value, ph[0], ph[1]
+
+    def cube_copy(self, npix: int, n_events: int):
+        """The resident cube as (offsets u64[npix+1], events)."""
+        off = np.zeros(npix + 1, np.uint64)
+        ev = np.zeros(max(n_events, 1), EVENT_DTYPE)
+        _check(lib().rt3d_cube_copy(self.h, ptr(off, _u64), ptr(ev, Event)))
+        return off, ev[:n_events]
 
     def prune(self, points, r_min):
         points = np.ascontiguousarray(points, POINT_DTYPE)

@@ -90,6 +90,7 @@ def lib() -> C.CDLL:
                                       C.POINTER(C.c_double), C.POINTER(Point),
                                       C.POINTER(C.c_uint8), C.POINTER(C.c_double)]
         L.rt3d_scene_free.argtypes = [C.c_void_p]
+        L.rt3d_scene_background.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -131,11 +132,14 @@ def simulate(spec: SceneSpec, seed: int, threads: int = 0) -> Scene:
     L.rt3d_scene_copy(h, ptr(offsets, C.c_uint64), events.ctypes.data_as(C.POINTER(Event)),
                       ptr(irf, C.c_double), truth.ctypes.data_as(C.POINTER(Point)),
                       ptr(deadm, C.c_uint8), ptr(meta, C.c_double))
+    bg = np.zeros(npix)
+    L.rt3d_scene_background(h, ptr(bg, C.c_double))
     L.rt3d_scene_free(h)
     sc = Scene(spec.rows, spec.cols, spec.bins, offsets, events[: ne.value], irf, meta[0],
                meta[1], superres=spec.superres, pixel_pitch=spec.pixel_pitch_m,
                bin_resolution=spec.bin_resolution_m, bin_width_s=meta[2], dead=deadm)
     sc.truth = truth[: nt.value].copy()
+    sc.background_truth = bg
     sc.signal_photons, sc.background_photons = int(meta[3]), int(meta[4])
     return sc
 

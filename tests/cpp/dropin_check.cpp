@@ -108,12 +108,31 @@ int main() {
     cfg.init.max_returns = 2;
     cfg.init.min_separation = 6;
 
+    // forward simulator on the device: the same cube (counter-based RNG)
+    {
+        auto [ref_cube, rep] = simulate_cube(spec, sensor, 7);
+        PhotonCube dev = b200::simulate_photons(rep.truth, rep.background_truth, sensor, 7);
+        std::size_t diff = 0;
+        if (dev.offsets != ref_cube.offsets || dev.events.size() != ref_cube.events.size()) {
+            diff = 1;
+        } else {
+            for (std::size_t k = 0; k < dev.events.size(); ++k)
+                diff += dev.events[k].bin != ref_cube.events[k].bin ||
+                        dev.events[k].count != ref_cube.events[k].count;
+        }
+        CHECK(diff == 0, "simulate_photons differs (%zu)", diff);
+        CHECK(dev.total_count == ref_cube.total_count, "simulate total count");
+    }
+
     // init + baseline + peaks: bitwise
     SceneState s0 = init_matched_filter(cube, sensor, cfg.init);
     SceneState s1 = b200::init_matched_filter(cube, sensor, cfg.init);
     CHECK(same_cloud(s0.cloud, s1.cloud), "init cloud");
     CHECK(s0.background == s1.background, "init background");
     CHECK(same_cloud(baseline_xcorr(cube, sensor), b200::baseline_xcorr(cube, sensor)), "baseline");
+    CHECK(encode_ply(s0.cloud, sensor.pixel_pitch) == b200::encode_ply(s0.cloud, sensor.pixel_pitch),
+          "encode_ply");
+    CHECK(encode_ply(s0.cloud) == b200::encode_ply(s0.cloud), "encode_ply without pitch");
     {
         const PointCloud bl = baseline_xcorr(cube, sensor);
         for (double tau : {0.01, 0.05, 0.3}) {
