@@ -13,7 +13,9 @@
 // boundary (tests/test_sim.py measures the agreement).
 //
 // Two passes over the same samples (they are recomputed, not stored): count
-// the active bins per pixel, exclusive-scan into the CSR offsets, write.
+// the active bins per pixel, exclusive-scan into the CSR offsets, write (the
+// write pass stops at a pixel's last event).  The RNG key chain and the
+// background's exp(-lambda) are hoisted per pixel.
 #include <cub/cub.cuh>
 
 #include "rt3d_sim.cuh"
@@ -29,22 +31,20 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-// CounterRng (rng.hpp:11-40)
+// CounterRng (rng.hpp:11-40).  The constructor's chain
+//   base = mix(mix(mix(mix(a+G) ^ mix(b+2G)) ^ mix(c+3G)) ^ mix(d+5G))
+// is evaluated in pieces: the seed and pixel terms once per pixel, the bin
+// term once per bin for both streams; the values are the same.
 struct Crng {
     uint64_t base, counter;
-    __device__ Crng(uint64_t a, uint64_t b, uint64_t c, uint64_t d) : counter(0) {
-        base = mix64(a + kGamma);
-        base = mix64(base ^ mix64(b + 2 * kGamma));
-        base = mix64(base ^ mix64(c + 3 * kGamma));
-        base = mix64(base ^ mix64(d + 5 * kGamma));
-    }
+    __device__ explicit Crng(uint64_t b) : base(b), counter(0) {}
     __device__ uint64_t next_u64() { return mix64(base + (++counter) * kGamma); }
     __device__ double next_unit() {
         return ((double)(next_u64() >> 11) + 0.5) * 0x1.0p-53;
     }
-    // rng.hpp:52-61
-    __device__ uint32_t inversion(double lambda) {
-        const double limit = exp(-lambda);
+    // rng.hpp:52-61 (limit = exp(-lambda), hoisted by the caller when lambda
+    // is the same for every bin of a pixel)
+    __device__ uint32_t inversion(double limit) {
         uint32_t k = 0;
         double p = 1.0;
         do {
@@ -89,17 +89,35 @@ struct Crng {
             }
         }
     }
-    __device__ uint32_t poisson(double lambda) {
+    __device__ uint32_t poisson(double lambda, double limit) {
         if (!(lambda > 0.0)) return 0;
-        if (lambda < 10.0) return inversion(lambda);
+        if (lambda < 10.0) return inversion(limit);
         return ptrd(lambda);
     }
 };
 
+// Per-pixel constants of the sampler.
+struct PixelRng {
+    uint64_t base_px;  // mix(mix(seed+G) ^ mix(p+2G))
+    uint64_t m1, m2;   // mix(1+5G), mix(2+5G): the stream terms
+    double lam_bg, limit_bg;
+};
+
+__device__ __forceinline__ PixelRng pixel_rng(const SimArgs& a, uint32_t p, double g) {
+    PixelRng r;
+    r.base_px = mix64(mix64(a.seed + kGamma) ^ mix64((uint64_t)p + 2 * kGamma));
+    r.m1 = mix64(1 + 5 * kGamma);
+    r.m2 = mix64(2 + 5 * kGamma);
+    r.lam_bg = g * a.background[p];
+    r.limit_bg = exp(-r.lam_bg);
+    return r;
+}
+
 // One lane's bin: {signal, background} photons (simulate.hpp:190-201).
-__device__ __forceinline__ uint2 sample_bin(const SimArgs& a, const IrfDev& f, uint32_t p,
-                                            double g, int t, uint32_t k0, uint32_t k1) {
-    const double lam_bg = g * a.background[p];
+__device__ __forceinline__ uint2 sample_bin(const SimArgs& a, const IrfDev& f, const PixelRng& R,
+                                            uint32_t p, double g, int t, uint32_t k0,
+                                            uint32_t k1) {
+    const double lam_bg = R.lam_bg;
     double lam = lam_bg;
     for (uint32_t k = k0; k < k1; ++k) {
         const uint32_t q = __ldg(&a.bpts[k]);
@@ -111,8 +129,9 @@ __device__ __forceinline__ uint2 sample_bin(const SimArgs& a, const IrfDev& f, u
     const double d = lam - lam_bg;
     const double lam_sig = d > 0.0 ? d : 0.0;
     uint32_t zs = 0, zb = 0;
-    if (lam_sig > 0.0) zs = Crng(a.seed, p, (uint64_t)t, 1).poisson(lam_sig);
-    if (lam_bg > 0.0) zb = Crng(a.seed, p, (uint64_t)t, 2).poisson(lam_bg);
+    const uint64_t h = mix64(R.base_px ^ mix64((uint64_t)t + 3 * kGamma));
+    if (lam_sig > 0.0) zs = Crng(mix64(h ^ R.m1)).poisson(lam_sig, lam_sig < 10.0 ? exp(-lam_sig) : 0.0);
+    if (lam_bg > 0.0) zb = Crng(mix64(h ^ R.m2)).poisson(lam_bg, R.limit_bg);
     return make_uint2(zs, zb);
 }
 
@@ -131,16 +150,20 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a, uint32_t* counts,
             const IrfDev& f = a.irf_of_pix ? a.irfs[a.irf_of_pix[p]] : a.irfs[0];
             const uint32_t k0 = a.boff[p], k1 = a.boff[p + 1];
             uint32_t base = WRITE ? off[p] : 0;
+            const uint32_t end = WRITE ? off[p + 1] : 0;
+            if (WRITE && end == base) return;  // no events: nothing to write
+            const PixelRng R = pixel_rng(a, p, g);
             for (int t0 = 0; t0 < a.bins; t0 += 32) {
                 const int t = t0 + lane;
                 uint2 z = make_uint2(0, 0);
-                if (t < a.bins) z = sample_bin(a, f, p, g, t, k0, k1);
+                if (t < a.bins) z = sample_bin(a, f, R, p, g, t, k0, k1);
                 const uint32_t tot = z.x + z.y;
                 const unsigned m = __ballot_sync(0xffffffffu, tot > 0);
                 if (WRITE) {
                     if (tot > 0)
                         events[base + __popc(m & ((1u << lane) - 1))] = make_uint2((uint32_t)t, tot);
                     base += __popc(m);
+                    if (base == end) break;  // the pixel's last event is written
                 } else {
                     n += __popc(m);
                     sig += z.x;

@@ -1,7 +1,8 @@
-"""Frames/s on the other SURVEY.md §8d configurations (A, C), one stream, CUDA
+"""Frames/s on the other SURVEY.md §8d configurations (A, C; D, E on request), one stream, CUDA
 events around each frame (inputs resident), plus a short-run parity check
 against the C oracle (max |dt| and point counts after `check_iters`).
-usage: python tools/bench_configs.py [frames]"""
+usage: python tools/bench_configs.py [frames] [A C D E ...]
+(E, 1M pixels, skips the oracle check: the oracle needs minutes per iteration.)"""
 import json
 import sys
 import time
@@ -46,6 +47,33 @@ def config_c(frame=0):
     return "C 32x32x153 superres 3 (96x96), three surfaces, ~900 photons/px", spec, 1000 + frame, cfg
 
 
+def _camouflage(n, scale):
+    """a camouflage net with a grid of holes at
+    5 m, a target bump at 8 m, a back plane at 12 m (<= 3 surfaces per px)."""
+    pitch = 0.02
+    step, hole = 16 * scale, 8 * scale
+    holes = [(a, b, a + hole, b + hole) for a in range(0, n, step) for b in range(0, n, step)]
+    c = n * pitch / 2
+    return [SurfaceSpec(depth_m=5.0, holes=holes),
+            SurfaceSpec(kind="bump", depth_m=8.0, bump_amp=-0.5, bump_cx=c, bump_cy=c,
+                        bump_width=0.4 * c),
+            SurfaceSpec(depth_m=12.0)]
+
+
+def config_d():
+    spec = SceneSpec(rows=256, cols=256, bins=2048, bin_resolution_m=0.01, pixel_pitch_m=0.02,
+                     irf_sigma_bins=1.5, target_ppp=30.0, target_sbr=1.0,
+                     surfaces=_camouflage(256, 1))
+    return "D 256x256x2048 camouflage, ~60 photons/px", spec, 256, config_a()[3]
+
+
+def config_e():
+    spec = SceneSpec(rows=1024, cols=1024, bins=2048, bin_resolution_m=0.01, pixel_pitch_m=0.02,
+                     irf_sigma_bins=1.5, target_ppp=50.0, target_sbr=1.0,
+                     surfaces=_camouflage(1024, 4))
+    return "E 1024x1024x2048 camouflage, ~100 photons/px", spec, 1024, config_a()[3]
+
+
 def run(name, spec, seed, cfg, frames, check_iters=3):
     import dataclasses
     import oracle_lib as O
@@ -75,6 +103,8 @@ def run(name, spec, seed, cfg, frames, check_iters=3):
         out["kernel_ms_per_frame"] = {k: round(v[0] / 3, 3) for k, v in kt.items() if v[1]}
         out.update({"ms_per_frame": sum(ms) / frames, "frames_per_s": 1e3 * frames / sum(ms),
                     "points": int(rep["points"]), "iterations": int(rep["iterations"])})
+        if check_iters == 0:
+            return out
         short = dataclasses.replace(cfg, max_iters=check_iters)
         g = s.reconstruct(short)
         t0 = time.perf_counter()
@@ -93,8 +123,12 @@ def run(name, spec, seed, cfg, frames, check_iters=3):
 
 def main():
     frames = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-    for name, spec, seed, cfg in (config_a(), config_c()):
-        print(json.dumps(run(name, spec, seed, cfg, frames)), flush=True)
+    which = sys.argv[2:] or ["A", "C"]
+    table = {"A": (config_a, 3), "C": (config_c, 3), "D": (config_d, 1), "E": (config_e, 0)}
+    for key in which:
+        make, check = table[key]
+        name, spec, seed, cfg = make()
+        print(json.dumps(run(name, spec, seed, cfg, frames, check)), flush=True)
 
 
 if __name__ == "__main__":
