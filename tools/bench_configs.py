@@ -101,6 +101,8 @@ def run(name, spec, seed, cfg, frames, check_iters=3):
         kt = s.kernel_times()
         s.time_kernels(False)
         out["kernel_ms_per_frame"] = {k: round(v[0] / 3, 3) for k, v in kt.items() if v[1]}
+        out["backtracks_per_frame"] = {b: int(rep["steps"][f"{b}_backtracks"].sum())
+                                       for b in ("depth", "intensity", "background")}
         out.update({"ms_per_frame": sum(ms) / frames, "frames_per_s": 1e3 * frames / sum(ms),
                     "points": int(rep["points"]), "iterations": int(rep["iterations"])})
         if check_iters == 0:
