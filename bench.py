@@ -195,6 +195,33 @@ def load_measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+B200_FP64_NOMINAL_TFLOPS = 37.0  # NVIDIA B200 datasheet (vector FP64); not measured here
+
+
+def apss_fp64(points, radius: float, us_per_launch: float):
+    """The APSS kernel against the FP64 roof: ~70 flop per
+    (point, neighbour) pair for distance, weight, mean, covariance and the
+    Pratt moments, plus ~3000 flop per point for the 3x3 and 5x5 eigensolves.
+    Neighbour counts come from the final cloud (ball of `radius`, self
+    included), so this is an estimate of one launch's flops."""
+    try:
+        from scipy.spatial import cKDTree
+    except ImportError:
+        return None
+    if len(points) == 0 or not us_per_launch:
+        return None
+    xyz = np.stack([points["x"], points["y"], points["z"]], axis=1)
+    nbrs = cKDTree(xyz).query_ball_point(xyz, radius, return_length=True)
+    flops = 70.0 * float(np.sum(nbrs)) + 3000.0 * len(points)
+    achieved = flops / (us_per_launch * 1e-6) / 1e12
+    return {"achieved": achieved, "unit": "TFLOP/s", "peak": B200_FP64_NOMINAL_TFLOPS,
+            "frac": achieved / B200_FP64_NOMINAL_TFLOPS, "flops_per_launch": flops,
+            "mean_neighbours": float(np.mean(nbrs)),
+            "peak_source": "nominal B200 FP64 (datasheet), not measured",
+            "note": "APSS is FP64-issue-bound at this size; the HBM fraction above is "
+                    "~0 because its working set stays in L2"}
+
+
 def ncu_traffic_per_launch(cls: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of a kernel
     class, from the committed `ncu --set full` capture summary."""
@@ -463,6 +490,11 @@ def main():
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if dom == "apss":
+            pts, _ = sess.state()
+            fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"])
+            if fp:
+                line["roofline"]["fp64"] = fp
         print(json.dumps(line), flush=True)
     sess.close()
     for r in ring:
