@@ -924,9 +924,15 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     // opt-in (RT3D_FUSED_ITER=1): measured slower on config B, the neighbour
     // phases run at the stage kernels' occupancy
     F.cfg.fused_iter = (F.cfg.fuse_depth && getenv("RT3D_FUSED_ITER")) ? 1 : 0;
-    // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND)
+    // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND).
+    // Default: two intensity candidates on frames below 2^20 events, where
+    // the intensity block backtracks nearly every iteration and sweeps are
+    // latency-bound; one candidate on large arrays, where backtracks are rare
+    // and the second candidate is paid in full (config D: -5%,
+    // profiles/r01_d_switch_sweep.jsonl)
     F.cfg.two_cand = getenv("RT3D_ONE_CAND") ? 0
-                     : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND")) : 1;
+                     : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND"))
+                     : (s->n_events >= (1ull << 20) ? 0 : 1);
     {
         // first kNN window: about k fine pixels; no pruning on huge grids
         // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
