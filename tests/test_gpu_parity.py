@@ -285,6 +285,27 @@ def test_two_candidate_sweeps_agree(gpu, name):
     assert np.array_equal(a["steps"], b["steps"])
 
 
+def test_large_array_one_candidate_default_agrees(gpu):
+    """Frames of 2^20+ events default to one-candidate intensity sweeps
+    (rt3d.cu build_frame); on config D they take exactly the decisions of
+    forced two-candidate sweeps (both blocks)."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import bench_configs
+    from paper_1905_06700_b200.scene import simulate
+    _, spec, seed, cfg = bench_configs.config_d()
+    cfg.max_iters = 3
+    sc = simulate(spec, seed)
+    assert len(sc.events) >= (1 << 20)       # takes the large-array default
+    a = _recon_with_env(gpu, sc, cfg, {})
+    b = _recon_with_env(gpu, sc, cfg, {"RT3D_TWO_CAND": "3"})
+    assert np.array_equal(a["points"], b["points"])
+    assert np.array_equal(a["background"], b["background"])
+    assert np.array_equal(a["trace"], b["trace"])
+    assert np.array_equal(a["steps"], b["steps"])
+
+
 def test_concurrent_sessions_match_sequential(gpu):
     """Two sessions sized to share the device (rt3d_session_set_sharing)
     reconstructing alternate frames concurrently give the sequential results."""
