@@ -397,15 +397,25 @@ def _edge_scenes():
             "sparse_half_photon": (sparse, cfg)}
 
 
+@pytest.mark.parametrize("bg_mode", [0, 1])
 @pytest.mark.parametrize("name", ["dead_pixels_holes", "empty_cube", "sparse_half_photon"])
-def test_reconstruct_edge_cubes_match_oracle(gpu, name):
+def test_reconstruct_edge_cubes_match_oracle(gpu, name, bg_mode):
     """Ragged inputs the reference's tests exercise: dead (zero-event)
-    pixels, an all-empty cube, and a cube at half a photon per pixel.  The
-    CUDA path and the C oracle agree (same tolerances as the golden scenes)."""
+    pixels, an all-empty cube, and a cube at half a photon per pixel, with
+    the identity and the FFT background.  The CUDA path and the C oracle
+    agree (same tolerances as the golden scenes), and the streaming API
+    (frame_submit / frame_collect) returns the same frame."""
+    import dataclasses
     sc, cfg = _edge_scenes()[name]
+    if bg_mode:
+        cfg = dataclasses.replace(cfg, background_mode=1, fft_cutoff=0.4)
     gpu.set_scene(sc)
     rep = gpu.reconstruct(cfg)
     ref = O.reconstruct(sc, cfg, "oracle")
     assert rep["iterations"] == ref["iterations"]
     _assert_recon_parity(rep, ref, name)
-    np.testing.assert_allclose(rep["background"], ref["background"], rtol=1e-9, atol=1e-15)
+    np.testing.assert_allclose(rep["background"], ref["background"],
+                               rtol=1e-7 if bg_mode else 1e-9, atol=1e-12 if bg_mode else 1e-15)
+    pts, bg, _ = gpu.frame_collect(gpu.frame_submit(sc, cfg))
+    assert np.array_equal(pts, rep["points"])
+    assert np.array_equal(bg, rep["background"])
