@@ -419,3 +419,21 @@ def test_reconstruct_edge_cubes_match_oracle(gpu, name, bg_mode):
     pts, bg, _ = gpu.frame_collect(gpu.frame_submit(sc, cfg))
     assert np.array_equal(pts, rep["points"])
     assert np.array_equal(bg, rep["background"])
+
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-5])
+@pytest.mark.parametrize("name", ["two_surface_24", "small_s13", "dense_12"])
+def test_reconstruct_early_stop_matches_oracle(gpu, name, tol):
+    """stop_tol > 0: the relative-nll stopping rule (reconstruct.hpp's PALM
+    loop) ends the device loop at the oracle's iteration, with the same
+    cloud and trace."""
+    import dataclasses
+    sc, cfg, _ = G.scene(name)
+    cfg = dataclasses.replace(cfg, stop_tol=tol, max_iters=40)
+    ref = O.reconstruct(sc, cfg, "oracle")
+    gpu.set_scene(sc)
+    rep = gpu.reconstruct(cfg)
+    assert rep["iterations"] == ref["iterations"], (rep["iterations"], ref["iterations"])
+    _assert_recon_parity(rep, ref, f"{name}/tol{tol}")
+    pts, bg, r2 = gpu.frame_collect(gpu.frame_submit(sc, cfg))
+    assert np.array_equal(pts, rep["points"]) and r2["iterations"] == rep["iterations"]
