@@ -113,3 +113,41 @@ def test_device_decode_errors(gpu):
         assert expect[kind] in str(ei.value), (kind, str(ei.value))
     gpu.set_cube_spcb(encode_spcb(sc))             # a good cube afterwards
     gpu.reconstruct(cfg)
+
+
+def test_set_cube_validation_errors(gpu):
+    """rt3d_set_cube applies PhotonCube::validate (cube.hpp:84-112) to the
+    caller's CSR: each violation is RT3D_ERR_FORMAT with the reference's
+    message, and the session stays usable."""
+    import copy
+    from paper_1905_06700_b200.rt3d import Rt3dError
+    sc, cfg, _ = G.scene("small_s3")
+    gpu.set_scene(sc)
+    p = int(np.argmax(np.diff(sc.offsets.astype(np.int64)) >= 2))   # a pixel with 2+ events
+    k = int(sc.offsets[p])
+
+    def bad(mut):
+        b = copy.copy(sc)
+        b.offsets, b.events = sc.offsets.copy(), sc.events.copy()
+        mut(b)
+        return b
+
+    cases = {
+        "cube: non-positive dimensions": bad(lambda b: setattr(b, "n_bins", 0)),
+        "cube: bad offset table": bad(lambda b: b.offsets.__setitem__(-1, b.offsets[-1] - 1)),
+        "cube: bins not strictly increasing at pixel": bad(
+            lambda b: b.events.__setitem__(k + 1, (b.events[k]["bin"], 1))),
+        "cube: bin out of range at pixel": bad(
+            lambda b: b.events.__setitem__(k + 1, (b.n_bins, 1))),
+        "cube: zero count at pixel": bad(lambda b: b.events.__setitem__(k, (b.events[k]["bin"], 0))),
+    }
+    for msg, b in cases.items():
+        with pytest.raises(Rt3dError) as ei:
+            gpu.set_cube(b)
+        assert ei.value.status == 2, msg           # RT3D_ERR_FORMAT
+        assert msg in str(ei.value), (msg, str(ei.value))
+        if "pixel" in msg:
+            assert str(ei.value).rstrip().endswith(f"pixel {p}"), str(ei.value)
+    gpu.set_cube(sc)                               # a good cube afterwards
+    rep = gpu.reconstruct(cfg)
+    assert len(rep["points"]) > 0
