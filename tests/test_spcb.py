@@ -115,6 +115,7 @@ def test_device_decode_errors(gpu):
     gpu.reconstruct(cfg)
 
 
+@pytest.mark.gpu
 def test_set_cube_validation_errors(gpu):
     """rt3d_set_cube applies PhotonCube::validate (cube.hpp:84-112) to the
     caller's CSR: each violation is RT3D_ERR_FORMAT with the reference's
