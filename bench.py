@@ -35,26 +35,24 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-from paper_1905_06700_b200.abi import Config  # noqa: E402
-from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
+sys.path.insert(0, str(ROOT / "tools"))
+import workloads  # noqa: E402
 
 PAPER_MS_PER_FRAME = 13.0  # 141x141x4613 on a Titan Xp
 
 
 def config_b():
     """141x141 px, 4613 bins of 0.3 mm."""
-    pitch = 0.0025
-    spec = SceneSpec(
-        rows=141, cols=141, bins=4613, bin_resolution_m=0.0003, pixel_pitch_m=pitch,
-        irf_sigma_bins=1.5, target_ppp=3.0, target_sbr=13.0,
-        surfaces=[
-            SurfaceSpec(depth_m=1.2, holes=[(40, 30, 101, 121)]),
-            SurfaceSpec(kind="bump", depth_m=1.0, bump_amp=-0.12, bump_width=0.06,
-                        bump_cx=70.5 * pitch, bump_cy=75.5 * pitch, region=(35, 25, 106, 126)),
-        ])
-    cfg = Config(max_iters=25, stop_tol=0.0, apss_radius=0.02, knn_k=9, r_min=0.25,
-                 init_max_returns=3, init_peak_threshold=0.5, init_min_separation=6)
-    return spec, 141, cfg, "141x141 px x 4613 bins polystyrene-head-like synthetic frame"
+    name, spec, seed, cfg = workloads.config_b()
+    return spec, seed, cfg, name
+
+
+def shared_config(spec, cfg, n_events) -> dict:
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": workloads.config_b()[0], "pixels": spec.rows * spec.cols,
+            "bins": spec.bins, "palm_iterations": cfg.max_iters, "events": int(n_events),
+            "recon": "acceptance preset, apss_radius 0.02 m, stop_tol 0 (fixed budget)",
+            "l2": "GPU arm: flushed between frames (256 MB write)"}
 
 
 KERNEL_NAMES = {
@@ -234,12 +232,15 @@ def ncu_traffic_per_launch(cls: str):
     return None
 
 
-def reference_frame_seconds(sc, cfg, threads: int = 0):
+def reference_frame(sc, cfg, threads: int = 0):
     """The reference implementation itself (headers compiled unchanged,
-    oracle/_ref/libref.so) timed on the host cores; else the C port."""
+    oracle/_ref/libref.so) timed on the host cores with steady_clock around
+    splidar::reconstruct (the bench_scaling method, eval.hpp:229-233); else
+    the C port.  Returns (seconds, kind, cores, cloud)."""
     import ctypes as C
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
+    from paper_1905_06700_b200.abi import POINT_DTYPE, Point, ptr
     if O.ref_available():
         lib = O.ref()
         lib.ref_set_threads(threads)
@@ -248,21 +249,34 @@ def reference_frame_seconds(sc, cfg, threads: int = 0):
                                  C.byref(cfg.to_c()), C.byref(n), C.byref(it), C.byref(secs))
         if rc != 0:
             raise RuntimeError(lib.ref_last_error().decode())
+        cloud = np.zeros(max(n.value, 1), POINT_DTYPE)
+        lib.ref_result_copy(ptr(cloud, Point), None)
         cores = threads if threads > 0 else (os.cpu_count() or 1)
-        return secs.value, "reference", cores
+        return secs.value, "reference", cores, cloud[: n.value]
     t0 = time.perf_counter()
-    O.reconstruct(sc, cfg, "oracle")
-    return time.perf_counter() - t0, "port", 1
+    r = O.reconstruct(sc, cfg, "oracle")
+    return time.perf_counter() - t0, "port", 1, r["points"]
+
+
+def reference_cube(spec, seed):
+    """The workload's cube from the reference's own simulate_cube
+    (simulate.hpp:139-223, oracle/_ref/libref.so) on the SceneSpec text."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    if O.ref_available():
+        return O.ref_simulate(workloads.spec_text(spec), seed)
+    from scenegen.scene import simulate
+    return simulate(spec, seed)
 
 
 def run_reference_arm(args, world, rank):
     if rank != 0:
         return 0
     spec, seed, cfg, workload = config_b()
-    sc = simulate(spec, seed)
+    sc = reference_cube(spec, seed)
     times = []
     for k in range(args.warmup + args.steps):
-        secs, kind, cores = reference_frame_seconds(sc, cfg)
+        secs, kind, cores, _ = reference_frame(sc, cfg)
         if k >= args.warmup:
             times.append(secs)
     total = sum(times)
@@ -272,16 +286,43 @@ def run_reference_arm(args, world, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload, "pixels": 141 * 141, "bins": 4613,
-                   "palm_iterations": cfg.max_iters, "events": int(len(sc.events))},
+        "config": shared_config(spec, cfg, len(sc.events)),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": f"{len(times)} full frames (25 PALM iterations) after "
-                                   f"{args.warmup} warm-up frames"},
+                                   f"{args.warmup} warm-up frames; cube from the reference's "
+                                   "own simulate_cube"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def parity_block(sess, sc, cfg, ref_cloud, gpu_cloud) -> dict:
+    """bench-time parity at the benchmarked workload (tests/parity.py): the
+    GPU cloud of the timed frames against the reference's own cloud from the
+    cpu_baseline run (free running, reported), every PALM step against the
+    reference from its own state (asserted by the tests), and the full
+    reconstruction against the C oracle (same trajectory)."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_lib as O
+    import parity as PY
+    out = {"tolerance": {"t_bins": PY.T_TOL_BINS, "r_rel": PY.R_TOL_REL, "count_rel": PY.COUNT_TOL}}
+    if ref_cloud is not None:
+        out["vs_reference_free_running"] = PY.cloud_diff(gpu_cloud, ref_cloud)
+    if O.ref_available():
+        out["init_bitexact_vs_reference"] = PY.init_bitexact(sess, sc, cfg, "ref")
+        w = PY.stepwise(sess, sc, cfg, "ref")
+        w["within_tolerance"] = bool(w["same_cells"] and w["count_rel"] <= PY.COUNT_TOL and
+                                     w["max_dt_bins"] <= PY.T_TOL_BINS and
+                                     w["max_rel_dr"] <= PY.R_TOL_REL)
+        out["vs_reference_stepwise"] = w
+    t0 = time.perf_counter()
+    d = PY.free_running(sess, sc, cfg, "oracle")
+    d["within_tolerance"] = PY.within_tolerance(d)
+    d["oracle_seconds"] = time.perf_counter() - t0
+    out["vs_oracle_free_running"] = d
+    return out
 
 
 def main():
@@ -292,6 +333,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_init()
@@ -304,6 +346,7 @@ def main():
     from paper_1905_06700_b200.rt3d import Session
 
     torch.cuda.set_device(local)
+    from scenegen.scene import simulate
     spec, seed, cfg, workload = config_b()
     sc = simulate(spec, seed)
     sess = Session(local)
@@ -357,17 +400,6 @@ def main():
     value = world * K / dev_s_max
     rep = sess.report()
     pts, _ = sess.state()
-
-    # phase breakdown of one (untimed) frame from the in-kernel timer
-    sess.profile(True)
-    sess.reconstruct_async(cfg)
-    sess.synchronize()
-    phases = {}
-    for name, ns in sess.profile_phases():
-        d = phases.setdefault(name, [0, 0.0])
-        d[0] += 1
-        d[1] += ns / 1e3
-    sess.profile(False)
 
     # e2e through the C ABI from pinned host buffers
     n_e2e = args.e2e_steps or max(2 * K, 40)
@@ -437,11 +469,14 @@ def main():
     launches = sum(n for _, n in ktimes.values())
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        secs, kind, cores = reference_frame_seconds(sc, cfg)
+        secs, kind, cores, ref_cloud = reference_frame(sc, cfg)
         cpu = {"value": 1.0 / secs, "unit": "frames/s", "cores": cores, "kind": kind,
                "sample": "1 full frame of the same workload (25 PALM iterations), "
                          "reference headers compiled unchanged (oracle/_ref), all host threads"}
+        if not args.no_parity:
+            parity = parity_block(sess, sc, cfg, ref_cloud, pts)
 
     if rank == 0:
         line = {
@@ -450,12 +485,10 @@ def main():
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": value / (1000.0 / PAPER_MS_PER_FRAME),
             "dtype": "f64", "data": "synthetic",
-            "config": {
-                "workload": workload, "pixels": 141 * 141, "bins": 4613,
-                "palm_iterations": cfg.max_iters, "events": int(len(sc.events)),
+            "config": shared_config(spec, cfg, len(sc.events)),
+            "details": {
                 "points_init": int(rep["steps"][0]["points_before"]) if len(rep["steps"]) else 0,
                 "points_final": int(rep["points"]), "parallelism": f"frames x{world} (replicas)",
-                "l2": "flushed between frames (256 MB write)",
                 "vs_baseline_ref": "paper GPU 13 ms/frame on Titan Xp (BASELINE.md)",
                 "ms_per_frame_p50": statistics.median(frame_ms),
                 "ms_per_frame_min": min(frame_ms),
@@ -484,14 +517,13 @@ def main():
             "kernel_classes": classes,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
-            "phases_us_per_frame": {k: round(v[1], 1) for k, v in phases.items()},
-            "phase_counts": {k: v[0] for k, v in phases.items()},
             "wall_s_timed_region": t_wall,
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        if parity:
+            line["parity"] = parity
         if dom == "apss":
-            pts, _ = sess.state()
             fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"])
             if fp:
                 line["roofline"]["fp64"] = fp

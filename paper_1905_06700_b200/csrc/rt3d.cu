@@ -679,6 +679,10 @@ rt3d_status fail(rt3d_status st, const char* fmt, ...) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }  // every member buffer goes with its session
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap && p) return cudaSuccess;
         if (p) cudaFree(p);
@@ -724,6 +728,7 @@ struct rt3d_session {
     bool have_cube = false;
     int c_rows = 0, c_cols = 0, c_bins = 0;
     uint64_t n_events = 0;
+    uint64_t lam_cap = 0;  // event capacity of the sweep spill slots (Frame::nev)
     DevBuf off, ev;
     // pipelined frames (rt3d_frame_submit / rt3d_frame_collect): a second
     // cube slot, a copy stream, result slots
@@ -740,6 +745,7 @@ struct rt3d_session {
     uint64_t next_ticket = 0;
     int inflight[2] = {0, 0};
     uint64_t slot_ticket[2] = {0, 0};
+    size_t slot_npix[2] = {0, 0};  // background size of the frame in each slot
     // state
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
@@ -850,8 +856,12 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.wpb = 1 << (F.G - F.Gb);
     F.nbn = 1u << F.Gb;
     // scratch
-    CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->n_events, 1) * 32));
-    F.nev = s->n_events;
+    // per-event spill slots strided by a power-of-two capacity, not by this
+    // cube's event count: the Frame bytes (the CUDA-graph cache key) then
+    // stay the same across the frames of a stream
+    while (s->lam_cap < s->n_events) s->lam_cap = s->lam_cap ? 2 * s->lam_cap : 4096;
+    CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->lam_cap, 1) * 32));
+    F.nev = s->lam_cap;
     CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
     CUDA_TRY(s->tblk.ensure((size_t)npix * 32 + 64));
     CUDA_TRY(s->tbmax.ensure((size_t)npix * 16 + 64));
@@ -1389,12 +1399,6 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     cudaSetDevice(s->device);
     cudaStreamSynchronize(s->stream);
     for (int k = 0; k < (int)(sizeof(s->gc) / sizeof(s->gc[0])); ++k) graph_cache_drop(s, k);
-    DevBuf* bufs[] = {&s->irfs, &s->irf_tab, &s->irf_of_pix, &s->gain, &s->dead, &s->off, &s->ev,
-                      &s->gt, &s->ct, &s->gr, &s->cr, &s->gb, &s->cb, &s->oog, &s->lam, &s->blk, &s->part,
-                      &s->bmax, &s->cnt, &s->btot, &s->pk_t, &s->pk_resp, &s->pk_mass,
-                      &s->pk_int, &s->npk, &s->nval, &s->fft_re, &s->fft_im, &s->amom, &s->tblk, &s->tbmax, &s->ctl, &s->diag,
-                      &s->trace, &s->outpts, &s->misc};
-    for (DevBuf* b : bufs) b->release();
     for (auto& t : s->timed) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -1406,32 +1410,18 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
             cudaEventDestroy(s->cube_ready[k]);
             cudaEventDestroy(s->frame_done[k]);
             if (s->h_off[k]) cudaFreeHost(s->h_off[k]);
-            s->res_pts[k].release();
-            s->res_bg[k].release();
-            s->res_ctl[k].release();
         }
         cudaFreeHost(s->h_res_ctl);
         cudaStreamDestroy(s->cstream);
     }
-    s->off2.release();
-    s->ev2.release();
-    s->mig[0].release();
-    s->mig[1].release();
-    for (int k = 0; k < 2; ++k) {
-        s->t[k].release();
-        s->r[k].release();
-        s->b[k].release();
-        s->pix[k].release();
-        s->fi[k].release();
-        s->fj[k].release();
-        s->fl[k].release();
-        s->bo[k].release();
-    }
     if (s->h_ctl) cudaFreeHost(s->h_ctl);
+    if (s->h_dbg) cudaFreeHost(s->h_dbg);
+    if (s->d_dbg) cudaFree(s->d_dbg);
+    if (s->side) cudaStreamDestroy(s->side);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->stream) cudaStreamDestroy(s->stream);
-    delete s;
+    delete s;  // DevBuf members free their device memory
     return RT3D_OK;
 }
 
@@ -1727,6 +1717,10 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     rt3d_status st = require_device(s);
     if (st) return st;
     if ((st = validate_cfg(cfg))) return st;
+    // reconstruct -> palm_step -> fft_background_denoise (denoise.hpp:269-270)
+    if (program == PROG_RECON && cfg->background_mode == 1 && s->have_sensor &&
+        (s->rows < 2 || s->cols < 2))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "fft_lowpass_filter: image must be at least 2x2");
     Cfg g = cfg_from(cfg, program);
     const size_t npix = (size_t)s->rows * s->cols;
     const size_t pcap = program == PROG_BASELINE
@@ -1835,6 +1829,7 @@ rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* c, const rt3d_re
     CUDA_TRY(cudaEventRecord(s->frame_done[slot], s->stream));
     s->inflight[slot] = 1;
     s->slot_ticket[slot] = s->next_ticket;
+    s->slot_npix[slot] = npix;
     *ticket = s->next_ticket++;
     return RT3D_OK;
 }
@@ -1851,16 +1846,17 @@ rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* pts
     CUDA_TRY(cudaMemcpyAsync(s->h_res_ctl, s->res_ctl[slot].p, sizeof(Ctl), cudaMemcpyDeviceToHost,
                              s->cstream));
     CUDA_TRY(cudaStreamSynchronize(s->cstream));
-    s->inflight[slot] = 0;
     const Ctl& c = *s->h_res_ctl;
-    if (c.abort)
-        return fail(RT3D_ERR_CUDA, "rt3d: grid barrier watchdog aborted frame %llu",
-                    (unsigned long long)ticket);
     if (n_points) *n_points = c.P;
+    // a buffer too small keeps the frame in flight: collect it again with room
     if (pts && c.P > cap)
         return fail(RT3D_ERR_OUT_OF_RANGE, "rt3d: %u points do not fit in %llu", c.P,
                     (unsigned long long)cap);
-    const size_t npix = (size_t)s->rows * s->cols;
+    s->inflight[slot] = 0;
+    if (c.abort)
+        return fail(RT3D_ERR_CUDA, "rt3d: grid barrier watchdog aborted frame %llu",
+                    (unsigned long long)ticket);
+    const size_t npix = s->slot_npix[slot];
     if (pts && c.P)
         CUDA_TRY(cudaMemcpyAsync(pts, s->res_pts[slot].p, (size_t)c.P * sizeof(rt3d_point),
                                  cudaMemcpyDeviceToHost, s->cstream));

@@ -1,11 +1,11 @@
 /*
- * scene.c — libscene.so: synthetic photon cubes (include/rt3d_scene.h).
+ * scene.c — libscene.so: synthetic photon cubes (scenegen/rt3d_scene.h).
  * Restates the reference's forward simulator (simulate.hpp:139-223) and its
  * counter-based RNG (rng.hpp:11-98) so that benchmark inputs of the named
  * shapes can be made on the GPU box, bit-identical to the reference's cubes.
  * Compiled without FMA contraction, like the reference's Release build.
  */
-#include "../../include/rt3d_scene.h"
+#include "rt3d_scene.h"
 
 #include <math.h>
 #include <pthread.h>

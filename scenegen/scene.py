@@ -1,4 +1,4 @@
-"""Synthetic scenes (libscene.so, include/rt3d_scene.h): a restatement of the
+"""Synthetic scenes (scenegen/libscene.so, scenegen/rt3d_scene.h): a restatement of the
 reference's simulate_cube (simulate.hpp:139-223) used to make benchmark
 inputs of the shapes BASELINE.json names."""
 from __future__ import annotations
@@ -10,7 +10,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .abi import EVENT_DTYPE, POINT_DTYPE, Event, Point, Scene, ptr
+from paper_1905_06700_b200.abi import EVENT_DTYPE, POINT_DTYPE, Event, Point, Scene, ptr
 
 LIB_PATH = Path(__file__).resolve().parent / "libscene.so"
 

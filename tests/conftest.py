@@ -4,7 +4,7 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
-for p in (str(ROOT), str(ROOT / "tests")):
+for p in (str(ROOT), str(ROOT / "tests"), str(ROOT / "tools")):
     if p not in sys.path:
         sys.path.insert(0, p)
 

@@ -120,6 +120,7 @@ def ref() -> C.CDLL:
                P(StepDiag), P(C.c_int)])
         _bind(lib, "ref_reconstruct", C.c_int,
               [P(Cube), P(Sensor), P(ReconConfig), P(_u64), P(C.c_int), P(_dbl)])
+        _bind(lib, "ref_result_copy", C.c_int, [P(Point), P(_dbl)])
         _bind(lib, "ref_evaluate", C.c_int, [P(Point), _u64, P(Point), _u64, _dbl, _dbl, P(_dbl)])
         _bind(lib, "ref_baseline_xcorr", C.c_int, [P(Cube), P(Sensor), P(Point), P(_u64)])
         _bind(lib, "ref_simulate", C.c_int,

@@ -1,5 +1,5 @@
-"""CPU: librt3d.so / libscene.so load, export every symbol include/*.h
-declares, and refuse to compute without a CUDA device (no CPU fallback)."""
+"""CPU: librt3d.so (and the input generator scenegen/libscene.so) load, export
+every symbol their headers declare, and refuse to compute without a CUDA device (no CPU fallback)."""
 import ctypes as C
 import re
 from pathlib import Path
@@ -7,13 +7,14 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-from paper_1905_06700_b200 import abi, rt3d, scene
+from paper_1905_06700_b200 import abi, rt3d
+from scenegen import scene
 
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def declared(header):
-    text = (ROOT / "include" / header).read_text()
+def declared(header, where="include"):
+    text = (ROOT / where / header).read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(rt3d_[a-z0-9_]+)\s*\(", text)))
 
@@ -30,7 +31,7 @@ def test_librt3d_exports_every_declared_symbol():
 
 def test_libscene_exports_every_declared_symbol():
     L = scene.lib()
-    for n in declared("rt3d_scene.h"):
+    for n in declared("rt3d_scene.h", "scenegen"):
         assert hasattr(L, n), n
 
 

@@ -27,7 +27,7 @@ def _frame_digest(f):
     synthetic frame (test infrastructure as the checker)."""
     import oracle_lib as O
     from paper_1905_06700_b200.abi import Config
-    from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate
+    from scenegen.scene import SceneSpec, SurfaceSpec, simulate
     spec = SceneSpec(rows=6, cols=6, bins=120, bin_resolution_m=0.01, pixel_pitch_m=0.02,
                      target_ppp=20, target_sbr=5,
                      surfaces=[SurfaceSpec(depth_m=0.5 + 0.01 * f)])

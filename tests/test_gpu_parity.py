@@ -195,7 +195,7 @@ def test_knn_window_pruning_is_exact(gpu, name):
         from pathlib import Path
         sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
         import bench
-        from paper_1905_06700_b200.scene import simulate
+        from scenegen.scene import simulate
         spec, seed, cfg, _ = bench.config_b()
         cfg.max_iters = 4
         sc = simulate(spec, seed)
@@ -271,7 +271,7 @@ def test_two_candidate_sweeps_agree(gpu, name):
         from pathlib import Path
         sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
         import bench
-        from paper_1905_06700_b200.scene import simulate
+        from scenegen.scene import simulate
         spec, seed, cfg, _ = bench.config_b()
         cfg.max_iters = 6
         sc = simulate(spec, seed)
@@ -293,7 +293,7 @@ def test_large_array_one_candidate_default_agrees(gpu):
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
     import bench_configs
-    from paper_1905_06700_b200.scene import simulate
+    from scenegen.scene import simulate
     _, spec, seed, cfg = bench_configs.config_d()
     cfg.max_iters = 3
     sc = simulate(spec, seed)
@@ -378,7 +378,7 @@ def test_one_launch_iteration_matches_kernel_sequence(gpu, name):
 
 def _edge_scenes():
     import copy
-    from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate
+    from scenegen.scene import SceneSpec, SurfaceSpec, simulate
     from paper_1905_06700_b200.abi import Config
     cfg = Config(max_iters=8, stop_tol=0.0, apss_radius=0.08, knn_k=9, r_min=0.25,
                  init_max_returns=3, init_peak_threshold=0.5, init_min_separation=6)

@@ -6,7 +6,7 @@ import pytest
 
 import golden_io as G
 import oracle_lib as O
-from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate
+from scenegen.scene import SceneSpec, SurfaceSpec, simulate
 
 SPECS = {
     "small_s3": (SceneSpec(rows=16, cols=16, bins=300, bin_resolution_m=0.01, pixel_pitch_m=0.02,

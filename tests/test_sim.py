@@ -8,7 +8,7 @@ so the test allows a sample to differ only in a vanishing fraction of bins
 import numpy as np
 import pytest
 
-from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate
+from scenegen.scene import SceneSpec, SurfaceSpec, simulate
 from test_scene import SPECS
 
 MAX_DIFF_FRACTION = 1e-6   # of all (pixel, bin) samples

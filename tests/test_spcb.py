@@ -9,7 +9,7 @@ import pytest
 
 import golden_io as G
 import oracle_lib as O
-from paper_1905_06700_b200.scene import encode_spcb
+from scenegen.scene import encode_spcb
 
 
 def _ref_encode(sc):

@@ -16,7 +16,7 @@ import torch  # noqa: E402
 
 from paper_1905_06700_b200.abi import Config  # noqa: E402
 from paper_1905_06700_b200.rt3d import Session  # noqa: E402
-from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
+from scenegen.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
 
 
 def config_a():

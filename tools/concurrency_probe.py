@@ -5,7 +5,7 @@ sys.path.insert(0, '.')
 import numpy as np
 import bench
 from paper_1905_06700_b200.rt3d import Session
-from paper_1905_06700_b200.scene import simulate
+from scenegen.scene import simulate
 S = int(sys.argv[1]); N = int(sys.argv[2])
 spec, seed, cfg, _ = bench.config_b()
 sc = simulate(spec, seed)

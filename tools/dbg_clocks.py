@@ -4,7 +4,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
 import golden_io as G, bench
 from paper_1905_06700_b200 import rt3d
-from paper_1905_06700_b200.scene import simulate
+from scenegen.scene import simulate
 L = rt3d.lib()
 L.rt3d_debug_clocks.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
 for name in ["small_s3", "B"]:

@@ -3,7 +3,7 @@ import sys, hashlib
 sys.path.insert(0, '.')
 import bench
 from paper_1905_06700_b200.rt3d import Session
-from paper_1905_06700_b200.scene import simulate
+from scenegen.scene import simulate
 spec, seed, cfg, _ = bench.config_b()
 cfg.max_iters = int(sys.argv[1]) if len(sys.argv) > 1 else 25
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 6

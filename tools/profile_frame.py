@@ -7,7 +7,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_1905_06700_b200.rt3d import Session  # noqa: E402
-from paper_1905_06700_b200.scene import simulate  # noqa: E402
+from scenegen.scene import simulate  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 spec, seed, cfg, _ = bench.config_b()

@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 
 import bench  # noqa: E402
 from paper_1905_06700_b200.rt3d import Session  # noqa: E402
-from paper_1905_06700_b200.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
+from scenegen.scene import SceneSpec, SurfaceSpec, simulate  # noqa: E402
 
 
 def config_d():

@@ -2,7 +2,7 @@ import sys, os
 sys.path.insert(0, os.getcwd())
 import bench
 from paper_1905_06700_b200.rt3d import Session
-from paper_1905_06700_b200.scene import simulate
+from scenegen.scene import simulate
 spec, seed = bench.config_b()[:2]
 sc = simulate(spec, seed)
 s = Session(0)
