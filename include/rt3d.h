@@ -251,9 +251,10 @@ rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
  * staging copy) on the session's copy stream into one of two device slots
  * and enqueues reconstruct (reconstruct.hpp:457-489) plus an end-of-frame copy
  * of the cloud and background into a result slot; it returns at once with a
- * ticket.  rt3d_frame_collect waits for that frame and copies its cloud
- * (cap points at most; *n_points receives the count), background and report
- * out.  At most two frames are in flight; `cube` must stay valid until its
+ * ticket.  rt3d_frame_collect waits for that frame and copies its cloud,
+ * background and report out; *n_points receives the count.  A cloud of more
+ * than cap points returns RT3D_ERR_OUT_OF_RANGE and copies nothing: the frame
+ * stays in flight and can be collected again with a larger buffer.  At most two frames are in flight; `cube` must stay valid until its
  * frame is collected. */
 rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* cube, const rt3d_recon_config* cfg,
                               uint64_t* ticket);

@@ -217,6 +217,9 @@ class Scene:
     dead: Optional[np.ndarray] = None
     points: Optional[np.ndarray] = None      # POINT_DTYPE
     background: Optional[np.ndarray] = None  # f8[npix]
+    # SensorModel::irf_per_pixel (sensor.hpp:160-164): None, or npix
+    # (samples, tau_min, dtau) tuples in row-major pixel order
+    irf_per_pixel: Optional[list] = None
     _keep: list = field(default_factory=list, repr=False)
 
     def __post_init__(self):
@@ -260,6 +263,18 @@ class Scene:
         s.bin_resolution = self.bin_resolution
         s.irf_shared = self.irf_c()
         s.irf_per_pixel = None
+        if self.irf_per_pixel is not None:
+            assert len(self.irf_per_pixel) == self.n_pixels
+            arr = (Irf * self.n_pixels)()
+            keep = []
+            for k, (smp, tmin, dt) in enumerate(self.irf_per_pixel):
+                smp = np.ascontiguousarray(smp, np.float64)
+                keep.append(smp)
+                arr[k].tau_min, arr[k].dtau = float(tmin), float(dt)
+                arr[k].samples = ptr(smp, C.c_double)
+                arr[k].n_samples = len(smp)
+            self._keep = [arr, keep]
+            s.irf_per_pixel = C.cast(arr, C.POINTER(Irf))
         s.gain = ptr(self.gain, C.c_double)
         s.dead = ptr(self.dead, C.c_uint8)
         return s

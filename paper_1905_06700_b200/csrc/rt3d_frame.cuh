@@ -1035,7 +1035,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
 // the same reduced values (its own Ctl copy in shared memory); only block 0
 // (`writer`) records the diagnostics and trace, and writes the state back to
 // F.ctl at the end of the kernel.
-__device__ void set_block(const Frame& F, Ctl* c, bool writer, int blk, double cmax, int it) {
+static __device__ void set_block(const Frame& F, Ctl* c, bool writer, int blk, double cmax, int it) {
     c->cmax = cmax;
     c->alpha = F.cfg.step_auto[blk] ? 1.0 : F.cfg.step[blk];
     c->bt = 0;
@@ -1053,7 +1053,7 @@ __device__ void set_block(const Frame& F, Ctl* c, bool writer, int blk, double c
     }
 }
 
-__device__ void controller(const Frame& F, Ctl* c, bool writer, int op, int it, double v,
+static __device__ void controller(const Frame& F, Ctl* c, bool writer, int op, int it, double v,
                            double cmax) {
     switch (op) {
         case OP_RESULT:
@@ -1764,7 +1764,7 @@ __device__ __forceinline__ double lowpass_mask(double rho, double cutoff) {
 }
 
 // stage 1: forward DFT along every row of img (real) -> (re, im)
-__device__ void fft_stage1(const double* img, double* re, double* im, int nr, int nc,
+static __device__ void fft_stage1(const double* img, double* re, double* im, int nr, int nc,
                            uint32_t gtid, uint32_t nth) {
     for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
         const int a = idx / nc, k = idx % nc;
@@ -1783,7 +1783,7 @@ __device__ void fft_stage1(const double* img, double* re, double* im, int nr, in
 }
 
 // stage 2: per column: forward DFT along rows, mask, backward DFT along rows
-__device__ void fft_stage2(double* re, double* im, double* re2, double* im2, int nr, int nc,
+static __device__ void fft_stage2(double* re, double* im, double* re2, double* im2, int nr, int nc,
                            double cutoff, uint32_t gtid, uint32_t nth) {
     const double fmax_r = (double)(nr / 2) / nr;
     const double fmax_c = (double)(nc / 2) / nc;
@@ -1809,7 +1809,7 @@ __device__ void fft_stage2(double* re, double* im, double* re2, double* im2, int
     }
 }
 
-__device__ void fft_stage3(const double* re2, const double* im2, double* re, double* im, int nr,
+static __device__ void fft_stage3(const double* re2, const double* im2, double* re, double* im, int nr,
                            int nc, uint32_t gtid, uint32_t nth) {
     // backward along rows (column direction) for each (a, b)
     for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {
@@ -1828,7 +1828,7 @@ __device__ void fft_stage3(const double* re2, const double* im2, double* re, dou
     }
 }
 
-__device__ void fft_stage4(const double* re, const double* im, double* out, int nr, int nc,
+static __device__ void fft_stage4(const double* re, const double* im, double* out, int nr, int nc,
                            int clamp_nonneg, uint32_t gtid, uint32_t nth) {
     const double total = (double)nr * nc;
     for (uint32_t idx = gtid; idx < (uint32_t)(nr * nc); idx += nth) {

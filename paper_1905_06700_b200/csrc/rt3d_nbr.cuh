@@ -205,7 +205,7 @@ __device__ __forceinline__ double warp_halving_sum(double v) {
 // APSS moments over the current state: warp per point, results to F.amom
 // (kMom doubles per point, one coalesced store per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
 // the covariance is read off M, see apss_pass_b).
-__device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t P, int tc, int sc) {
+static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t P, int tc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ApssWarpSm& A = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;
@@ -367,7 +367,7 @@ __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t P, i
 
 // sphere fit, projection and pinning, one thread per point
 // (denoise.hpp:186-214, reconstruct.hpp:352-363); writes t[tc^1] and flags
-__device__ void apss_fit_threads(const Frame& F, uint32_t P, int tc, int sc) {
+static __device__ void apss_fit_threads(const Frame& F, uint32_t P, int tc, int sc) {
     (void)F.amom_stride;
     for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < P; n += gridDim.x * blockDim.x) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
@@ -476,7 +476,7 @@ __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k,
 // the next ring, no member outside can enter the top k and the selection is
 // final; otherwise the window grows to the first ring whose bound exceeds
 // the k-th key (at most W, the full ball).
-__device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int tc, int rc, int sc) {
+static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int tc, int rc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KnnWarpSm& K = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;

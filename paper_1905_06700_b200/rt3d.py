@@ -307,8 +307,11 @@ class Session:
         try:
             _check(lib().rt3d_frame_collect(self.h, ticket, ptr(points, Point), len(points),
                                             C.byref(n), ptr(background, _dbl), C.byref(r)))
-        finally:
-            self._inflight.pop(ticket, None)
+        except Rt3dError as e:
+            if e.status != 3:  # OUT_OF_RANGE: the frame stays in flight (collect again)
+                self._inflight.pop(ticket, None)
+            raise
+        self._inflight.pop(ticket, None)
         rep = {"iterations": r.iterations, "points": int(r.points), "init_nll": r.init_nll,
                "final_nll": r.final_nll, "total_seconds": r.total_seconds}
         return points[: n.value], background, rep
