@@ -38,6 +38,7 @@ namespace rt3d {
 StageFn stage_fn_g4(int st);
 StageFn stage_fn_g32(int st);
 StageFn stage_fn_g3(int st);
+StageFn stage_fn_g1(int st);
 
 __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -389,9 +390,10 @@ struct rt3d_session {
     int nsm = 0;
     cudaStream_t stream = nullptr;
     int grid_frame = 0;      // max over the configs (per-block scratch sizing)
-    int grid_frame_c[3] = {0, 0, 0};  // cooperative grid of stage_kernel per lane-group config
-    int per_sm_c[3] = {0, 0, 0};      // co-resident stage blocks per SM per config
-    int want_per_sm = 2;              // RT3D_BLOCKS_PER_SM
+    int grid_frame_c[4] = {0, 0, 0, 0};  // cooperative grid of stage_kernel per lane-group config
+    int per_sm_c[4] = {0, 0, 0, 0};      // co-resident stage blocks per SM per config
+    int want_per_sm = 2;              // RT3D_BLOCKS_PER_SM (lane-group configs 4, 32, 3)
+    int want_per_sm_g1 = 0;           // RT3D_G1_BLOCKS_PER_SM (thread per pixel; 0: occupancy)
     int sharing = 1;                  // sessions running frames concurrently on the device
     int occ_apss = 1, occ_knn = 1, occ_fit = 1;  // co-resident blocks per SM
     int grid_apss = 0, grid_knn = 0, grid_fit = 0;
@@ -504,6 +506,15 @@ rt3d_status ensure_state(rt3d_session* s, size_t pcap, size_t npix) {
     CUDA_TRY(s->cb.ensure(npix * 8));
     s->pcap = std::max(s->pcap, pc);
     return RT3D_OK;
+}
+
+// lane-group configs of the stage kernels (lanes per pixel 4, 32, 3, 1)
+int cfg_index(int gsz) { return gsz == 4 ? 0 : gsz == 32 ? 1 : gsz == 3 ? 2 : 3; }
+
+// stage blocks per SM a frame's cooperative grid uses for lane-group config c
+int blocks_per_sm(const rt3d_session* s, int c) {
+    if (c == 3) return s->want_per_sm_g1 > 0 ? s->want_per_sm_g1 : s->per_sm_c[3];
+    return s->want_per_sm;
 }
 
 rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters) {
@@ -645,14 +656,20 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
             const uint64_t warps4 = (uint64_t)s->grid_frame_c[0] * kWarps;
             const uint64_t chunks4 = (npix + 7) / 8;
             F.cfg.gsz = (chunks4 > warps4 && !getenv("RT3D_G4")) ? 3 : 4;
+        } else if (mpp <= (uint32_t)kThreadPts && npix >= (1u << 16) &&
+                   !getenv("RT3D_WARP_PER_PIXEL")) {
+            // large dense arrays (D, E): a thread per pixel, no staging, more
+            // blocks per SM (sweep_node_thread)
+            F.cfg.gsz = 1;
         } else {
             F.cfg.gsz = 32;
         }
-        // test hook: force a lane-group config (3, 4 need <= 4 points per pixel)
+        // test hook: force a lane-group config (1, 3, 4 need <= 4 points per pixel)
         if (const char* gs = getenv("RT3D_GSZ")) {
             const int g = atoi(gs);
-            if (g == 32 || ((g == 3 || g == 4) && mpp <= 4)) F.cfg.gsz = g;
+            if (g == 32 || ((g == 1 || g == 3 || g == 4) && mpp <= 4)) F.cfg.gsz = g;
         }
+        if (F.cfg.gsz == 1) F.cfg.fused_iter = 0;  // ST_ITER is not built for G == 1
     }
     {
         // blocktree block nodes: the shallowest depth <= G whose nodes hold at
@@ -675,8 +692,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         F.tblk2[1] = F.tblk[0] + 3 * F.tb_nbn;
     }
     {
-        const int cfgi = F.cfg.gsz == 4 ? 0 : F.cfg.gsz == 32 ? 1 : 2;
-        if (std::min(s->per_sm_c[cfgi], s->want_per_sm) < s->sharing)
+        const int cfgi = cfg_index(F.cfg.gsz);
+        if (std::min(s->per_sm_c[cfgi], blocks_per_sm(s, cfgi)) < s->sharing)
             return fail(RT3D_ERR_UNSUPPORTED,
                         "rt3d: this frame's stage kernels do not fit %d sessions per device",
                         s->sharing);
@@ -688,15 +705,17 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     return RT3D_OK;
 }
 
-// lane-group configs of the stage kernels: lanes per pixel
-constexpr int kNumCfg = 3;
+// lane-group configs of the stage kernels: lanes per pixel 4, 32, 3, 1
+constexpr int kNumCfg = 4;
 // dynamic shared memory of the stage kernels per config
 static size_t stage_smem(int cfgi) {
-    return cfgi == 0 ? sizeof(SmemT<4>) : cfgi == 1 ? sizeof(SmemT<32>) : sizeof(SmemT<3>);
+    return cfgi == 0 ? sizeof(SmemT<4>) : cfgi == 1 ? sizeof(SmemT<32>)
+                     : cfgi == 2 ? sizeof(SmemT<3>) : sizeof(SmemT<1>);
 }
 // [config][stage]
 static StageFn stage_fn(int cfgi, int st) {
-    return cfgi == 0 ? stage_fn_g4(st) : cfgi == 1 ? stage_fn_g32(st) : stage_fn_g3(st);
+    return cfgi == 0 ? stage_fn_g4(st) : cfgi == 1 ? stage_fn_g32(st)
+                     : cfgi == 2 ? stage_fn_g3(st) : stage_fn_g1(st);
 }
 
 cudaEvent_t pool_event(rt3d_session* s) {
@@ -748,7 +767,7 @@ rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
                              s->stream));
     // the frame as a stream-ordered kernel sequence; every decision stays on
     // the device (Ctl), so nothing here waits for the GPU
-    const int cfgi = F.cfg.gsz == 4 ? 0 : F.cfg.gsz == 32 ? 1 : 2;
+    const int cfgi = cfg_index(F.cfg.gsz);
     static const int stage_cls[5] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
                                      RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL, RT3D_KC_ITER};
     auto stage = [&](int st, int it) -> rt3d_status {
@@ -964,8 +983,8 @@ static void set_frame_grids(rt3d_session* s) {
     s->grid_knn = s->nsm * s->occ_knn;
     s->grid_fit = s->nsm * s->occ_fit;
     s->grid_frame = 0;
-    for (int c = 0; c < 3; ++c) {
-        const int per = std::max(1, std::min(s->per_sm_c[c], s->want_per_sm) / std::max(1, s->sharing));
+    for (int c = 0; c < kNumCfg; ++c) {
+        const int per = std::max(1, std::min(s->per_sm_c[c], blocks_per_sm(s, c)) / std::max(1, s->sharing));
         s->grid_frame_c[c] = s->nsm * per;
         s->grid_frame = std::max(s->grid_frame, s->grid_frame_c[c]);
     }
@@ -1008,9 +1027,10 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     s->device = device;
     s->nsm = prop.multiProcessorCount;
     CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
-    int per_sm_c[kNumCfg] = {1 << 30, 1 << 30, 1 << 30};
+    int per_sm_c[kNumCfg] = {1 << 30, 1 << 30, 1 << 30, 1 << 30};
     for (int c = 0; c < kNumCfg; ++c)
         for (int st = 0; st < 5; ++st) {
+            if (!stage_fn(c, st)) continue;  // ST_ITER is not built for G == 1
             int b = 0;
             const size_t sz = stage_smem(c);
             CUDA_TRY(cudaFuncSetAttribute((const void*)stage_fn(c, st),
@@ -1019,7 +1039,7 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
                 &b, (const void*)stage_fn(c, st), kBlock, sz));
             per_sm_c[c] = std::min(per_sm_c[c], b);
         }
-    const int per_sm = std::min(std::min(per_sm_c[0], per_sm_c[1]), per_sm_c[2]);
+    const int per_sm = std::min(std::min(per_sm_c[0], per_sm_c[1]), std::min(per_sm_c[2], per_sm_c[3]));
     {
         int a = 0, k = 0;
         CUDA_TRY(cudaFuncSetAttribute(apss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1044,6 +1064,7 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     int want = env ? atoi(env) : 2;
     if (want < 1) want = 1;
     s->want_per_sm = want;
+    if (const char* e1 = getenv("RT3D_G1_BLOCKS_PER_SM")) s->want_per_sm_g1 = std::max(1, atoi(e1));
     for (int c = 0; c < kNumCfg; ++c) s->per_sm_c[c] = per_sm_c[c];
     set_frame_grids(s);
     int per_sm_fft = 0;

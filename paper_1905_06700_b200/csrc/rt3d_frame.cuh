@@ -207,10 +207,11 @@ struct Frame {
 // Staging capacities: lane groups of 4 (sparse frames, <= 4 points and ~12
 // events per pixel) stage 8 pixels per batch; a warp per pixel stages up to
 // 32.  The smaller footprint lets two 256-thread blocks share an SM.
+// (G == 1, thread per pixel, reads the CSR directly: no staging)
 template <int G>
 struct SweepDims {
-    static constexpr int EVC = G >= 32 ? 192 : 64;
-    static constexpr int PVC = G >= 32 ? 128 : 32;
+    static constexpr int EVC = G >= 32 ? 192 : G == 1 ? 1 : 64;
+    static constexpr int PVC = G >= 32 ? 128 : G == 1 ? 1 : 32;
 };
 template <int EVC, int PVC>
 struct WarpSweepSmT {
@@ -243,7 +244,9 @@ struct SmemT {
         } sw;
         double top[kTopMin];
         InitWarpSm init[kWarps];
-        alignas(16) unsigned char nbr[kWarps * kNbrWarpBytes];  // APSS / kNN phases of ST_ITER
+        // APSS / kNN phases of ST_ITER (not instantiated for G == 1, whose
+        // small footprint lets more blocks share an SM)
+        alignas(16) unsigned char nbr[G == 1 ? 16 : kWarps * kNbrWarpBytes];
     } u;
     double node[kWarps];
     double wmax[kWarps];
@@ -1029,6 +1032,213 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
 }
 
 // ---------------------------------------------------------------------------
+// Thread-per-pixel likelihood sweep (G == 1) for dense large arrays (configs
+// D/E: tens of events per pixel, <= kThreadPts points per pixel).  Each
+// thread runs one pixel exactly as the reference's per-pixel loop body does
+// (likelihood.hpp:100-333): events read straight from the CSR in order, the
+// rate of every event formed point by point in cloud order, the nll partial,
+// the background gradient and each point's gradient / curvature summed
+// sequentially in the reference's order, so every result is bit-identical to
+// the staged lane-group sweep (sweep_node) and to the reference.  Rates are
+// recomputed in the per-point loops instead of being stored: a few FP64
+// operations per support event against 8 B of HBM traffic per event.
+// ---------------------------------------------------------------------------
+constexpr int kThreadPts = 4;
+
+struct TpPoints {
+    double t[kThreadPts], r[kThreadPts], mig[kThreadPts];
+    int lo[kThreadPts], hi[kThreadPts];
+};
+
+// detail::active_rates (likelihood.hpp:111-119) at one event
+__device__ __forceinline__ double tp_rate(const IrfDev& f, double g, double b, int np,
+                                          const TpPoints& P, uint32_t bin) {
+    if (g == 0.0) return 0.0;
+    double l = g * b;
+#pragma unroll
+    for (int q = 0; q < kThreadPts; ++q)
+        if (q < np && (int)bin >= P.lo[q] && (int)bin <= P.hi[q])
+            l += g * P.r[q] * irf_value_fast(f, (double)bin - P.t[q]);
+    return l;
+}
+
+template <int KIND, class SM>
+__device__ __forceinline__ void sweep_node_thread(const Frame& F, SM& sm, const SweepCtx& X,
+                                                  uint32_t lo, uint32_t size, double& cmax,
+                                                  double* spart, double* spart2) {
+    const int lane = threadIdx.x & 31;
+    if ((uint32_t)lane >= size) return;
+    const uint32_t p = lo + (uint32_t)lane;
+    const uint32_t e0 = F.off[p], m = F.off[p + 1] - e0;
+    const uint32_t* bo = F.bo[X.sc];
+    const uint32_t n0 = bo[p];
+    const int np = (int)(bo[p + 1] - n0);
+    const bool dead = F.dead[p] != 0;
+    const double gain = F.gain[p];
+    const double g = dead ? 0.0 : gain;
+    double b;
+    if (KIND == K_CAND_B) {
+        double dir = F.gb[p];
+        if (F.cfg.step_auto[2]) dir = dir / (F.cb[p] + X.cfloor);
+        b = std_max(0.0, F.b[X.bc][p] - X.alpha * dir);
+        F.b[X.bc ^ 1][p] = b;
+    } else {
+        b = F.b[X.bc][p];
+        if (X.apply_floor) {
+            b = (b < kBackgroundFloor) ? kBackgroundFloor : b;
+            F.b[X.bc][p] = b;
+        }
+    }
+    const IrfDev& f = pixel_irf(F, sm, p);
+    const int T = F.bins;
+    const uint2* ev = F.ev + e0;
+    const int ncand = ((KIND == K_CAND_T || KIND == K_CAND_R) && X.two) ? 2 : 1;
+    for (int cand = 0; cand < ncand; ++cand) {
+        const double alpha = cand ? X.alpha2 : X.alpha;
+        (void)alpha;
+        TpPoints P;
+#pragma unroll
+        for (int k = 0; k < kThreadPts; ++k) {
+            P.t[k] = P.r[k] = P.mig[k] = 0.0;
+            P.lo[k] = 1;
+            P.hi[k] = 0;
+            if (k < np) {
+                const uint32_t n = n0 + (uint32_t)k;
+                double t = F.t[X.tc][n], r = F.r[X.rc][n];
+                if (KIND == K_CAND_T) {
+                    t = cand_t_value(F, X, n, t, alpha);
+                    if (!X.two) F.t[X.tc ^ 1][n] = t;
+                }
+                if (KIND == K_CAND_R) {
+                    r = cand_r_value(F, X, n, r, alpha);
+                    if (!X.two) F.r[X.rc ^ 1][n] = r;
+                }
+                int a, c;
+                irf_support(f, t, T, a, c);
+                constexpr bool kCompute = KIND == K_CAND_T || KIND == K_GRAD_R || KIND == K_NLL ||
+                                          KIND == K_GRAD_T;
+                double mg;
+                if (kCompute && !(KIND == K_GRAD_T && X.mig_cached)) {
+                    mg = mig_fast(f, t, a, c);
+                    if (KIND == K_GRAD_R) F.mig[X.sc][n] = mg;
+                } else {
+                    mg = F.mig[X.sc][n];
+                }
+                P.t[k] = t;
+                P.r[k] = r;
+                P.lo[k] = a;
+                P.hi[k] = c;
+                P.mig[k] = mg;
+            }
+        }
+        // events in order: rates, the nll partial (likelihood.hpp:141-165)
+        // and the background gradient / curvature (:256-277, :300-307)
+        double acc = 0.0, gbv = g * T, bs = 0.0;
+        bool inf = false;
+        if (!dead) {
+            double mass = T * b;
+            for (int q = 0; q < np && q < kThreadPts; ++q) mass += P.r[q] * P.mig[q];
+            acc = gain * mass;
+        }
+        for (uint32_t k = 0; k < m; ++k) {
+            const uint2 e = __ldg(&ev[k]);
+            const double l = tp_rate(f, g, b, np, P, e.x);
+            const double z = (double)e.y;
+            if (!dead && !inf) {
+                if (l <= 0.0) inf = true;
+                else acc -= (l > 0.0) ? z * log(l) : 0.0;
+            }
+            if (KIND == K_GRAD_B && l > 0.0) {
+                gbv -= g * z / l;
+                bs += g * g * z / (l * l);
+            }
+        }
+        const double part = dead ? 0.0 : (inf ? INFINITY : acc);
+        double* sp = cand ? spart2 : spart;
+        if (sp) sp[lane] = part;
+        else F.part[p] = part;
+        if (KIND == K_GRAD_B) {
+            const double gval = g != 0.0 ? gbv : 0.0;
+            const double bsv = g != 0.0 ? bs : 0.0;
+            F.gb[p] = gval;
+            F.cb[p] = bsv;
+            cmax = std_max(cmax, bsv);
+        }
+        if (KIND == K_GRAD_T || KIND == K_GRAD_R) {  // per point (likelihood.hpp:178-253)
+            const bool skip = (np == 0) || g == 0.0;
+            for (int k = 0; k < np && k < kThreadPts; ++k) {
+                const uint32_t n = n0 + (uint32_t)k;
+                double gval = 0.0, cv = 0.0;
+                uint8_t og = 0;
+                if (!skip) {
+                    double t = 0.0, r = 0.0, mgk = 0.0;
+                    int plo = 1, phi = 0;
+#pragma unroll
+                    for (int q = 0; q < kThreadPts; ++q)
+                        if (q == k) {
+                            t = P.t[q];
+                            r = P.r[q];
+                            mgk = P.mig[q];
+                            plo = P.lo[q];
+                            phi = P.hi[q];
+                        }
+                    uint32_t kk = m;
+                    if (plo <= phi) kk = first_event_ge(F.ev, e0, m, (uint32_t)plo);
+                    if (KIND == K_GRAD_T) {
+                        if (plo > phi) {
+                            og = 1;
+                        } else {
+                            const double grr = g * r;
+                            double a = neg_deriv_sum(f, t, plo, phi);
+                            for (; kk < m; ++kk) {
+                                const uint2 e = __ldg(&ev[kk]);
+                                if (e.x > (uint32_t)phi) break;
+                                const double l = tp_rate(f, g, b, np, P, e.x);
+                                const double dv = irf_deriv_fast(f, (double)e.x - t);
+                                if (l > 0.0) a += dv * (double)e.y / l;
+                                if (!(l <= 0.0)) {
+                                    const double zl2 = (double)e.y / (l * l);
+                                    const double dh = grr * dv;
+                                    cv += dh * dh * zl2;
+                                }
+                            }
+                            if (r != 0.0) gval = grr * a;
+                        }
+                    } else {
+                        double a = mgk;
+                        if (plo <= phi) {
+                            for (; kk < m; ++kk) {
+                                const uint2 e = __ldg(&ev[kk]);
+                                if (e.x > (uint32_t)phi) break;
+                                const double l = tp_rate(f, g, b, np, P, e.x);
+                                const double hv = irf_value_fast(f, (double)e.x - t);
+                                if (l > 0.0) a -= hv * (double)e.y / l;
+                                if (!(l <= 0.0)) {
+                                    const double zl2 = (double)e.y / (l * l);
+                                    const double h = g * hv;
+                                    cv += h * h * zl2;
+                                }
+                            }
+                        }
+                        gval = g * a;
+                    }
+                }
+                if (KIND == K_GRAD_T) {
+                    F.gt[n] = gval;
+                    F.ct[n] = cv;
+                    F.oog[n] = og;
+                    if (og && F.cfg.set_oog_flags) F.fl[X.sc][n] |= 2u;
+                } else {
+                    F.gr[n] = gval;
+                    F.cr[n] = cv;
+                }
+                cmax = std_max(cmax, cv);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Controller: runs on thread 0 of the last block after each grid reduction
 // ---------------------------------------------------------------------------
 // The controller state is replicated: every block runs the same decisions on
@@ -1381,8 +1591,12 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             for (uint32_t c = warp; c < nch; c += kWarps) {
                 const uint32_t lo = blo + c * NG;
                 const uint32_t size = blo + bsz - lo < NG ? blo + bsz - lo : NG;
-                sweep_node<KIND, G>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo),
-                                    two ? sm.bpart2 + (lo - blo) : nullptr);
+                if constexpr (G == 1)
+                    sweep_node_thread<KIND>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo),
+                                            two ? sm.bpart2 + (lo - blo) : nullptr);
+                else
+                    sweep_node<KIND, G>(F, sm, X, lo, size, cm, sm.bpart + (lo - blo),
+                                        two ? sm.bpart2 + (lo - blo) : nullptr);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cm = std_max(cm, __shfl_xor_sync(0xffffffffu, cm, o));
@@ -1431,7 +1645,10 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
             for (uint32_t c = gw; c < nchunks; c += nw) {
                 const uint32_t lo = c * NG;
                 const uint32_t size = F.npix - lo < NG ? F.npix - lo : NG;
-                sweep_node<KIND, G>(F, sm, X, lo, size, cmax);
+                if constexpr (G == 1)
+                    sweep_node_thread<KIND>(F, sm, X, lo, size, cmax, nullptr, nullptr);
+                else
+                    sweep_node<KIND, G>(F, sm, X, lo, size, cmax);
             }
         }
 #pragma unroll

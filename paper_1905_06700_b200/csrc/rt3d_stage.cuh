@@ -7,6 +7,10 @@
 #include "rt3d_frame.cuh"
 #include "rt3d_nbr.cuh"
 
+#ifndef RT3D_G1_MIN_BLOCKS
+#define RT3D_G1_MIN_BLOCKS 3
+#endif
+
 namespace rt3d {
 
 // grid barrier + optional phase stamp (leader thread, after the barrier)
@@ -102,15 +106,22 @@ __device__ int depth_block(const Frame& F, SmemT<G>& sm, int it, int tc, int rc,
     return tc;
 }
 
+// blocks per SM the register budget is sized for: 2 (128 registers) for the
+// lane-group sweeps, more for the thread-per-pixel sweeps of large arrays
+template <int G>
+struct StageOcc {
+    static constexpr int kBlocks = G == 1 ? RT3D_G1_MIN_BLOCKS : 2;
+};
+
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it);
+__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Frame F, int it);
 
 // One stage of a frame: a cooperative kernel whose phases are separated by
 // grid barriers.  Buffer toggles live in Ctl between kernels; every block
 // reads them at entry, the leader writes them back at exit (after at least
 // one barrier, so no block still reads them).
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, 2) stage_kernel(Frame F, int it) {
+__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Frame F, int it) {
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);
