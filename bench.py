@@ -196,12 +196,13 @@ def load_measured_peaks():
 B200_FP64_NOMINAL_TFLOPS = 37.0  # NVIDIA B200 datasheet (vector FP64); not measured here
 
 
-def apss_fp64(points, radius: float, us_per_launch: float):
+def apss_fp64(points, radius: float, us_per_launch: float, frames: int = 1):
     """The APSS kernel against the FP64 roof: ~70 flop per
     (point, neighbour) pair for distance, weight, mean, covariance and the
     Pratt moments, plus ~3000 flop per point for the 3x3 and 5x5 eigensolves.
     Neighbour counts come from the final cloud (ball of `radius`, self
-    included), so this is an estimate of one launch's flops."""
+    included) of the first frame, times the frames one launch processes, so
+    this is an estimate of one launch's flops."""
     try:
         from scipy.spatial import cKDTree
     except ImportError:
@@ -210,7 +211,7 @@ def apss_fp64(points, radius: float, us_per_launch: float):
         return None
     xyz = np.stack([points["x"], points["y"], points["z"]], axis=1)
     nbrs = cKDTree(xyz).query_ball_point(xyz, radius, return_length=True)
-    flops = 70.0 * float(np.sum(nbrs)) + 3000.0 * len(points)
+    flops = frames * (70.0 * float(np.sum(nbrs)) + 3000.0 * len(points))
     achieved = flops / (us_per_launch * 1e-6) / 1e12
     return {"achieved": achieved, "unit": "TFLOP/s", "peak": B200_FP64_NOMINAL_TFLOPS,
             "frac": achieved / B200_FP64_NOMINAL_TFLOPS, "flops_per_launch": flops,
@@ -334,6 +335,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--batch", type=int, default=8,
+                    help="frames per step (rt3d_reconstruct_batch), 1..8")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_init()
@@ -343,114 +346,120 @@ def main():
         return rc
 
     import torch
+    from paper_1905_06700_b200.abi import POINT_DTYPE
     from paper_1905_06700_b200.rt3d import Session
+    from scenegen.scene import simulate
 
     torch.cuda.set_device(local)
-    from scenegen.scene import simulate
     spec, seed, cfg, workload = config_b()
-    sc = simulate(spec, seed)
-    sess = Session(local)
-    sess.set_scene(sc)
+    NB = args.batch
+    # a stream of NB frames of the scene (photon noise seeds seed .. seed+NB-1)
+    cubes = [simulate(spec, seed + k) for k in range(NB)]
+    sc = cubes[0]
+    sessions = [Session(local) for _ in range(NB)]
+    for s, c in zip(sessions, cubes):
+        s.set_scene(c)
+    sess = sessions[0]
     stream = torch.cuda.ExternalStream(sess.stream_ptr, device=torch.device("cuda", local))
     flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
 
-    # warm-up (module load, buffers)
+    def run_batch():
+        Session.reconstruct_batch_async(sessions, cfg)
+
+    # warm-up (module load, buffers, CUDA graphs)
     for _ in range(args.warmup):
+        run_batch()
         sess.reconstruct_async(cfg)
     sess.synchronize()
-    rep = sess.report()
+
+    def timed(fn, K):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
+        with torch.cuda.stream(stream):
+            for k in range(K):
+                flush.zero_()  # evict the working set from L2 between steps
+                evs[k][0].record(stream)
+                fn()
+                evs[k][1].record(stream)
+        stream.synchronize()
+        return [x.elapsed_time(y) for x, y in evs]
 
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
         t_wall0 = time.perf_counter()
-        with torch.cuda.stream(stream):
-            for k in range(K):
-                flush.zero_()  # evict the frame's working set from L2 between frames
-                ev[k][0].record(stream)
-                sess.reconstruct_async(cfg)
-                ev[k][1].record(stream)
-        stream.synchronize()
+        step_ms = timed(run_batch, K)           # one step = one batch of NB frames
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     barrier(world)
-    frame_ms = [a.elapsed_time(b) for a, b in ev]
-    # second timed pass for the per-kernel breakdown: CUDA events around every
-    # launch on the session stream (the value pass replays each frame as one
-    # CUDA graph, inside which events cannot time kernels)
+    # single-frame latency (one frame per launch sequence), reported alongside
+    single_ms = timed(lambda: sess.reconstruct_async(cfg), K)
+    # per-kernel breakdown: CUDA events around every launch of a batch on the
+    # launching stream (the value pass replays each batch as one CUDA graph,
+    # inside which events cannot time kernels)
     sess.time_kernels(True)
     torch.cuda.synchronize()
-    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
-    with torch.cuda.stream(stream):
-        for k in range(K):
-            flush.zero_()
-            ev2[k][0].record(stream)
-            sess.reconstruct_async(cfg)
-            ev2[k][1].record(stream)
-    stream.synchronize()
+    timed_ms = timed(run_batch, K)
     ktimes = sess.kernel_times()
     sess.time_kernels(False)
-    timed_ms = [a.elapsed_time(b) for a, b in ev2]
-    dev_s = sum(frame_ms) / 1e3
+    dev_s = sum(step_ms) / 1e3
     dev_s_max = barrier_max(dev_s, world, local)
-    value = world * K / dev_s_max
+    value = world * K * NB / dev_s_max
     rep = sess.report()
     pts, _ = sess.state()
 
-    # e2e through the C ABI from pinned host buffers
-    n_e2e = args.e2e_steps or max(2 * K, 40)
-    pin_off = torch.empty(len(sc.offsets), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
-    pin_ev = torch.empty(len(sc.events) * 2, dtype=torch.int32, pin_memory=True).numpy().view(sc.events.dtype)
-    pin_off[:] = sc.offsets
-    pin_ev[:] = sc.events
-    from paper_1905_06700_b200.abi import POINT_DTYPE
+    # e2e through the public API from pinned host buffers: every step uploads
+    # its NB cubes (rt3d_set_cube), reconstructs them as one batch
+    # (rt3d_reconstruct_batch) and downloads every cloud and background
+    # (rt3d_state_copy), all inside the timed region
     import copy
-    sc_pin = copy.copy(sc)
-    sc_pin.offsets, sc_pin.events = pin_off, pin_ev
-    out_pts = torch.empty(len(pts) * 64 + 64 * 1024, dtype=torch.uint8, pin_memory=True).numpy()
-    # end to end through the public streaming API: two sessions (two
-    # streams, each sized to half the device with set_sharing(2)) take
-    # alternate frames, each with up to two frames in flight
-    # (rt3d_frame_submit / rt3d_frame_collect), so one frame's copies and
-    # kernels overlap the others'.  Every frame does its own H2D of the cube
-    # and D2H of its cloud + background.
+    n_e2e = args.e2e_steps or max(K // 2, 5)
+    pinned = []
+    for c in cubes:
+        cp = copy.copy(c)
+        off = torch.empty(len(c.offsets), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        ev = torch.empty(len(c.events) * 2, dtype=torch.int32,
+                         pin_memory=True).numpy().view(c.events.dtype)
+        off[:] = c.offsets
+        ev[:] = c.events
+        cp.offsets, cp.events = off, ev
+        pinned.append(cp)
     P_cap = cfg.init_max_returns * spec.superres * spec.superres * sc.n_pixels
-    ring = [Session(local), Session(local)]
-    for r in ring:
-        r.set_scene(sc)
-        r.set_sharing(2)
     outs = [(torch.empty(P_cap * 64, dtype=torch.uint8, pin_memory=True).numpy().view(POINT_DTYPE),
              torch.empty(sc.n_pixels, dtype=torch.float64, pin_memory=True).numpy())
-            for _ in range(4)]
-    for r in ring:                          # warm both slots of both sessions (buffers, graphs)
-        for w in range(2):
-            tk = r.frame_submit(sc_pin, cfg)
-            r.frame_collect(tk, *outs[w])
+            for _ in range(NB)]
+    import ctypes as C
+    from paper_1905_06700_b200 import rt3d as R
+
+    def e2e_step():
+        d2h = 0
+        for s, c in zip(sessions, pinned):
+            s.set_cube(c)
+        Session.reconstruct_batch_async(sessions, cfg)
+        for s, (op, ob) in zip(sessions, outs):
+            n = R._u64()
+            R._check(R.lib().rt3d_state_size(s.h, C.byref(n)))
+            R._check(R.lib().rt3d_state_copy(s.h, R.ptr(op, R.Point), R.ptr(ob, R._dbl)))
+            d2h += n.value * 64 + ob.nbytes
+        return d2h
+
+    e2e_step()
     barrier(world)
     t0 = time.perf_counter()
-    d2h = 0
-    pend = []
-    for k in range(n_e2e):
-        if len(pend) == 4:
-            ps, pt, po = pend.pop(0)
-            p_e2e, bg_e2e, _ = ps.frame_collect(pt, *outs[po])
-            d2h = p_e2e.nbytes + bg_e2e.nbytes
-        cur = ring[k % 2]
-        pend.append((cur, cur.frame_submit(sc_pin, cfg), k % 4))
-    for ps, pt, po in pend:
-        p_e2e, bg_e2e, _ = ps.frame_collect(pt, *outs[po])
-        d2h = p_e2e.nbytes + bg_e2e.nbytes
+    for _ in range(n_e2e):
+        d2h = e2e_step()
     e2e_s = time.perf_counter() - t0
     e2e_s = barrier_max(e2e_s, world, local)
-    e2e_fps = world * n_e2e / e2e_s
-    h2d = sc.offsets.nbytes + sc.events.nbytes
+    e2e_fps = world * n_e2e * NB / e2e_s
+    h2d = sum(c.offsets.nbytes + c.events.nbytes for c in cubes)
 
     peak, peak_src = load_measured_peaks()
-    cb = class_bytes(sc, rep, fused_depth=ktimes["stage_depth"][1] == 0)
+    # algorithmic bytes of one batch: every frame's own report
+    cb = dict.fromkeys(KERNEL_NAMES, 0.0)
+    for s, c in zip(sessions, cubes):
+        for k, v in class_bytes(c, s.report(), fused_depth=ktimes["stage_depth"][1] == 0).items():
+            cb[k] += v
     if ktimes["iteration"][1] > 0:  # one launch per iteration: its classes merge
         for c in ("apss", "apss_fit", "stage_intensity", "knn", "stage_tail"):
             cb["iteration"] += cb[c]
@@ -459,7 +468,7 @@ def main():
     classes = {}
     for cls, (ms, n) in ktimes.items():
         per_launch_bytes = cb[cls] * K / n if n else 0.0
-        classes[cls] = {"ms_per_frame": ms / K, "launches_per_frame": n / K,
+        classes[cls] = {"ms_per_frame": ms / (K * NB), "launches_per_batch": n / K,
                         "us_per_launch": 1e3 * ms / n if n else None,
                         "algorithmic_bytes_per_launch": per_launch_bytes,
                         "gbs": per_launch_bytes / (ms / n) / 1e6 if n and ms else None}
@@ -487,33 +496,38 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": shared_config(spec, cfg, len(sc.events)),
             "details": {
+                "frames_per_step": NB,
+                "step": f"one batch of {NB} frames (photon-noise seeds {seed}..{seed + NB - 1}) "
+                        "through rt3d_reconstruct_batch: one launch sequence, a frame axis "
+                        "in every kernel's grid, each frame with its own controller",
                 "points_init": int(rep["steps"][0]["points_before"]) if len(rep["steps"]) else 0,
                 "points_final": int(rep["points"]), "parallelism": f"frames x{world} (replicas)",
                 "vs_baseline_ref": "paper GPU 13 ms/frame on Titan Xp (BASELINE.md)",
-                "ms_per_frame_p50": statistics.median(frame_ms),
-                "ms_per_frame_min": min(frame_ms),
-                "ms_per_frame_direct_launch": sum(timed_ms) / K,
-                "frame_launch": "one CUDA graph per frame (captured once, replayed)",
+                "ms_per_step_p50": statistics.median(step_ms),
+                "ms_per_step_direct_launch": sum(timed_ms) / K,
+                "single_frame_latency_ms_p50": statistics.median(single_ms),
+                "single_frame_latency_ms_min": min(single_ms),
+                "single_frame_fps": 1e3 * K / sum(single_ms),
+                "frame_launch": "one CUDA graph per batch (captured once, replayed)",
             },
             "e2e": {"value": e2e_fps, "unit": "frames/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "mode": "public streaming API (rt3d_frame_submit / rt3d_frame_collect), "
-                            "pinned cube in, cloud + background out; two sessions sized to half "
-                            "the device each (rt3d_session_set_sharing) take alternate frames, "
-                            "up to four frames in flight"},
+                    "mode": f"public API per step: rt3d_set_cube x{NB} from pinned host cubes, "
+                            f"rt3d_reconstruct_batch, rt3d_state_copy x{NB} (cloud + background) "
+                            "into pinned host buffers; wall clock, no overlap between steps"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic_per_launch(dom),
                          "kernel": KERNEL_NAMES[dom],
-                         "share_of_frame": dc["ms_per_frame"] / (sum(timed_ms) / K),
+                         "share_of_step": dc["ms_per_frame"] * NB / (sum(timed_ms) / K),
                          "us_per_launch": dc["us_per_launch"],
                          "algorithmic_bytes_per_launch": dc["algorithmic_bytes_per_launch"],
                          "peak_source": peak_src,
-                         "timing": "CUDA events on the session stream around every launch, "
-                                   "summed over a second timed pass of K frames launched "
-                                   "directly (the value pass replays each frame as a CUDA "
+                         "timing": "CUDA events on the launching stream around every launch, "
+                                   "summed over a second timed pass of K batches launched "
+                                   "directly (the value pass replays each batch as a CUDA "
                                    "graph)"},
             "frame_roofline": {"achieved": fb / (dev_s / K) / 1e9, "unit": "GB/s",
-                               "algorithmic_bytes_per_frame": fb},
+                               "algorithmic_bytes_per_step": fb},
             "kernel_classes": classes,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
@@ -524,13 +538,12 @@ def main():
         if parity:
             line["parity"] = parity
         if dom == "apss":
-            fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"])
+            fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"], NB)
             if fp:
                 line["roofline"]["fp64"] = fp
         print(json.dumps(line), flush=True)
-    sess.close()
-    for r in ring:
-        r.close()
+    for s in sessions:
+        s.close()
     barrier(world)
     if world > 1:
         import torch.distributed as dist

@@ -245,6 +245,14 @@ rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_by
  * session stream (returns before the frame finishes). */
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg);
 rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
+/* A batch of frames: reconstruct (reconstruct.hpp:457-489) on each of the n
+ * (<= 8) sessions' resident cubes, all in one launch sequence on sessions[0]'s
+ * stream (a frame axis in every kernel's grid; video streams).
+ * Sessions share the device and the configuration; each session's report and
+ * state then read exactly as after rt3d_reconstruct on that session.
+ * RT3D_ERR_UNSUPPORTED when the cubes need different sweep layouts. */
+rt3d_status rt3d_reconstruct_batch(rt3d_session* const* sessions, int32_t n,
+                                   const rt3d_recon_config* cfg);
 
 /* Pipelined frames (a video stream through one session):
  * rt3d_frame_submit validates `cube`, copies it (pinned host memory avoids a
@@ -254,8 +262,9 @@ rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
  * ticket.  rt3d_frame_collect waits for that frame and copies its cloud,
  * background and report out; *n_points receives the count.  A cloud of more
  * than cap points returns RT3D_ERR_OUT_OF_RANGE and copies nothing: the frame
- * stays in flight and can be collected again with a larger buffer.  At most two frames are in flight; `cube` must stay valid until its
- * frame is collected. */
+ * stays in flight and can be collected again with a larger buffer.  At most
+ * two frames are in flight; `cube` must stay valid until its frame is
+ * collected. */
 rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* cube, const rt3d_recon_config* cfg,
                               uint64_t* ticket);
 rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* points, uint64_t cap,

@@ -40,7 +40,10 @@ StageFn stage_fn_g32(int st);
 StageFn stage_fn_g3(int st);
 StageFn stage_fn_g1(int st);
 
-__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
+#define BATCH_FRAME(FB) (FB).f[(FB).n == 1 ? 0u : blockIdx.x / (FB).bpf]
+
+__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
@@ -48,13 +51,15 @@ __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(Frame F) {
                       ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
 }
 
-__global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(Frame F) {
+__global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS_FIT);
     apss_fit_threads(F, ld_cg(&F.ctl->P), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
 }
 
-__global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(Frame F) {
+__global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
@@ -446,6 +451,7 @@ struct rt3d_session {
     int iterations = 0;
     int report_iters_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t xev = nullptr;  // cross-stream ordering of batched frames
     unsigned long long* h_dbg = nullptr;  // RT3D_DEBUG records (pinned copy)
     unsigned long long* d_dbg = nullptr;
     cudaStream_t side = nullptr;
@@ -463,7 +469,8 @@ struct rt3d_session {
     // frame (its Frame bytes: buffers, config, toggles) and timing mode match
     struct GraphCache {
         bool valid = false;
-        Frame F;
+        int n = 0;  // frames of the batch
+        Frame F[kMaxBatch];
         cudaGraphExec_t exec = nullptr;
         uint64_t used = 0;
     } gc[4];  // pipelined frames alternate two cube slots: two live graphs
@@ -761,20 +768,46 @@ rt3d_status timed_launch(rt3d_session* s, int cls, Fn&& fn) {
     return st;
 }
 
-rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
-    CUDA_TRY(cudaMemsetAsync(F.ctl, 0, sizeof(Ctl), s->stream));
-    CUDA_TRY(cudaMemsetAsync(F.diag, 0, sizeof(StepDiagDev) * std::max(F.cfg.max_iters, 1),
-                             s->stream));
-    // the frame as a stream-ordered kernel sequence; every decision stays on
-    // the device (Ctl), so nothing here waits for the GPU
+// The batch of frames as one parameter block per kernel: frame k takes blocks
+// [k bpf, (k+1) bpf) of the launch and its own barrier counters
+static void make_batch(FrameBatch& FB, const Frame* Fs, int n, uint32_t bpf) {
+    FB.n = (uint32_t)n;
+    FB.bpf = bpf;
+    for (int k = 0; k < n; ++k) {
+        FB.f[k] = Fs[k];
+        FB.f[k].blk0 = (uint32_t)k * bpf;
+        FB.f[k].nblk = bpf;
+        FB.f[k].barc = Fs[k].ctl;
+        FB.f[k].bar_n = bpf;
+        FB.f[k].bar_b0 = (uint32_t)k * bpf;
+    }
+}
+
+// the frames as a stream-ordered kernel sequence on s's stream; every
+// decision stays on the device (each frame's Ctl), so nothing here waits for
+// the GPU.  The frames of a batch share every launch (same configuration).
+rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n) {
+    const Frame& F = Fs[0];
+    for (int k = 0; k < n; ++k) {
+        CUDA_TRY(cudaMemsetAsync(Fs[k].ctl, 0, sizeof(Ctl), s->stream));
+        CUDA_TRY(cudaMemsetAsync(Fs[k].diag, 0,
+                                 sizeof(StepDiagDev) * std::max(Fs[k].cfg.max_iters, 1), s->stream));
+    }
     const int cfgi = cfg_index(F.cfg.gsz);
     static const int stage_cls[5] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
                                      RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL, RT3D_KC_ITER};
+    // cooperative stage grids: the co-resident blocks split among the frames
+    const uint32_t sbpf = (uint32_t)std::max(1, s->grid_frame_c[cfgi] / n);
+    static thread_local FrameBatch fb_stage, fb_apss, fb_fit, fb_knn;
+    make_batch(fb_stage, Fs, n, sbpf);
+    make_batch(fb_apss, Fs, n, (uint32_t)s->grid_apss);
+    make_batch(fb_fit, Fs, n, (uint32_t)s->grid_fit);
+    make_batch(fb_knn, Fs, n, (uint32_t)s->grid_knn);
     auto stage = [&](int st, int it) -> rt3d_status {
         return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
-            void* args[] = {&F, &it};
+            void* args[] = {&fb_stage, &it};
             CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st),
-                                                 dim3(s->grid_frame_c[cfgi]), dim3(kBlock), args,
+                                                 dim3(sbpf * (uint32_t)n), dim3(kBlock), args,
                                                  stage_smem(cfgi), s->stream));
             return RT3D_OK;
         });
@@ -790,20 +823,22 @@ rt3d_status launch_frame_direct(rt3d_session* s, Frame& F) {
             }
             if (!F.cfg.fuse_depth && (st = stage(ST_DEPTH, it))) return st;
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
-                apss_kernel<<<s->grid_apss, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps, s->stream>>>(F);
+                apss_kernel<<<s->grid_apss * n, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps,
+                              s->stream>>>(fb_apss);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
             if (st) return st;
             st = timed_launch(s, RT3D_KC_APSS_FIT, [&]() -> rt3d_status {
-                apss_fit_kernel<<<s->grid_fit, kFitBlock, 0, s->stream>>>(F);
+                apss_fit_kernel<<<s->grid_fit * n, kFitBlock, 0, s->stream>>>(fb_fit);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
             if (st) return st;
             if ((st = stage(ST_INTENSITY, it))) return st;
             st = timed_launch(s, RT3D_KC_KNN, [&]() -> rt3d_status {
-                knn_kernel<<<s->grid_knn, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps, s->stream>>>(F);
+                knn_kernel<<<s->grid_knn * n, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
+                             s->stream>>>(fb_knn);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
@@ -825,19 +860,19 @@ static void graph_cache_drop(rt3d_session* s, int k) {
 
 // A frame is ~150 launches; replaying them as a CUDA graph removes the
 // per-launch host cost and most of the inter-kernel gaps.  Graphs are cached
-// by the Frame bytes (buffers, configuration, toggles), least recently used
-// out.  Kernel timing (CUDA events around every launch) and the in-kernel
-// profiler launch directly; so does RT3D_NO_GRAPH=1.
-rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
-    // no host staging: back-to-back async launches must not race on it
-    F.P0 = P_init;
-    F.prof_cap = F.prof ? (uint32_t)(s->prof.cap / 16) : 0u;
+// by the Frame bytes of the batch (buffers, configuration, toggles), least
+// recently used out.  Kernel timing (CUDA events around every launch) and the
+// in-kernel profiler launch directly; so does RT3D_NO_GRAPH=1.
+rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n) {
+    for (int k = 0; k < n; ++k) Fs[k].prof_cap = Fs[k].prof ? (uint32_t)(s->prof.cap / 16) : 0u;
     static const bool no_graph = getenv("RT3D_NO_GRAPH") != nullptr;
-    if (no_graph || F.prof || s->time_kernels) return launch_frame_direct(s, F);
+    if (no_graph || Fs[0].prof || s->time_kernels) return launch_frames_direct(s, Fs, n);
     const int nc = (int)(sizeof(s->gc) / sizeof(s->gc[0]));
     int hit = -1, victim = 0;
     for (int k = 0; k < nc; ++k) {
-        if (s->gc[k].valid && std::memcmp(&s->gc[k].F, &F, sizeof F) == 0) hit = k;
+        if (s->gc[k].valid && s->gc[k].n == n &&
+            std::memcmp(s->gc[k].F, Fs, sizeof(Frame) * (size_t)n) == 0)
+            hit = k;
         if (!s->gc[k].valid || (s->gc[victim].valid && s->gc[k].used < s->gc[victim].used)) victim = k;
     }
     if (hit < 0) {
@@ -845,7 +880,7 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
         graph_cache_drop(s, hit);
         auto& g = s->gc[hit];
         CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
-        const rt3d_status st = launch_frame_direct(s, F);
+        const rt3d_status st = launch_frames_direct(s, Fs, n);
         cudaGraph_t graph = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(s->stream, &graph);
         if (st) {
@@ -856,12 +891,19 @@ rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
         const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
         cudaGraphDestroy(graph);
         if (ie != cudaSuccess) return fail(RT3D_ERR_CUDA, "CUDA: graph instantiate: %s", cudaGetErrorString(ie));
-        g.F = F;
+        std::memcpy(g.F, Fs, sizeof(Frame) * (size_t)n);
+        g.n = n;
         g.valid = true;
     }
     s->gc[hit].used = ++s->gc_clock;
     CUDA_TRY(cudaGraphLaunch(s->gc[hit].exec, s->stream));
     return RT3D_OK;
+}
+
+rt3d_status launch_frame(rt3d_session* s, Frame& F, uint32_t P_init) {
+    // no host staging: back-to-back async launches must not race on it
+    F.P0 = P_init;
+    return launch_frames(s, &F, 1);
 }
 
 rt3d_status read_ctl(rt3d_session* s) {
@@ -1080,6 +1122,7 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     }
     CUDA_TRY(cudaEventCreate(&s->ev0));
     CUDA_TRY(cudaEventCreate(&s->ev1));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->xev, cudaEventDisableTiming));
     *out = s;
     return RT3D_OK;
 }
@@ -1110,6 +1153,7 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     if (s->side) cudaStreamDestroy(s->side);
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
+    if (s->xev) cudaEventDestroy(s->xev);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;  // DevBuf members free their device memory
     return RT3D_OK;
@@ -1403,7 +1447,10 @@ rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_by
     return RT3D_OK;
 }
 
-static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program) {
+// validation, buffers and the Frame of an init-like program (reconstruct,
+// init, baseline) on s's resident sensor and cube
+static rt3d_status prepare_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program,
+                                     Frame& F) {
     rt3d_status st = require_device(s);
     if (st) return st;
     if ((st = validate_cfg(cfg))) return st;
@@ -1421,17 +1468,28 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     g.set_oog_flags = 1;
     s->max_pts_per_pixel = program == PROG_BASELINE ? 1u : (uint32_t)cfg->init.max_returns * s->s * s->s;
     s->tc = s->rc = s->bc = s->sc = 0;
-    Frame F;
     if ((st = build_frame(s, F, g, program == PROG_RECON ? cfg->max_iters : 1))) return st;
-    CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
-    if ((st = launch_frame(s, F, 0))) return st;
-    CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+    F.P0 = 0;
+    return RT3D_OK;
+}
+
+static void finish_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program) {
     s->have_state = true;
     s->baseline_state = program == PROG_BASELINE;
     s->state_pinned = true;
     s->perm.clear();
     s->iterations = -1;  // resolved lazily (report / state queries)
     s->report_iters_cap = program == PROG_RECON ? cfg->max_iters : 0;
+}
+
+static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program) {
+    Frame F;
+    rt3d_status st = prepare_init_like(s, cfg, program, F);
+    if (st) return st;
+    CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+    if ((st = launch_frames(s, &F, 1))) return st;
+    CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+    finish_init_like(s, cfg, program);
     return RT3D_OK;
 }
 
@@ -1452,6 +1510,46 @@ static rt3d_status resolve_state(rt3d_session* s) {
 
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
     return run_init_like(s, cfg, PROG_RECON);
+}
+
+// n frames (one per session, each on its own resident cube) in one launch
+// sequence on the first session's stream: every stage / neighbour kernel of
+// the batch is one launch whose blocks split among the frames (FrameBatch),
+// each frame with its own controller and grid barrier.  The sessions'
+// streams are ordered before and after the batch, so their results read as
+// after rt3d_reconstruct.
+rt3d_status rt3d_reconstruct_batch(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
+    if (!ss || n < 1 || n > kMaxBatch)
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: batch of 1..%d sessions", kMaxBatch);
+    for (int k = 0; k < n; ++k) {
+        if (!ss[k]) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session in batch");
+        if (ss[k]->device != ss[0]->device)
+            return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: batched sessions must share a device");
+        for (int j = 0; j < k; ++j)
+            if (ss[j] == ss[k]) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: session twice in a batch");
+    }
+    rt3d_session* s0 = ss[0];
+    static thread_local Frame Fs[kMaxBatch];
+    rt3d_status st;
+    for (int k = 0; k < n; ++k)
+        if ((st = prepare_init_like(ss[k], cfg, PROG_RECON, Fs[k]))) return st;
+    for (int k = 1; k < n; ++k)
+        if (std::memcmp(&Fs[k].cfg, &Fs[0].cfg, sizeof(Cfg)) != 0)
+            return fail(RT3D_ERR_UNSUPPORTED,
+                        "rt3d: batched frames need the same sweep layout (similar cubes)");
+    for (int k = 1; k < n; ++k) {  // s0's stream after each session's uploads
+        CUDA_TRY(cudaEventRecord(ss[k]->xev, ss[k]->stream));
+        CUDA_TRY(cudaStreamWaitEvent(s0->stream, ss[k]->xev, 0));
+    }
+    for (int k = 0; k < n; ++k) CUDA_TRY(cudaEventRecord(ss[k]->ev0, s0->stream));
+    if ((st = launch_frames(s0, Fs, n))) return st;
+    CUDA_TRY(cudaEventRecord(s0->xev, s0->stream));
+    for (int k = 0; k < n; ++k) {
+        CUDA_TRY(cudaEventRecord(ss[k]->ev1, s0->stream));
+        if (k) CUDA_TRY(cudaStreamWaitEvent(ss[k]->stream, s0->xev, 0));
+        finish_init_like(ss[k], cfg, PROG_RECON);
+    }
+    return RT3D_OK;
 }
 
 static rt3d_status pipeline_init(rt3d_session* s) {

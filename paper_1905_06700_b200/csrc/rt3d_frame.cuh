@@ -191,6 +191,11 @@ struct Frame {
     uint32_t amom_stride;
     double* fft_re;   // 2*npix complex scratch (fft background mode)
     double* fft_im;
+    // launch geometry: this frame's blocks are blk0 .. blk0 + nblk - 1 of the
+    // launch (a batch of frames shares one launch, FrameBatch); the grid
+    // barrier counts bar_n blocks on barc's counters, led by block bar_b0
+    uint32_t blk0, nblk, bar_n, bar_b0;
+    Ctl* barc;
     // control / report
     unsigned long long* prof;  // optional (id, %globaltimer) pairs after each barrier
     volatile unsigned long long* dbg;  // mapped host memory: progress / fault records
@@ -199,6 +204,19 @@ struct Frame {
     double* trace;
     Cfg cfg;
 };
+
+// frames of one launch (a batch shares each stage / neighbour kernel): block
+// b serves frame b / bpf; kernels take the batch as a __grid_constant__
+// parameter and keep a reference to their frame
+constexpr int kMaxBatch = 8;
+struct FrameBatch {
+    uint32_t n, bpf;
+    Frame f[kMaxBatch];
+};
+
+// this block's index / the block count within its frame
+__device__ __forceinline__ uint32_t vblock(const Frame& F) { return blockIdx.x - F.blk0; }
+__device__ __forceinline__ uint32_t vgrid(const Frame& F) { return F.nblk; }
 
 // Likelihood sweep staging: a warp owns a tree node of <= 32 consecutive
 // pixels; their events and points are contiguous CSR ranges, copied into
@@ -369,10 +387,10 @@ __device__ __forceinline__ double mf_response(const uint2* ev, uint32_t e0, uint
 template <class SM>
 __device__ void phase_init_peaks(const Frame& F, SM& sm) {
     const int lane = threadIdx.x & 31;
-    const uint32_t nwarps = gridDim.x * kWarps;
+    const uint32_t nwarps = vgrid(F) * kWarps;
     const int K = F.cfg.K, sep = F.cfg.sep, T = F.bins;
     const double thr = F.cfg.thr;
-    for (uint32_t p = blockIdx.x * kWarps + (threadIdx.x >> 5); p < F.npix; p += nwarps) {
+    for (uint32_t p = vblock(F) * kWarps + (threadIdx.x >> 5); p < F.npix; p += nwarps) {
         const double g = F.dead[p] ? 0.0 : F.gain[p];
         const uint32_t e0 = F.off[p], e1 = F.off[p + 1], m = e1 - e0;
         if (g == 0.0 || m == 0) {
@@ -557,9 +575,9 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
 // chunked grid scan: stage A writes per-pixel block-local prefixes, stage B
 // adds the block base (after a grid barrier)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void chunk_range(uint32_t n, uint32_t& c0, uint32_t& c1) {
-    uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
-    c0 = blockIdx.x * chunk;
+__device__ __forceinline__ void chunk_range(const Frame& F, uint32_t n, uint32_t& c0, uint32_t& c1) {
+    uint32_t chunk = (n + vgrid(F) - 1) / vgrid(F);
+    c0 = vblock(F) * chunk;
     c1 = c0 + chunk;
     if (c0 > n) c0 = n;
     if (c1 > n) c1 = n;
@@ -568,7 +586,7 @@ __device__ __forceinline__ void chunk_range(uint32_t n, uint32_t& c0, uint32_t& 
 template <class SM, typename CountFn>
 __device__ void scan_stage_a(const Frame& F, SM& sm, CountFn count) {
     uint32_t c0, c1;
-    chunk_range(F.npix, c0, c1);
+    chunk_range(F, F.npix, c0, c1);
     unsigned int carry = 0;
     for (uint32_t base = c0; base < c1; base += kBlock) {
         uint32_t p = base + threadIdx.x;
@@ -577,19 +595,19 @@ __device__ void scan_stage_a(const Frame& F, SM& sm, CountFn count) {
         if (p < c1) F.cnt[p] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) F.btot[blockIdx.x] = carry;
+    if (threadIdx.x == 0) F.btot[vblock(F)] = carry;
 }
 
 // returns this block's base; thread 0 of the last block publishes the total
 template <class SM>
 __device__ unsigned int scan_stage_b_base(const Frame& F, SM& sm, unsigned int* total_out) {
     unsigned int part = 0;
-    for (uint32_t b = threadIdx.x; b < blockIdx.x; b += kBlock) part += ld_cg(&F.btot[b]);
+    for (uint32_t b = threadIdx.x; b < vblock(F); b += kBlock) part += ld_cg(&F.btot[b]);
     unsigned int tot;
     unsigned int ex = block_exclusive_scan(part, sm, tot);
     (void)ex;
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0)
-        *total_out = tot + ld_cg(&F.btot[blockIdx.x]);
+    if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0)
+        *total_out = tot + ld_cg(&F.btot[vblock(F)]);
     return tot;
 }
 
@@ -607,7 +625,7 @@ __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
     unsigned int total = 0;
     unsigned int base = scan_stage_b_base(F, sm, &total);
     uint32_t c0, c1;
-    chunk_range(F.npix, c0, c1);
+    chunk_range(F, F.npix, c0, c1);
     const int s = F.s, K = F.cfg.K;
     for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
         uint32_t o = base + ld_cg(&F.cnt[p]);
@@ -642,7 +660,7 @@ __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
                 }
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0) {
         F.bo[0][F.npix] = total;
         F.ctl->P = total;
     }
@@ -900,7 +918,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
     const int gl = lane % G, grp = lane / G;
     constexpr int NG = 32 / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-    const bool w0t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool w0t0 = vblock(F) == 0 && threadIdx.x == 0;
     SWEEP_STAMP(w0t0, 110);
     // ---- meta, lane per pixel
     if ((uint32_t)lane < size) {
@@ -1351,8 +1369,8 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
         // one word: block 0 adds 2^31 - (n - 1), the others 1, so the top bit
         // flips exactly when the last block arrives and the low bits return
         // to where they were
-        Ctl* c = F.ctl;
-        const unsigned int inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1u) : 1u;
+        Ctl* c = F.barc;
+        const unsigned int inc = blockIdx.x == F.bar_b0 ? 0x80000000u - (F.bar_n - 1u) : 1u;
         __threadfence();
         const unsigned int old = atomicAdd(&c->bar_count, inc);
         const unsigned long long t0 = globaltimer();
@@ -1369,6 +1387,7 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
                 if (globaltimer() - t0 > kBarrierTimeoutNs) {
                     if (atomicExch(&c->abort, 1u) == 0u) {
                         c->abort_block = blockIdx.x;
+                        if (F.ctl != c) atomicExch(&F.ctl->abort, 1u);
                         c->abort_op = op;
                         c->abort_it = it;
                         c->abort_count = ld_volatile(&c->bar_count);
@@ -1566,10 +1585,10 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
                              int op, int it) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t NG = 32 / G;
-    const bool b0t0 = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool b0t0 = vblock(F) == 0 && threadIdx.x == 0;
     SWEEP_STAMP(b0t0, 100);
     if (threadIdx.x == 0 && F.dbg)
-        F.dbg[64 + blockIdx.x] = ((unsigned long long)it << 40) | ((unsigned long long)op << 32) |
+        F.dbg[64 + vblock(F)] = ((unsigned long long)it << 40) | ((unsigned long long)op << 32) |
                                  (unsigned long long)sm.nsweep;
     double total = 0.0, gm = 0.0, total2 = 0.0;
     if (F.cfg.blocktree) {
@@ -1583,7 +1602,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         // recursion of <= 32 pixels
         const int dG = F.G > F.tb_G ? F.G - F.tb_G : 0;
         const bool sub = F.tb_G >= F.G;
-        for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
+        for (uint32_t bn = vblock(F); bn < F.tb_nbn; bn += vgrid(F)) {
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
             const uint32_t nch = (bsz + NG - 1) / NG;
@@ -1640,7 +1659,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
     } else {
         double cmax = 0.0;
         {
-            const uint32_t gw = blockIdx.x * kWarps + warp, nw = gridDim.x * kWarps;
+            const uint32_t gw = vblock(F) * kWarps + warp, nw = vgrid(F) * kWarps;
             const uint32_t nchunks = (F.npix + NG - 1) / NG;
             for (uint32_t c = gw; c < nchunks; c += nw) {
                 const uint32_t lo = c * NG;
@@ -1658,14 +1677,14 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         if (threadIdx.x == 0) {
             double bm = 0.0;
             for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
-            F.bmax[blockIdx.x] = bm;
+            F.bmax[vblock(F)] = bm;
         }
         if (gbar(F, sm, op, it)) {
             if (threadIdx.x == 0) sm.c.done = 1;
             __syncthreads();
             return;
         }
-        for (uint32_t bn = blockIdx.x; bn < F.nbn; bn += gridDim.x) {
+        for (uint32_t bn = vblock(F); bn < F.nbn; bn += vgrid(F)) {
             if (warp < F.wpb) {
                 uint32_t lo, size;
                 tree_node_range(F.npix, F.G, bn * (uint32_t)F.wpb + warp, lo, size);
@@ -1687,14 +1706,14 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         if (threadIdx.x == 0) {
             __threadfence();
             unsigned int tk = atomicAdd(&F.ctl->ticket, 1u);
-            sm.is_last = (tk == gridDim.x - 1);
+            sm.is_last = (tk == vgrid(F) - 1);
         }
         __syncthreads();
         if (sm.is_last) {
             __threadfence();
             double t = top_tree(F, sm);
             double g = 0.0;
-            for (uint32_t b = threadIdx.x; b < gridDim.x; b += kBlock) g = std_max(g, ld_cg(&F.bmax[b]));
+            for (uint32_t b = threadIdx.x; b < vgrid(F); b += kBlock) g = std_max(g, ld_cg(&F.bmax[b]));
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) g = std_max(g, __shfl_xor_sync(0xffffffffu, g, o));
             if (lane == 0) sm.wmax[warp] = g;
@@ -1716,11 +1735,11 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         gm = ld_cg(&F.ctl->red_max);
     }
     if (threadIdx.x == 0) {
-        controller(F, &sm.c, blockIdx.x == 0, op, it, total, gm);
+        controller(F, &sm.c, vblock(F) == 0, op, it, total, gm);
         // the second candidate is the next backtracking step: taken exactly
         // when the first was rejected and the search goes on
         if ((KIND == K_CAND_T || KIND == K_CAND_R) && X.two && F.cfg.blocktree && !sm.c.done)
-            controller(F, &sm.c, blockIdx.x == 0, op, it, total2, gm);
+            controller(F, &sm.c, vblock(F) == 0, op, it, total2, gm);
         sm.nsweep += 1u;
     }
     SWEEP_STAMP(b0t0, 103);
@@ -1941,7 +1960,7 @@ __device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
     unsigned int total = 0;
     unsigned int base = scan_stage_b_base(F, sm, &total);
     uint32_t c0, c1;
-    chunk_range(F.npix, c0, c1);
+    chunk_range(F, F.npix, c0, c1);
     const uint32_t* bo = F.bo[sc];
     const double rmin = F.cfg.r_min;
     for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
@@ -1960,7 +1979,7 @@ __device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
             ++o;
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0) {
         F.bo[sc ^ 1][F.npix] = total;
         F.ctl->P = total;
     }

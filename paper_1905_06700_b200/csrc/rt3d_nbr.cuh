@@ -209,7 +209,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ApssWarpSm& A = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;
-    const uint32_t gw = blockIdx.x * wpb + warp, nw = gridDim.x * wpb;
+    const uint32_t gw = vblock(F) * wpb + warp, nw = vgrid(F) * wpb;
     const double R = F.cfg.R, r2 = R * R;
     (void)F.amom_stride;
     const int W = F.cfg.W;
@@ -270,31 +270,19 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             window_rows(F, nfi, W, nci0, nci1);
             single_next = nci1 - nci0 < 32;
         }
-        // pass A: ball size, weights, wsum and weighted mean (denoise.hpp:172-186)
+        // pass A (denoise.hpp:172-186): the scan only collects the ball (member
+        // rank order = ascending index) with its d^2 into the list; the weights
+        // and the weighted sums then run densely over the list, member m on
+        // lane m mod 32 in increasing m: the same per-lane sequences as
+        // accumulating chunk by chunk, with every lane busy in the costly
+        // sqrt / division / weight work
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         unsigned int cnt = 0;
         auto visitA = [&](int rank, uint32_t, const Pos& o, double d2, int mfi, int mfj) {
-            const double w = apss_weight(R, sqrt(d2));
-            double* c = A.chunk[rank];
-            c[0] = w;
-            c[1] = o.x;
-            c[2] = o.y;
-            c[3] = o.z;
             const unsigned int g = cnt + (unsigned int)rank;
-            if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, w, mfi, mfj};
+            if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, d2, mfi, mfj};
         };
-        auto flushA = [&](int nm) {
-            const int r = (lane - (int)cnt) & 31;  // member cnt + r has lane (cnt + r) mod 32
-            if (r < nm) {
-                const double* c = A.chunk[r];
-                const double w = c[0];
-                a0 += w;
-                a1 += w * c[1];
-                a2 += w * c[2];
-                a3 += w * c[3];
-            }
-            cnt += (unsigned int)nm;
-        };
+        auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
         if (single) rows_scan(F, tc, sc, rcur, total, q, r2, visitA, flushA);
         else ball_scan(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
         if (has_next && single_next) rows_load(F, sc, nfi, nfj, W, nci0, nci1, nm0, nlen);
@@ -302,6 +290,42 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             single_cur = single_next;
             if (has_next && single_next) ntot = rows_finish(A.rtn[(j + 1) & 1u], nm0, nlen);
         };
+        if (cnt <= (unsigned int)kApssList) {
+            __syncwarp();
+            for (unsigned int g = lane; g < cnt; g += 32) {
+                ApssMember& mb = A.u.list[g];
+                const double w = apss_weight(R, sqrt(mb.w));
+                mb.w = w;
+                a0 += w;
+                a1 += w * ((mb.fi + 0.5) * F.pitch);
+                a2 += w * ((mb.fj + 0.5) * F.pitch);
+                a3 += w * mb.z;
+            }
+            __syncwarp();
+        } else {  // ball larger than the list: accumulate chunk by chunk on a rescan
+            unsigned int c1 = 0;
+            ball_scan(
+                F, tc, sc, A.rt, fi, fj, q, r2,
+                [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
+                    double* c = A.chunk[rank];
+                    c[0] = apss_weight(R, sqrt(d2));
+                    c[1] = o.x;
+                    c[2] = o.y;
+                    c[3] = o.z;
+                },
+                [&](int nm) {
+                    const int r = (lane - (int)c1) & 31;  // member c1 + r has lane (c1 + r) mod 32
+                    if (r < nm) {
+                        const double* c = A.chunk[r];
+                        const double w = c[0];
+                        a0 += w;
+                        a1 += w * c[1];
+                        a2 += w * c[2];
+                        a3 += w * c[3];
+                    }
+                    c1 += (unsigned int)nm;
+                });
+        }
         const double wsum = warp_halving_sum(a0);
         double m0 = warp_halving_sum(a1), m1 = warp_halving_sum(a2), m2 = warp_halving_sum(a3);
         if (cnt < (unsigned int)F.cfg.min_nbrs || wsum <= 0.0) {
@@ -369,7 +393,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
 // (denoise.hpp:186-214, reconstruct.hpp:352-363); writes t[tc^1] and flags
 static __device__ void apss_fit_threads(const Frame& F, uint32_t P, int tc, int sc) {
     (void)F.amom_stride;
-    for (uint32_t n = blockIdx.x * blockDim.x + threadIdx.x; n < P; n += gridDim.x * blockDim.x) {
+    for (uint32_t n = vblock(F) * blockDim.x + threadIdx.x; n < P; n += vgrid(F) * blockDim.x) {
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
         const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
         uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
@@ -480,7 +504,7 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KnnWarpSm& K = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;
-    const uint32_t gw = blockIdx.x * wpb + warp, nw = gridDim.x * wpb;
+    const uint32_t gw = vblock(F) * wpb + warp, nw = vgrid(F) * wpb;
     const double R = F.cfg.R, r2 = R * R;
     const double* rr = F.r[rc];
     const int k = F.cfg.knn_k, Wfull = F.cfg.W;

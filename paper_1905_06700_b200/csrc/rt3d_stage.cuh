@@ -17,7 +17,7 @@ namespace rt3d {
 template <class SM>
 __device__ __forceinline__ void gsync(SM& sm, const Frame& F, int phase) {
     gbar(F, sm, 1000 + phase);
-    if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (F.prof && vblock(F) == 0 && threadIdx.x == 0) {
         unsigned int k = F.ctl->nprof;
         if (k < F.ctl->prof_cap) {
             F.prof[2 * k] = (unsigned long long)phase;
@@ -28,7 +28,7 @@ __device__ __forceinline__ void gsync(SM& sm, const Frame& F, int phase) {
 }
 
 __device__ __forceinline__ void stamp(const Frame& F, int phase) {
-    if (F.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (F.prof && vblock(F) == 0 && threadIdx.x == 0) {
         unsigned int k = F.ctl->nprof;
         if (k < F.ctl->prof_cap) {
             F.prof[2 * k] = (unsigned long long)phase;
@@ -68,7 +68,7 @@ __device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, 
         // two-candidate sweeps do not store their candidates: write the
         // accepted one for this block's own points (same expressions)
         const double a = sm.c.alpha;
-        for (uint32_t bn = blockIdx.x; bn < F.tb_nbn; bn += gridDim.x) {
+        for (uint32_t bn = vblock(F); bn < F.tb_nbn; bn += vgrid(F)) {
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
             const uint32_t n0 = F.bo[sc][blo], n1 = F.bo[sc][blo + bsz];
@@ -90,7 +90,7 @@ enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3, ST
 template <int G>
 __device__ int depth_block(const Frame& F, SmemT<G>& sm, int it, int tc, int rc, int bc, int sc) {
     const uint32_t P = ld_cg(&F.ctl->P);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (vblock(F) == 0 && threadIdx.x == 0) {
         StepDiagDev& d = F.diag[it];
         d.nll_before = sm.c.nll_cur;
         d.points_before = P;
@@ -114,18 +114,21 @@ struct StageOcc {
 };
 
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Frame F, int it);
+__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
+    stage_kernel(const __grid_constant__ FrameBatch FB, int it);
 
 // One stage of a frame: a cooperative kernel whose phases are separated by
 // grid barriers.  Buffer toggles live in Ctl between kernels; every block
 // reads them at entry, the leader writes them back at exit (after at least
 // one barrier, so no block still reads them).
 template <int STAGE, int G>
-__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Frame F, int it) {
+__global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
+    stage_kernel(const __grid_constant__ FrameBatch FB, int it) {
+    const Frame& F = FB.f[FB.n == 1 ? 0u : blockIdx.x / FB.bpf];
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);
-    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    const bool leader = vblock(F) == 0 && threadIdx.x == 0;
     const int prog = F.cfg.program;
     if (STAGE != ST_FIRST && (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort))) return;
     if (!F.irf_of_pix) {  // shared IRF: tables in shared memory
@@ -298,8 +301,8 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Fra
         cand_loop<K_CAND_B, G>(F, sm, tc, rc, bc, sc, OP_CAND_B, it);
         if (sm.c.accept) bc ^= 1;
         if (F.cfg.bg_mode == 1) {
-            const uint32_t nth = gridDim.x * kBlock;
-            const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
+            const uint32_t nth = vgrid(F) * kBlock;
+            const uint32_t gtid = vblock(F) * kBlock + threadIdx.x;
             const int nr = F.rows, nc = F.cols;
             double* re = F.fft_re;
             double* im = F.fft_im;
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks) stage_kernel(Fra
     }
 }
 
-using StageFn = void (*)(Frame, int);
+using StageFn = void (*)(FrameBatch, int);
 enum { kNumStages = 5 };
 
 }  // namespace rt3d

@@ -65,6 +65,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
     _bind(L, "rt3d_set_cube_spcb", _st, [SS, C.c_void_p, _u64])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
+    _bind(L, "rt3d_reconstruct_batch", _st, [P(SS), _i32, P(ReconConfig)])
     _bind(L, "rt3d_frame_submit", _st, [SS, P(Cube), P(ReconConfig), P(_u64)])
     _bind(L, "rt3d_frame_collect", _st, [SS, _u64, P(Point), _u64, P(_u64), P(_dbl), P(Report)])
     _bind(L, "rt3d_report_info", _st, [SS, P(Report)])
@@ -108,7 +109,7 @@ EXPORTED = [
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
-    "rt3d_reconstruct", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
+    "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
     "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
@@ -212,6 +213,15 @@ class Session:
     def reconstruct_async(self, cfg: Config):
         self._cfg_c = cfg.to_c()
         _check(lib().rt3d_reconstruct(self.h, C.byref(self._cfg_c)))
+
+    @staticmethod
+    def reconstruct_batch_async(sessions, cfg: Config):
+        """rt3d_reconstruct_batch: one frame per session (each on its own
+        resident cube) in one launch sequence on sessions[0]'s stream."""
+        arr = (C.c_void_p * len(sessions))(*[s.h for s in sessions])
+        c = cfg.to_c()
+        sessions[0]._cfg_c = c
+        _check(lib().rt3d_reconstruct_batch(arr, len(sessions), C.byref(c)))
 
     @property
     def stream_ptr(self) -> int:
