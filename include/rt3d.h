@@ -253,6 +253,24 @@ rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
  * RT3D_ERR_UNSUPPORTED when the cubes need different sweep layouts. */
 rt3d_status rt3d_reconstruct_batch(rt3d_session* const* sessions, int32_t n,
                                    const rt3d_recon_config* cfg);
+/* Row bands of ONE large frame: n in {1,2,4,8}
+ * sessions holding the same sensor and cube; session k reconstructs the
+ * pixels of node k at depth log2(n) of parallel::pairwise_sum's tree
+ * (parallel.hpp:52-61; whole rows), reading its neighbours' halo rows before
+ * APSS and kNN (reconstruct.hpp:352-397) and combining the sweep sums over all
+ * bands with the reference's tree, so the frame equals rt3d_reconstruct's bit
+ * for bit.  Afterwards rt3d_state_size / rt3d_state_copy of session k give
+ * its own points (the frame's cloud = the bands' clouds in order) and the
+ * background of its pixels rt3d_band_pixels(). */
+rt3d_status rt3d_reconstruct_bands(rt3d_session* const* sessions, int32_t n,
+                                   const rt3d_recon_config* cfg);
+rt3d_status rt3d_band_pixels(rt3d_session* s, uint32_t* pixel_begin, uint32_t* pixel_end);
+/* The band plan (host only, no device): band k's pixels [begin[k], end[k])
+ * and the halo rows every band reads on either side; RT3D_ERR_UNSUPPORTED
+ * when the bands are not whole rows at least halo_rows tall. */
+rt3d_status rt3d_band_plan(uint32_t n_rows, uint32_t n_cols, int32_t superres, double pixel_pitch,
+                           double apss_radius, int32_t n, uint32_t* begin, uint32_t* end,
+                           uint32_t* halo_rows);
 
 /* Pipelined frames (a video stream through one session):
  * rt3d_frame_submit validates `cube`, copies it (pinned host memory avoids a

@@ -40,22 +40,23 @@ StageFn stage_fn_g32(int st);
 StageFn stage_fn_g3(int st);
 StageFn stage_fn_g1(int st);
 
-#define BATCH_FRAME(FB) (FB).f[(FB).n == 1 ? 0u : blockIdx.x / (FB).bpf]
+#define BATCH_FRAME(FB) (FB).f[(FB).n == 1 ? 0u : (FB).first + blockIdx.x / (FB).bpf]
 
 __global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(const __grid_constant__ FrameBatch FB) {
     const Frame& F = BATCH_FRAME(FB);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
-    apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw), ld_cg(&F.ctl->P),
-                      ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
+    apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase),
+                      ld_cg(&F.ctl->pown), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
 }
 
 __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(const __grid_constant__ FrameBatch FB) {
     const Frame& F = BATCH_FRAME(FB);
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS_FIT);
-    apss_fit_threads(F, ld_cg(&F.ctl->P), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
+    apss_fit_threads(F, ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown), ld_cg(&F.ctl->tc),
+                     ld_cg(&F.ctl->sc));
 }
 
 __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant__ FrameBatch FB) {
@@ -63,8 +64,53 @@ __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
-    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->P), ld_cg(&F.ctl->tc),
-              ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
+    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown),
+              ld_cg(&F.ctl->tc), ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
+}
+
+// Row bands: every band keeps full-size arrays in the global
+// index space (pixels and points), so a halo is a plain copy of the
+// neighbouring bands' rows into this band's arrays at the same indices:
+// the bucket offsets of the halo pixels and, for their points, t and the
+// fine cells (what & 1: before APSS) and t and r (what & 2: before kNN).
+// The neighbours' buffers are read directly (the same device here; peer
+// memory over NVLink when the bands sit on different GPUs).
+__global__ void halo_kernel(const __grid_constant__ FrameBatch FB, int what) {
+    const uint32_t k = FB.first + blockIdx.x / FB.bpf;
+    const Frame& F = FB.f[k];
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
+    const uint32_t nth = FB.bpf * blockDim.x;
+    const uint32_t tid = (blockIdx.x - F.blk0) * blockDim.x + threadIdx.x;
+    const int tc = ld_cg(&F.ctl->tc), rc = ld_cg(&F.ctl->rc), sc = ld_cg(&F.ctl->sc);
+    for (int side = 0; side < 2; ++side) {
+        const int j = (int)k + (side ? 1 : -1);
+        if (j < 0 || j >= (int)FB.n) continue;
+        const Frame& N = FB.f[j];
+        uint32_t p0, p1;  // the halo pixels, owned by band j
+        if (side == 0) {
+            p0 = F.bpix0 > F.halo_px ? F.bpix0 - F.halo_px : 0u;
+            p1 = F.bpix0;
+        } else {
+            p0 = F.bpix1;
+            p1 = F.bpix1 + F.halo_px < F.npix ? F.bpix1 + F.halo_px : F.npix;
+        }
+        const uint32_t* nbo = N.bo[sc];
+        uint32_t* obo = F.bo[sc];
+        if (what & 1)  // bo[p0 .. p1) above (bo[bpix0] is ours), bo(p0 .. p1] below
+            for (uint32_t q = tid; q < p1 - p0; q += nth) {
+                const uint32_t p = side ? p0 + 1 + q : p0 + q;
+                obo[p] = ld_cg(&nbo[p]);
+            }
+        const uint32_t n0 = ld_cg(&nbo[p0]), n1 = ld_cg(&nbo[p1]);
+        for (uint32_t n = n0 + tid; n < n1; n += nth) {
+            F.t[tc][n] = ld_cg(&N.t[tc][n]);
+            if (what & 2) F.r[rc][n] = ld_cg(&N.r[rc][n]);
+            if (what & 1) {
+                F.fi[sc][n] = ld_cg(&N.fi[sc][n]);
+                F.fj[sc][n] = ld_cg(&N.fj[sc][n]);
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -306,10 +352,11 @@ __global__ void gather_frame_kernel(Frame F, rt3d_point* out, double* bg, Ctl* c
     if (tid == 0) *ctl_out = *c;
 }
 
-__global__ void gather_points_kernel(Frame F, uint32_t P, int tc, int rc, int sc, int baseline,
-                                     rt3d_point* out) {
-    uint32_t n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= P) return;
+__global__ void gather_points_kernel(Frame F, uint32_t pb, uint32_t P, int tc, int rc, int sc,
+                                     int baseline, rt3d_point* out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= P) return;
+    const uint32_t n = pb + k;
     rt3d_point q;
     const uint32_t p = F.pix[sc][n];
     const int i = (int)(p / F.cols), j = (int)(p % F.cols);
@@ -330,7 +377,7 @@ __global__ void gather_points_kernel(Frame F, uint32_t P, int tc, int rc, int sc
         q.y = (q.fj + 0.5) * F.pitch;
     }
     q.z = q.t * F.bres;
-    out[n] = q;
+    out[k] = q;
 }
 
 }  // namespace rt3d
@@ -444,6 +491,9 @@ struct rt3d_session {
     bool baseline_state = false;
     bool state_pinned = true;
     uint32_t P = 0;
+    uint32_t pbase = 0;        // first point of the state (row bands: the band's own)
+    bool banded = false;       // the state is one row band of a frame (rt3d_reconstruct_bands)
+    uint32_t band_pix0 = 0, band_pix1 = 0;
     int tc = 0, rc = 0, bc = 0, sc = 0;
     std::vector<uint32_t> perm;  // device order -> caller's cloud order (nll/grads API)
     uint32_t max_pts_per_pixel = 0;
@@ -469,7 +519,9 @@ struct rt3d_session {
     // frame (its Frame bytes: buffers, config, toggles) and timing mode match
     struct GraphCache {
         bool valid = false;
-        int n = 0;  // frames of the batch
+        int n = 0, first = 0, count = 0;  // frames of the batch; the ones launched
+        uint32_t bpf = 0;
+        bool zero_ctl = true;
         Frame F[kMaxBatch];
         cudaGraphExec_t exec = nullptr;
         uint64_t used = 0;
@@ -698,6 +750,13 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
         F.tblk2[0] = F.tblk[0] + 2 * F.tb_nbn;
         F.tblk2[1] = F.tblk[0] + 3 * F.tb_nbn;
     }
+    // one band: the whole frame
+    F.nbands = 1;
+    F.band = 0;
+    F.bpix0 = 0;
+    F.bpix1 = npix;
+    F.bbn0 = 0;
+    F.bbn1 = F.tb_nbn;
     {
         const int cfgi = cfg_index(F.cfg.gsz);
         if (std::min(s->per_sm_c[cfgi], blocks_per_sm(s, cfgi)) < s->sharing)
@@ -770,26 +829,38 @@ rt3d_status timed_launch(rt3d_session* s, int cls, Fn&& fn) {
 
 // The batch of frames as one parameter block per kernel: frame k takes blocks
 // [k bpf, (k+1) bpf) of the launch and its own barrier counters
-static void make_batch(FrameBatch& FB, const Frame* Fs, int n, uint32_t bpf) {
+// Row bands of one frame (Fs[k].nbands > 1) are coupled: one grid barrier
+// over all bands' blocks (band 0's counters), one scan over all bands' blocks
+// in band order (band 0's block totals).
+static void make_batch(FrameBatch& FB, const Frame* Fs, int n, uint32_t bpf, int first = 0) {
+    const bool coupled = Fs[0].nbands > 1;
     FB.n = (uint32_t)n;
     FB.bpf = bpf;
+    FB.first = (uint32_t)first;
     for (int k = 0; k < n; ++k) {
         FB.f[k] = Fs[k];
-        FB.f[k].blk0 = (uint32_t)k * bpf;
+        FB.f[k].blk0 = (uint32_t)(k - first) * bpf;  // (frames outside the launch: unused)
         FB.f[k].nblk = bpf;
-        FB.f[k].barc = Fs[k].ctl;
-        FB.f[k].bar_n = bpf;
-        FB.f[k].bar_b0 = (uint32_t)k * bpf;
+        FB.f[k].barc = coupled ? Fs[0].ctl : Fs[k].ctl;
+        FB.f[k].bar_n = coupled ? bpf * (uint32_t)n : bpf;
+        FB.f[k].sblk0 = coupled ? (uint32_t)k * bpf : 0u;
+        FB.f[k].sblk_n = coupled ? bpf * (uint32_t)n : bpf;
     }
 }
 
 // the frames as a stream-ordered kernel sequence on s's stream; every
 // decision stays on the device (each frame's Ctl), so nothing here waits for
 // the GPU.  The frames of a batch share every launch (same configuration).
-rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n) {
-    const Frame& F = Fs[0];
-    for (int k = 0; k < n; ++k) {
-        CUDA_TRY(cudaMemsetAsync(Fs[k].ctl, 0, sizeof(Ctl), s->stream));
+// frames [first, first + count) of the n run on s's device; the others (row
+// bands on other GPUs) only lend their buffers' addresses.  bpf: stage
+// blocks per frame (0: the co-resident stage blocks split among count).
+rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int first, int count,
+                                 uint32_t bpf, bool zero_ctl = true) {
+    const Frame& F = Fs[first];
+    for (int k = first; k < first + count; ++k) {
+        // (bands on several devices: the controllers were zeroed before any
+        // device started, see rt3d_reconstruct_bands)
+        if (zero_ctl) CUDA_TRY(cudaMemsetAsync(Fs[k].ctl, 0, sizeof(Ctl), s->stream));
         CUDA_TRY(cudaMemsetAsync(Fs[k].diag, 0,
                                  sizeof(StepDiagDev) * std::max(Fs[k].cfg.max_iters, 1), s->stream));
     }
@@ -797,17 +868,25 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n) {
     static const int stage_cls[5] = {RT3D_KC_STAGE_FIRST, RT3D_KC_STAGE_DEPTH,
                                      RT3D_KC_STAGE_INTENSITY, RT3D_KC_STAGE_TAIL, RT3D_KC_ITER};
     // cooperative stage grids: the co-resident blocks split among the frames
-    const uint32_t sbpf = (uint32_t)std::max(1, s->grid_frame_c[cfgi] / n);
-    static thread_local FrameBatch fb_stage, fb_apss, fb_fit, fb_knn;
-    make_batch(fb_stage, Fs, n, sbpf);
-    make_batch(fb_apss, Fs, n, (uint32_t)s->grid_apss);
-    make_batch(fb_fit, Fs, n, (uint32_t)s->grid_fit);
-    make_batch(fb_knn, Fs, n, (uint32_t)s->grid_knn);
+    const uint32_t sbpf = bpf ? bpf : (uint32_t)std::max(1, s->grid_frame_c[cfgi] / count);
+    static thread_local FrameBatch fb_stage, fb_apss, fb_fit, fb_knn, fb_halo;
+    make_batch(fb_stage, Fs, n, sbpf, first);
+    const bool bands = F.nbands > 1;
+    if (bands) make_batch(fb_halo, Fs, n, (uint32_t)s->nsm, first);
+    auto halo = [&](int what) -> rt3d_status {
+        if (!bands) return RT3D_OK;
+        halo_kernel<<<s->nsm * count, 256, 0, s->stream>>>(fb_halo, what);
+        CUDA_TRY(cudaGetLastError());
+        return RT3D_OK;
+    };
+    make_batch(fb_apss, Fs, n, (uint32_t)s->grid_apss, first);
+    make_batch(fb_fit, Fs, n, (uint32_t)s->grid_fit, first);
+    make_batch(fb_knn, Fs, n, (uint32_t)s->grid_knn, first);
     auto stage = [&](int st, int it) -> rt3d_status {
         return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
             void* args[] = {&fb_stage, &it};
             CUDA_TRY(cudaLaunchCooperativeKernel((const void*)stage_fn(cfgi, st),
-                                                 dim3(sbpf * (uint32_t)n), dim3(kBlock), args,
+                                                 dim3(sbpf * (uint32_t)count), dim3(kBlock), args,
                                                  stage_smem(cfgi), s->stream));
             return RT3D_OK;
         });
@@ -822,22 +901,24 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n) {
                 continue;
             }
             if (!F.cfg.fuse_depth && (st = stage(ST_DEPTH, it))) return st;
+            if ((st = halo(1))) return st;  // t, cells, buckets of the halo rows
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
-                apss_kernel<<<s->grid_apss * n, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps,
+                apss_kernel<<<s->grid_apss * count, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps,
                               s->stream>>>(fb_apss);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
             if (st) return st;
             st = timed_launch(s, RT3D_KC_APSS_FIT, [&]() -> rt3d_status {
-                apss_fit_kernel<<<s->grid_fit * n, kFitBlock, 0, s->stream>>>(fb_fit);
+                apss_fit_kernel<<<s->grid_fit * count, kFitBlock, 0, s->stream>>>(fb_fit);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
             if (st) return st;
             if ((st = stage(ST_INTENSITY, it))) return st;
+            if ((st = halo(2))) return st;  // t after APSS, r after the intensity step
             st = timed_launch(s, RT3D_KC_KNN, [&]() -> rt3d_status {
-                knn_kernel<<<s->grid_knn * n, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
+                knn_kernel<<<s->grid_knn * count, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
                              s->stream>>>(fb_knn);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
@@ -863,14 +944,18 @@ static void graph_cache_drop(rt3d_session* s, int k) {
 // by the Frame bytes of the batch (buffers, configuration, toggles), least
 // recently used out.  Kernel timing (CUDA events around every launch) and the
 // in-kernel profiler launch directly; so does RT3D_NO_GRAPH=1.
-rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n) {
+rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n, int first = 0, int count = -1,
+                          uint32_t bpf = 0, bool zero_ctl = true) {
+    if (count < 0) count = n;
     for (int k = 0; k < n; ++k) Fs[k].prof_cap = Fs[k].prof ? (uint32_t)(s->prof.cap / 16) : 0u;
     static const bool no_graph = getenv("RT3D_NO_GRAPH") != nullptr;
-    if (no_graph || Fs[0].prof || s->time_kernels) return launch_frames_direct(s, Fs, n);
+    if (no_graph || Fs[first].prof || s->time_kernels)
+        return launch_frames_direct(s, Fs, n, first, count, bpf, zero_ctl);
     const int nc = (int)(sizeof(s->gc) / sizeof(s->gc[0]));
     int hit = -1, victim = 0;
     for (int k = 0; k < nc; ++k) {
-        if (s->gc[k].valid && s->gc[k].n == n &&
+        if (s->gc[k].valid && s->gc[k].n == n && s->gc[k].first == first &&
+            s->gc[k].count == count && s->gc[k].bpf == bpf && s->gc[k].zero_ctl == zero_ctl &&
             std::memcmp(s->gc[k].F, Fs, sizeof(Frame) * (size_t)n) == 0)
             hit = k;
         if (!s->gc[k].valid || (s->gc[victim].valid && s->gc[k].used < s->gc[victim].used)) victim = k;
@@ -880,7 +965,7 @@ rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n) {
         graph_cache_drop(s, hit);
         auto& g = s->gc[hit];
         CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
-        const rt3d_status st = launch_frames_direct(s, Fs, n);
+        const rt3d_status st = launch_frames_direct(s, Fs, n, first, count, bpf, zero_ctl);
         cudaGraph_t graph = nullptr;
         const cudaError_t ce = cudaStreamEndCapture(s->stream, &graph);
         if (st) {
@@ -893,6 +978,10 @@ rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n) {
         if (ie != cudaSuccess) return fail(RT3D_ERR_CUDA, "CUDA: graph instantiate: %s", cudaGetErrorString(ie));
         std::memcpy(g.F, Fs, sizeof(Frame) * (size_t)n);
         g.n = n;
+        g.first = first;
+        g.count = count;
+        g.bpf = bpf;
+        g.zero_ctl = zero_ctl;
         g.valid = true;
     }
     s->gc[hit].used = ++s->gc_clock;
@@ -1473,7 +1562,9 @@ static rt3d_status prepare_init_like(rt3d_session* s, const rt3d_recon_config* c
     return RT3D_OK;
 }
 
-static void finish_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program) {
+static void finish_init_like(rt3d_session* s, const rt3d_recon_config* cfg, int program,
+                             bool banded = false) {
+    s->banded = banded;
     s->have_state = true;
     s->baseline_state = program == PROG_BASELINE;
     s->state_pinned = true;
@@ -1493,13 +1584,31 @@ static rt3d_status run_init_like(rt3d_session* s, const rt3d_recon_config* cfg, 
     return RT3D_OK;
 }
 
+// Host tree_node_range (rt3d_math.cuh): node k at depth d of pairwise_sum's
+// recursion over n elements
+static void host_node_range(uint32_t n, int d, uint32_t k, uint32_t& lo, uint32_t& size) {
+    lo = 0;
+    size = n;
+    for (int b = d - 1; b >= 0; --b) {
+        const uint32_t h = size / 2;
+        if ((k >> b) & 1u) {
+            lo += h;
+            size -= h;
+        } else {
+            size = h;
+        }
+    }
+}
+
 static rt3d_status resolve_state(rt3d_session* s) {
     if (!s->have_state) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no state in session");
     if (s->iterations != -1) return RT3D_OK;
     rt3d_status st = read_ctl(s);
     if (st) return st;
     const Ctl& c = *s->h_ctl;
-    s->P = c.P;
+    // a row band's state is its own points [pbase, pbase + pown)
+    s->P = s->banded ? c.pown : c.P;
+    s->pbase = s->banded ? c.pbase : 0u;
     s->tc = c.tc;
     s->rc = c.rc;
     s->bc = c.bc;
@@ -1518,6 +1627,196 @@ rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
 // each frame with its own controller and grid barrier.  The sessions'
 // streams are ordered before and after the batch, so their results read as
 // after rt3d_reconstruct.
+// One frame split into n row bands: session k owns
+// the pixels of node k at depth log2(n) of pairwise_sum's tree, so each
+// band's nll is an exact subtree and the combined tree is the single-GPU
+// tree bit for bit.  Every session holds the same sensor and cube and
+// full-size state arrays in the global index space; a band computes only its
+// own pixels and points, and reads its neighbours' halo rows (ceil(W / s)
+// coarse rows, W the APSS window) through halo_kernel before APSS and kNN.
+// The bands' stage kernels are coupled: one grid barrier and one prune /
+// spawn scan over all bands' blocks, one block-node array for the sweep
+// trees.  Bands on one device run in one launch sequence; bands on several
+// devices run one coupled launch sequence per device.  The result is
+// identical to rt3d_reconstruct for any n.
+rt3d_status rt3d_reconstruct_bands(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
+    if (!ss || n < 1 || n > kMaxBatch || (n & (n - 1)))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: 1, 2, 4 or 8 row bands");
+    for (int k = 0; k < n; ++k) {
+        if (!ss[k]) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session in bands");
+        for (int j = 0; j < k; ++j)
+            if (ss[j] == ss[k]) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: session twice in bands");
+        if (!ss[k]->have_cube || !ss[k]->have_sensor)
+            return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no sensor / cube set");
+        if (ss[k]->rows != ss[0]->rows || ss[k]->cols != ss[0]->cols ||
+            ss[k]->bins != ss[0]->bins || ss[k]->n_events != ss[0]->n_events)
+            return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: row bands need the same sensor and cube");
+    }
+    if (!cfg) return fail(RT3D_ERR_INVALID_ARGUMENT, "null config");
+    if (n > 1 && cfg->background_mode != 0)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: row bands need the identity background");
+    rt3d_session* s0 = ss[0];
+    static thread_local Frame Fs[kMaxBatch];
+    rt3d_status st;
+    for (int k = 0; k < n; ++k)
+        if ((st = prepare_init_like(ss[k], cfg, PROG_RECON, Fs[k]))) return st;
+    for (int k = 1; k < n; ++k)
+        if (std::memcmp(&Fs[k].cfg, &Fs[0].cfg, sizeof(Cfg)) != 0)
+            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: bands built different sweep layouts");
+    const uint32_t npix = Fs[0].npix, cols = (uint32_t)s0->cols;
+    int d = 0;
+    while ((1 << d) < n) ++d;
+    if (n > 1) {
+        if (!Fs[0].cfg.blocktree || !Fs[0].cfg.fuse_depth || Fs[0].cfg.fused_iter)
+            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: row bands need the default frame layout");
+        if (Fs[0].tb_G < d)
+            return fail(RT3D_ERR_UNSUPPORTED, "rt3d: frame too small for %d row bands", n);
+    }
+    const uint32_t hrows = (uint32_t)((Fs[0].cfg.W + s0->s - 1) / s0->s);
+    const uint32_t halo_px = hrows * cols;
+    for (int k = 0; k < n; ++k) {
+        uint32_t lo, size;
+        host_node_range(npix, d, (uint32_t)k, lo, size);
+        if (n > 1 && (lo % cols != 0 || size < halo_px))
+            return fail(RT3D_ERR_UNSUPPORTED,
+                        "rt3d: row band %d [%u, %u) is not whole rows of at least %u rows", k, lo,
+                        lo + size, hrows);
+        Frame& F = Fs[k];
+        F.nbands = n;
+        F.band = k;
+        F.bpix0 = lo;
+        F.bpix1 = lo + size;
+        F.bbn0 = (uint32_t)k * (F.tb_nbn / (uint32_t)n);
+        F.bbn1 = F.bbn0 + F.tb_nbn / (uint32_t)n;
+        F.halo_px = halo_px;
+        // the sweep trees and the scans run over band 0's arrays
+        for (int q = 0; q < 2; ++q) {
+            F.tblk[q] = Fs[0].tblk[q];
+            F.tbmax[q] = Fs[0].tbmax[q];
+            F.tblk2[q] = Fs[0].tblk2[q];
+        }
+        F.btot = Fs[0].btot;
+        ss[k]->band_pix0 = lo;
+        ss[k]->band_pix1 = lo + size;
+    }
+    // bands on several GPUs: runs of consecutive bands on one device form a
+    // launch on that device (its first session's stream), all launches with
+    // the same stage blocks per band; the barrier, the scans and the halo
+    // reads reach the other devices' buffers as peer memory over NVLink
+    int gfirst[kMaxBatch], gcount[kMaxBatch], ng = 0, maxc = 0;
+    for (int k = 0; k < n; ++k) {
+        if (ng && ss[gfirst[ng - 1]]->device == ss[k]->device) {
+            ++gcount[ng - 1];
+        } else {
+            gfirst[ng] = k;
+            gcount[ng++] = 1;
+        }
+        maxc = std::max(maxc, gcount[ng - 1]);
+    }
+    for (int g = 0; g < ng; ++g)
+        for (int h = 0; h < ng; ++h) {
+            const int a = ss[gfirst[g]]->device, b = ss[gfirst[h]]->device;
+            if (a == b) continue;
+            int ok = 0;
+            CUDA_TRY(cudaDeviceCanAccessPeer(&ok, a, b));
+            if (!ok) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: no peer access %d -> %d", a, b);
+            CUDA_TRY(cudaSetDevice(a));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(RT3D_ERR_CUDA, "CUDA: enable peer access: %s", cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+    const int cfgi = cfg_index(Fs[0].cfg.gsz);
+    uint32_t bpf = 0xffffffffu;
+    for (int g = 0; g < ng; ++g)
+        bpf = std::min<uint32_t>(bpf, (uint32_t)std::max(1, ss[gfirst[g]]->grid_frame_c[cfgi] / maxc));
+    for (int g = 0; g < ng; ++g) {
+        rt3d_session* sl = ss[gfirst[g]];
+        CUDA_TRY(cudaSetDevice(sl->device));
+        for (int k = gfirst[g] + 1; k < gfirst[g] + gcount[g]; ++k) {
+            CUDA_TRY(cudaEventRecord(ss[k]->xev, ss[k]->stream));
+            CUDA_TRY(cudaStreamWaitEvent(sl->stream, ss[k]->xev, 0));
+        }
+        for (int k = gfirst[g]; k < gfirst[g] + gcount[g]; ++k)
+            CUDA_TRY(cudaEventRecord(ss[k]->ev0, sl->stream));
+    }
+    // several devices: every controller (band 0's holds the barrier all
+    // devices spin on) is zeroed before any device starts the frame
+    if (ng > 1) {
+        for (int k = 0; k < n; ++k) {
+            CUDA_TRY(cudaSetDevice(ss[k]->device));
+            CUDA_TRY(cudaStreamSynchronize(ss[k]->stream));
+        }
+        for (int g = 0; g < ng; ++g) {
+            rt3d_session* sl = ss[gfirst[g]];
+            CUDA_TRY(cudaSetDevice(sl->device));
+            CUDA_TRY(cudaStreamSynchronize(sl->stream));
+            for (int k = gfirst[g]; k < gfirst[g] + gcount[g]; ++k)
+                CUDA_TRY(cudaMemsetAsync(Fs[k].ctl, 0, sizeof(Ctl), sl->stream));
+            CUDA_TRY(cudaStreamSynchronize(sl->stream));
+        }
+    }
+    // every device's launch sequence is issued before any waits: the coupled
+    // cooperative kernels of all devices run concurrently
+    for (int g = 0; g < ng; ++g) {
+        rt3d_session* sl = ss[gfirst[g]];
+        CUDA_TRY(cudaSetDevice(sl->device));
+        if ((st = launch_frames(sl, Fs, n, gfirst[g], gcount[g], n > 1 ? bpf : 0u, ng == 1)))
+            return st;
+    }
+    for (int g = 0; g < ng; ++g) {
+        rt3d_session* sl = ss[gfirst[g]];
+        CUDA_TRY(cudaSetDevice(sl->device));
+        CUDA_TRY(cudaEventRecord(sl->xev, sl->stream));
+        for (int k = gfirst[g]; k < gfirst[g] + gcount[g]; ++k) {
+            CUDA_TRY(cudaEventRecord(ss[k]->ev1, sl->stream));
+            if (k != gfirst[g]) CUDA_TRY(cudaStreamWaitEvent(ss[k]->stream, sl->xev, 0));
+            finish_init_like(ss[k], cfg, PROG_RECON, n > 1);
+        }
+    }
+    CUDA_TRY(cudaSetDevice(s0->device));
+    return RT3D_OK;
+}
+
+// The row-band plan of rt3d_reconstruct_bands (host only): band k's pixels
+// [begin[k], end[k]) = node k at depth log2(n) of pairwise_sum's tree, and
+// the halo rows each band reads on either side (ceil(W / superres) rows of
+// cols pixels, W = floor(R / pitch) + 1 fine pixels).
+rt3d_status rt3d_band_plan(uint32_t n_rows, uint32_t n_cols, int32_t superres, double pixel_pitch,
+                           double apss_radius, int32_t n, uint32_t* begin, uint32_t* end,
+                           uint32_t* halo_rows) {
+    if (n < 1 || n > kMaxBatch || (n & (n - 1)))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: 1, 2, 4 or 8 row bands");
+    if (!begin || !end || !halo_rows || superres < 1 || !(pixel_pitch > 0.0) || !(apss_radius > 0.0))
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: bad band plan arguments");
+    int d = 0;
+    while ((1 << d) < n) ++d;
+    const uint32_t npix = n_rows * n_cols;
+    const uint32_t hrows = (uint32_t)((window_w(apss_radius, pixel_pitch) + superres - 1) / superres);
+    for (int k = 0; k < n; ++k) {
+        uint32_t lo, size;
+        host_node_range(npix, d, (uint32_t)k, lo, size);
+        begin[k] = lo;
+        end[k] = lo + size;
+        if (n > 1 && (lo % n_cols != 0 || size < hrows * n_cols))
+            return fail(RT3D_ERR_UNSUPPORTED,
+                        "rt3d: row band %d [%u, %u) is not whole rows of at least %u rows", k, lo,
+                        lo + size, hrows);
+    }
+    *halo_rows = hrows;
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_band_pixels(rt3d_session* s, uint32_t* pix0, uint32_t* pix1) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!pix0 || !pix1) return fail(RT3D_ERR_INVALID_ARGUMENT, "null output");
+    if (!s->have_state) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: no state in session");
+    *pix0 = s->banded ? s->band_pix0 : 0u;
+    *pix1 = s->banded ? s->band_pix1 : (uint32_t)(s->rows * s->cols);
+    return RT3D_OK;
+}
+
 rt3d_status rt3d_reconstruct_batch(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
     if (!ss || n < 1 || n > kMaxBatch)
         return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: batch of 1..%d sessions", kMaxBatch);
@@ -1748,7 +2047,8 @@ rt3d_status rt3d_state_copy(rt3d_session* s, rt3d_point* pts, double* background
         if ((st = build_frame(s, F, g, 1))) return st;
         CUDA_TRY(s->outpts.ensure((size_t)s->P * sizeof(rt3d_point)));
         gather_points_kernel<<<(s->P + 255) / 256, 256, 0, s->stream>>>(
-            F, s->P, s->tc, s->rc, s->sc, s->baseline_state ? 1 : 0, s->outpts.as<rt3d_point>());
+            F, s->pbase, s->P, s->tc, s->rc, s->sc, s->baseline_state ? 1 : 0,
+            s->outpts.as<rt3d_point>());
         CUDA_TRY(cudaGetLastError());
         if (s->perm.empty()) {
             CUDA_TRY(cudaMemcpyAsync(pts, s->outpts.p, (size_t)s->P * sizeof(rt3d_point),
@@ -1844,6 +2144,8 @@ static rt3d_status run_sweeps(rt3d_session* s, int program) {
     rt3d_status st = require_device(s);
     if (st) return st;
     if ((st = resolve_state(s))) return st;
+    if (s->banded)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: a row band's state is a part of a frame");
     Cfg g;
     std::memset(&g, 0, sizeof g);
     g.program = program;
@@ -1907,6 +2209,8 @@ rt3d_status rt3d_palm_step(rt3d_session* s, const rt3d_recon_config* cfg, rt3d_s
     if (st) return st;
     if ((st = validate_cfg(cfg))) return st;
     if ((st = resolve_state(s))) return st;
+    if (s->banded)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: a row band's state is a part of a frame");
     if (!s->perm.empty())
         return fail(RT3D_ERR_UNSUPPORTED,
                     "rt3d: palm_step needs a pixel-ordered cloud (cloud order == bucket order)");

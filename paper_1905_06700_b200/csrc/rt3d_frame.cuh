@@ -95,6 +95,7 @@ struct Ctl {
     // kBarrierTimeoutNs aborts the frame instead of hanging the device
     unsigned int bar_count, bar_gen, abort, abort_block;
     unsigned int keep, pad1_;  // points the kNN filter left at r >= r_min (prune skip test)
+    unsigned int pown, pbase;  // this frame's (band's) own points [pbase, pbase + pown)
     int abort_op, abort_it;
     unsigned int abort_count, abort_nsweep;
 };
@@ -193,9 +194,17 @@ struct Frame {
     double* fft_im;
     // launch geometry: this frame's blocks are blk0 .. blk0 + nblk - 1 of the
     // launch (a batch of frames shares one launch, FrameBatch); the grid
-    // barrier counts bar_n blocks on barc's counters, led by block bar_b0
-    uint32_t blk0, nblk, bar_n, bar_b0;
+    // barrier counts bar_n blocks on barc's counters (led by scan slot 0)
+    uint32_t blk0, nblk, bar_n, pad_launch_;
     Ctl* barc;
+    // row bands (large arrays): this frame owns pixels
+    // [bpix0, bpix1) and the block nodes [bbn0, bbn1) of the pairwise tree;
+    // the prune / spawn scans run over all bands' blocks in band order
+    // (scan block sblk0 + vblock of sblk_n); global values (point count,
+    // barrier) live in barc.  One band: the whole frame.
+    int nbands, band;
+    uint32_t bpix0, bpix1, bbn0, bbn1, sblk0, sblk_n;
+    uint32_t halo_px;  // pixels of the halo rows on each side (ceil(W / s) rows)
     // control / report
     unsigned long long* prof;  // optional (id, %globaltimer) pairs after each barrier
     volatile unsigned long long* dbg;  // mapped host memory: progress / fault records
@@ -211,12 +220,15 @@ struct Frame {
 constexpr int kMaxBatch = 8;
 struct FrameBatch {
     uint32_t n, bpf;
+    uint32_t first, pad_;  // this launch runs frames first .. first + gridDim.x / bpf - 1
     Frame f[kMaxBatch];
 };
 
 // this block's index / the block count within its frame
 __device__ __forceinline__ uint32_t vblock(const Frame& F) { return blockIdx.x - F.blk0; }
 __device__ __forceinline__ uint32_t vgrid(const Frame& F) { return F.nblk; }
+// the frame's global point count (all bands)
+__device__ __forceinline__ uint32_t global_P(const Frame& F) { return __ldcg(&F.barc->P); }
 
 // Likelihood sweep staging: a warp owns a tree node of <= 32 consecutive
 // pixels; their events and points are contiguous CSR ranges, copied into
@@ -390,7 +402,7 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
     const uint32_t nwarps = vgrid(F) * kWarps;
     const int K = F.cfg.K, sep = F.cfg.sep, T = F.bins;
     const double thr = F.cfg.thr;
-    for (uint32_t p = vblock(F) * kWarps + (threadIdx.x >> 5); p < F.npix; p += nwarps) {
+    for (uint32_t p = F.bpix0 + vblock(F) * kWarps + (threadIdx.x >> 5); p < F.bpix1; p += nwarps) {
         const double g = F.dead[p] ? 0.0 : F.gain[p];
         const uint32_t e0 = F.off[p], e1 = F.off[p + 1], m = e1 - e0;
         if (g == 0.0 || m == 0) {
@@ -575,18 +587,24 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
 // chunked grid scan: stage A writes per-pixel block-local prefixes, stage B
 // adds the block base (after a grid barrier)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void chunk_range(const Frame& F, uint32_t n, uint32_t& c0, uint32_t& c1) {
+// this block's chunk of the band's pixels [bpix0, bpix1)
+__device__ __forceinline__ void chunk_range(const Frame& F, uint32_t& c0, uint32_t& c1) {
+    const uint32_t n = F.bpix1 - F.bpix0;
     uint32_t chunk = (n + vgrid(F) - 1) / vgrid(F);
     c0 = vblock(F) * chunk;
     c1 = c0 + chunk;
     if (c0 > n) c0 = n;
     if (c1 > n) c1 = n;
+    c0 += F.bpix0;
+    c1 += F.bpix0;
 }
+// this block's slot in the (all-band) scan
+__device__ __forceinline__ uint32_t scan_block(const Frame& F) { return F.sblk0 + vblock(F); }
 
 template <class SM, typename CountFn>
 __device__ void scan_stage_a(const Frame& F, SM& sm, CountFn count) {
     uint32_t c0, c1;
-    chunk_range(F, F.npix, c0, c1);
+    chunk_range(F, c0, c1);
     unsigned int carry = 0;
     for (uint32_t base = c0; base < c1; base += kBlock) {
         uint32_t p = base + threadIdx.x;
@@ -595,19 +613,32 @@ __device__ void scan_stage_a(const Frame& F, SM& sm, CountFn count) {
         if (p < c1) F.cnt[p] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) F.btot[vblock(F)] = carry;
+    if (threadIdx.x == 0) F.btot[scan_block(F)] = carry;
 }
 
-// returns this block's base; thread 0 of the last block publishes the total
+// returns this block's base (over all bands' scan blocks); the band's first
+// index in *band_base, the band's end in *band_end (the band's last block),
+// the total over all bands in *total_out (the scan's last block)
 template <class SM>
-__device__ unsigned int scan_stage_b_base(const Frame& F, SM& sm, unsigned int* total_out) {
-    unsigned int part = 0;
-    for (uint32_t b = threadIdx.x; b < vblock(F); b += kBlock) part += ld_cg(&F.btot[b]);
-    unsigned int tot;
-    unsigned int ex = block_exclusive_scan(part, sm, tot);
-    (void)ex;
-    if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0)
-        *total_out = tot + ld_cg(&F.btot[vblock(F)]);
+__device__ unsigned int scan_stage_b_base(const Frame& F, SM& sm, unsigned int* total_out,
+                                          unsigned int* band_base = nullptr,
+                                          unsigned int* band_end = nullptr) {
+    const uint32_t sb = scan_block(F);
+    unsigned int part = 0, bpart = 0;
+    for (uint32_t b = threadIdx.x; b < sb; b += kBlock) {
+        const unsigned int v = ld_cg(&F.btot[b]);
+        part += v;
+        if (b < F.sblk0) bpart += v;
+    }
+    unsigned int tot, btot_band;
+    (void)block_exclusive_scan(part, sm, tot);
+    (void)block_exclusive_scan(bpart, sm, btot_band);
+    const unsigned int mine = ld_cg(&F.btot[sb]);
+    if (threadIdx.x == 0) {
+        if (sb == F.sblk_n - 1) *total_out = tot + mine;
+        if (band_base) *band_base = btot_band;
+        if (band_end) *band_end = tot + mine;
+    }
     return tot;
 }
 
@@ -622,10 +653,10 @@ __device__ __forceinline__ unsigned int block_sum_u32(unsigned int v, SM& sm) {
 // spawn points of init_matched_filter (reconstruct.hpp:219-237, 245-247)
 template <class SM>
 __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
-    unsigned int total = 0;
-    unsigned int base = scan_stage_b_base(F, sm, &total);
+    unsigned int total = 0, band_base = 0, band_end = 0;
+    unsigned int base = scan_stage_b_base(F, sm, &total, &band_base, &band_end);
     uint32_t c0, c1;
-    chunk_range(F, F.npix, c0, c1);
+    chunk_range(F, c0, c1);
     const int s = F.s, K = F.cfg.K;
     for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
         uint32_t o = base + ld_cg(&F.cnt[p]);
@@ -661,9 +692,11 @@ __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
         }
     }
     if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0) {
-        F.bo[0][F.npix] = total;
-        F.ctl->P = total;
+        F.bo[0][F.bpix1] = band_end;
+        F.ctl->pbase = band_base;
+        F.ctl->pown = band_end - band_base;
     }
+    if (scan_block(F) == F.sblk_n - 1 && threadIdx.x == 0) F.barc->P = total;
 }
 
 // ---------------------------------------------------------------------------
@@ -1300,7 +1333,7 @@ static __device__ void controller(const Frame& F, Ctl* c, bool writer, int op, i
                 StepDiagDev& d = F.diag[it];
                 d.blk[2].nll_after_denoise = v;
                 d.nll_after = v;
-                d.points_after = ld_cg(&F.ctl->P);
+                d.points_after = global_P(F);
                 F.trace[it + 1] = v;
             }
             c->iterations = it + 1;
@@ -1369,10 +1402,14 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
         // one word: block 0 adds 2^31 - (n - 1), the others 1, so the top bit
         // flips exactly when the last block arrives and the low bits return
         // to where they were
+        // (row bands may sit on several GPUs: system-scope fences and atomics
+        // on band 0's counters, reached through peer memory)
         Ctl* c = F.barc;
-        const unsigned int inc = blockIdx.x == F.bar_b0 ? 0x80000000u - (F.bar_n - 1u) : 1u;
-        __threadfence();
-        const unsigned int old = atomicAdd(&c->bar_count, inc);
+        const bool sys = F.nbands > 1;
+        const unsigned int inc = scan_block(F) == 0 ? 0x80000000u - (F.bar_n - 1u) : 1u;
+        if (sys) __threadfence_system();
+        else __threadfence();
+        const unsigned int old = sys ? atomicAdd_system(&c->bar_count, inc) : atomicAdd(&c->bar_count, inc);
         const unsigned long long t0 = globaltimer();
         unsigned int spins = 0;
         while (((ld_volatile(&c->bar_count) ^ old) & 0x80000000u) == 0u) {
@@ -1385,7 +1422,7 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
                     break;
                 }
                 if (globaltimer() - t0 > kBarrierTimeoutNs) {
-                    if (atomicExch(&c->abort, 1u) == 0u) {
+                    if ((sys ? atomicExch_system(&c->abort, 1u) : atomicExch(&c->abort, 1u)) == 0u) {
                         c->abort_block = blockIdx.x;
                         if (F.ctl != c) atomicExch(&F.ctl->abort, 1u);
                         c->abort_op = op;
@@ -1398,7 +1435,8 @@ __device__ bool gbar(const Frame& F, SM& sm, int op = -1, int it = -1) {
                 }
             }
         }
-        __threadfence();
+        if (sys) __threadfence_system();
+        else __threadfence();
     }
     __syncthreads();
     return sm.aborted != 0;
@@ -1602,7 +1640,7 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         // recursion of <= 32 pixels
         const int dG = F.G > F.tb_G ? F.G - F.tb_G : 0;
         const bool sub = F.tb_G >= F.G;
-        for (uint32_t bn = vblock(F); bn < F.tb_nbn; bn += vgrid(F)) {
+        for (uint32_t bn = F.bbn0 + vblock(F); bn < F.bbn1; bn += vgrid(F)) {
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
             const uint32_t nch = (bsz + NG - 1) / NG;
@@ -1957,10 +1995,10 @@ __device__ void phase_prune_a(const Frame& F, SM& sm, int rc, int sc) {
 
 template <class SM>
 __device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
-    unsigned int total = 0;
-    unsigned int base = scan_stage_b_base(F, sm, &total);
+    unsigned int total = 0, band_base = 0, band_end = 0;
+    unsigned int base = scan_stage_b_base(F, sm, &total, &band_base, &band_end);
     uint32_t c0, c1;
-    chunk_range(F, F.npix, c0, c1);
+    chunk_range(F, c0, c1);
     const uint32_t* bo = F.bo[sc];
     const double rmin = F.cfg.r_min;
     for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
@@ -1980,9 +2018,11 @@ __device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
         }
     }
     if (vblock(F) == vgrid(F) - 1 && threadIdx.x == 0) {
-        F.bo[sc ^ 1][F.npix] = total;
-        F.ctl->P = total;
+        F.bo[sc ^ 1][F.bpix1] = band_end;
+        F.ctl->pbase = band_base;
+        F.ctl->pown = band_end - band_base;
     }
+    if (scan_block(F) == F.sblk_n - 1 && threadIdx.x == 0) F.barc->P = total;
 }
 
 // ---------------------------------------------------------------------------

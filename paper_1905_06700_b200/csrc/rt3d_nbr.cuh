@@ -205,7 +205,9 @@ __device__ __forceinline__ double warp_halving_sum(double v) {
 // APSS moments over the current state: warp per point, results to F.amom
 // (kMom doubles per point, one coalesced store per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
 // the covariance is read off M, see apss_pass_b).
-static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t P, int tc, int sc) {
+// points [pb, pb + P) (a band's own points; pb = 0 for a whole frame)
+static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t pb, uint32_t P,
+                                         int tc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     ApssWarpSm& A = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;
@@ -224,9 +226,9 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             jbase = j & ~31u;
             const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
             if (nl < P) {
-                pfi = F.fi[sc][nl];
-                pfj = F.fj[sc][nl];
-                pt = F.t[tc][nl];
+                pfi = F.fi[sc][pb + nl];
+                pfj = F.fj[sc][pb + nl];
+                pt = F.t[tc][pb + nl];
             }
         }
         fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
@@ -251,7 +253,8 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         }
     }
     uint32_t j = 0;
-    for (uint32_t n = gw; n < P; n += nw, ++j) {
+    for (uint32_t nl = gw; nl < P; nl += nw, ++j) {
+        const uint32_t n = pb + nl;
         int fi, fj;
         double tq;
         point(j, fi, fj, tq);
@@ -260,7 +263,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         const bool single = single_cur;
         const uint32_t total = ntot;
         // next point: positions and (single batch) row loads, finished after pass B
-        const bool has_next = n + nw < P;
+        const bool has_next = nl + nw < P;
         int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
         double ntq = 0.0;
         bool single_next = false;
@@ -391,9 +394,10 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
 
 // sphere fit, projection and pinning, one thread per point
 // (denoise.hpp:186-214, reconstruct.hpp:352-363); writes t[tc^1] and flags
-static __device__ void apss_fit_threads(const Frame& F, uint32_t P, int tc, int sc) {
+static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P, int tc, int sc) {
     (void)F.amom_stride;
-    for (uint32_t n = vblock(F) * blockDim.x + threadIdx.x; n < P; n += vgrid(F) * blockDim.x) {
+    for (uint32_t nl = vblock(F) * blockDim.x + threadIdx.x; nl < P; nl += vgrid(F) * blockDim.x) {
+        const uint32_t n = pb + nl;
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
         const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
         uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
@@ -500,7 +504,8 @@ __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k,
 // the next ring, no member outside can enter the top k and the selection is
 // final; otherwise the window grows to the first ring whose bound exceeds
 // the k-th key (at most W, the full ball).
-static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int tc, int rc, int sc) {
+static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, uint32_t P, int tc,
+                                 int rc, int sc) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     KnnWarpSm& K = wsm[warp];
     const uint32_t wpb = blockDim.x >> 5;
@@ -520,9 +525,9 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int
             jbase = j & ~31u;
             const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
             if (nl < P) {
-                pfi = F.fi[sc][nl];
-                pfj = F.fj[sc][nl];
-                pt = F.t[tc][nl];
+                pfi = F.fi[sc][pb + nl];
+                pfj = F.fj[sc][pb + nl];
+                pt = F.t[tc][pb + nl];
             }
         }
         fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
@@ -546,14 +551,15 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t P, int
     }
     uint32_t jj = 0;
     unsigned int kept = 0;
-    for (uint32_t n = gw; n < P; n += nw, ++jj) {
+    for (uint32_t nl = gw; nl < P; nl += nw, ++jj) {
+        const uint32_t n = pb + nl;
         int fi, fj;
         double tq;
         point(jj, fi, fj, tq);
         const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, tq * F.bres};
         const bool first_single = single_cur;
         const uint32_t first_total = ntot;
-        const bool has_next = n + nw < P;
+        const bool has_next = nl + nw < P;
         int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
         double ntq = 0.0;
         bool single_next = false;

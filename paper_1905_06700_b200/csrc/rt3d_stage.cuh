@@ -68,7 +68,7 @@ __device__ void cand_loop(const Frame& F, SmemT<G>& sm, int tc, int rc, int bc, 
         // two-candidate sweeps do not store their candidates: write the
         // accepted one for this block's own points (same expressions)
         const double a = sm.c.alpha;
-        for (uint32_t bn = vblock(F); bn < F.tb_nbn; bn += vgrid(F)) {
+        for (uint32_t bn = F.bbn0 + vblock(F); bn < F.bbn1; bn += vgrid(F)) {
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
             const uint32_t n0 = F.bo[sc][blo], n1 = F.bo[sc][blo + bsz];
@@ -89,7 +89,7 @@ enum Stage : int { ST_FIRST = 0, ST_DEPTH = 1, ST_INTENSITY = 2, ST_TAIL = 3, ST
 // next iteration), so it needs no launch of its own.
 template <int G>
 __device__ int depth_block(const Frame& F, SmemT<G>& sm, int it, int tc, int rc, int bc, int sc) {
-    const uint32_t P = ld_cg(&F.ctl->P);
+    const uint32_t P = global_P(F);
     if (vblock(F) == 0 && threadIdx.x == 0) {
         StepDiagDev& d = F.diag[it];
         d.nll_before = sm.c.nll_cur;
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
 template <int STAGE, int G>
 __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
     stage_kernel(const __grid_constant__ FrameBatch FB, int it) {
-    const Frame& F = FB.f[FB.n == 1 ? 0u : blockIdx.x / FB.bpf];
+    const Frame& F = FB.f[FB.n == 1 ? 0u : FB.first + blockIdx.x / FB.bpf];
     constexpr int stage = STAGE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemT<G>& sm = *reinterpret_cast<SmemT<G>*>(smem_raw);
@@ -170,6 +170,8 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
             const unsigned long long t0 = globaltimer();
             F.ctl->t_start = t0;
             F.ctl->P = F.P0;
+            F.ctl->pown = F.P0;
+            F.ctl->pbase = 0;
             F.ctl->prof_cap = F.prof_cap;
             if (F.prof && F.prof_cap) {
                 F.prof[0] = 0;
@@ -231,17 +233,18 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         // a whole iteration in one launch: the APSS moments and fit as grid
         // phases between barriers (same device functions as apss_kernel /
         // apss_fit_kernel, warp scratch in the stage union)
-        const uint32_t P = ld_cg(&F.ctl->P);
+        const uint32_t P = global_P(F);
         if (P > 0) {
-            apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(sm.u.nbr), P, tc, sc);
+            apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(sm.u.nbr), ld_cg(&F.ctl->pbase),
+                              ld_cg(&F.ctl->pown), tc, sc);
             gsync(sm, F, PH_APSS);
-            apss_fit_threads(F, P, tc, sc);
+            apss_fit_threads(F, ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown), tc, sc);
             gsync(sm, F, PH_APSS_FIT);
         }
     }
     if constexpr (STAGE == ST_INTENSITY || STAGE == ST_ITER) {
         // APSS wrote t[tc^1]; intensity block, :371-392
-        const uint32_t P = ld_cg(&F.ctl->P);
+        const uint32_t P = global_P(F);
         if (P > 0) {
             tc ^= 1;
             SweepCtx X = X0;
@@ -259,23 +262,25 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         // the kNN filter as a grid phase (knn_kernel's device function); it
         // counts the points prune will keep into ctl->keep (reset by the
         // previous kernel's write-back)
-        const uint32_t P = ld_cg(&F.ctl->P);
+        const uint32_t P = global_P(F);
         if (P > 0) {
             gsync(sm, F, PH_GRAD_R);  // the accepted intensity candidates of every block
-            knn_warps(F, reinterpret_cast<KnnWarpSm*>(sm.u.nbr), P, tc, rc, sc);
+            knn_warps(F, reinterpret_cast<KnnWarpSm*>(sm.u.nbr), ld_cg(&F.ctl->pbase),
+                      ld_cg(&F.ctl->pown), tc, rc, sc);
             gsync(sm, F, PH_KNN);
         }
     }
     if constexpr (STAGE == ST_TAIL || STAGE == ST_ITER) {
         // kNN wrote r[rc^1] (knn_kernel); prune + refresh (:395-397), then
         // the background block (:405-429) and the nll that ends the iteration
-        const uint32_t P = ld_cg(&F.ctl->P);
+        const uint32_t P = global_P(F);
         SweepCtx X = X0;
         if (P > 0) {
             rc ^= 1;
             // the kNN kernel counted the points at r >= r_min: when prune keeps
             // them all the compaction is the identity and the buffers stay
-            if (ld_cg(&F.ctl->keep) != P) {
+            // (row bands always compact: the count is per band)
+            if (F.nbands > 1 || ld_cg(&F.ctl->keep) != P) {
                 phase_prune_a(F, sm, rc, sc);
                 gsync(sm, F, PH_PRUNE_A);
                 phase_prune_b(F, sm, tc, rc, sc);
@@ -321,13 +326,16 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         X.apply_floor = 1;
         // t unchanged since GRAD_R (APSS output): mass_in_gate is cached,
         // unless the cloud was empty (no GRAD_R ran)
-        X.mig_cached = ld_cg(&F.ctl->P) > 0 ? 1 : 0;
+        X.mig_cached = global_P(F) > 0 ? 1 : 0;
         tree_sweep_g<K_GRAD_T, G>(F, sm, X, OP_GRAD_T_END, it);
         stamp(F, PH_GRAD_T);
         // the next iteration's depth block (skipped by the stop rule)
         if (F.cfg.fuse_depth && it + 1 < F.cfg.max_iters && !sm.c.stop)
             tc = depth_block<G>(F, sm, it + 1, tc, rc, bc, sc);
     }
+    // row bands: every band's writes of this stage (the accepted candidates
+    // included) are complete before any band's next kernel reads its halo
+    if (F.nbands > 1) gsync(sm, F, PH_LAUNCH);
     if (leader && !sm.aborted) {
         // the controller replica back to F.ctl for the next kernel and the host
         Ctl* c = F.ctl;
@@ -343,6 +351,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         c->alpha = sm.c.alpha;
         c->cmax = sm.c.cmax;
         c->keep = 0;  // the next kNN pass counts from zero
+        c->P = global_P(F);  // (row bands: all bands' points, from barc)
         F.ctl->tc = tc;
         F.ctl->rc = rc;
         F.ctl->bc = bc;

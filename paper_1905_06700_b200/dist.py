@@ -57,6 +57,69 @@ def combine_band_sums(sums: Sequence[float], sizes: Sequence[int]) -> float:
     return vals[0] if vals else 0.0
 
 
+def halo_ranges(bounds: Sequence[Tuple[int, int]], rank: int, halo_px: int, npix: int):
+    """The pixel ranges rank reads from its neighbours before APSS and kNN
+    (halo_kernel, rt3d.cu): [(neighbour, lo, hi)], halo_px = halo rows x cols."""
+    lo, hi = bounds[rank]
+    out = []
+    if rank > 0:
+        out.append((rank - 1, max(lo - halo_px, 0), lo))
+    if rank + 1 < len(bounds):
+        out.append((rank + 1, hi, min(hi + halo_px, npix)))
+    return out
+
+
+def exchange_halos(bo, values: dict, bounds, rank: int, halo_px: int):
+    """Host mirror of halo_kernel over torch.distributed point-to-point
+    (gloo on CPU): every band keeps full-size arrays in the global index
+    space; it receives its neighbours' halo pixels' bucket offsets `bo`
+    (npix + 1) and, for their points, each array in `values`, at the same
+    indices.  Both sides derive the point ranges from the sender's offsets,
+    so a band first receives the offsets, then the point slices."""
+    import torch
+    import torch.distributed as dist
+    npix = len(bo) - 1
+    me = halo_ranges(bounds, rank, halo_px, npix)
+    ops = []
+    # what my neighbours read from me (their halo ranges inside my band)
+    sends = []
+    for nb in (rank - 1, rank + 1):
+        if 0 <= nb < len(bounds):
+            for owner, a, b in halo_ranges(bounds, nb, halo_px, npix):
+                if owner == rank:
+                    sends.append((nb, a, b))
+    for nb, a, b in sends:
+        ops.append(dist.isend(torch.from_numpy(bo[a:b + 1].copy()), nb))
+    recvd = []
+    for owner, a, b in me:
+        buf = torch.empty(b - a + 1, dtype=torch.from_numpy(bo[:1]).dtype)
+        ops.append(dist.irecv(buf, owner))
+        recvd.append((owner, a, b, buf))
+    for op in ops:
+        op.wait()
+    ops = []
+    for owner, a, b, buf in recvd:
+        if owner < rank:
+            bo[a:b] = buf.numpy()[:-1]      # bo[lo] is ours
+        else:
+            bo[a + 1:b + 1] = buf.numpy()[1:]
+    for nb, a, b in sends:
+        n0, n1 = int(bo[a]), int(bo[b])
+        for k in sorted(values):
+            ops.append(dist.isend(torch.from_numpy(values[k][n0:n1].copy()), nb))
+    pending = []
+    for owner, a, b, _ in recvd:
+        n0, n1 = int(bo[a]), int(bo[b])
+        for k in sorted(values):
+            buf = torch.empty(n1 - n0, dtype=torch.from_numpy(values[k][:1]).dtype)
+            ops.append(dist.irecv(buf, owner))
+            pending.append((k, n0, n1, buf))
+    for op in ops:
+        op.wait()
+    for k, n0, n1, buf in pending:
+        values[k][n0:n1] = buf.numpy()
+
+
 def env_rank() -> Tuple[int, int, int]:
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))

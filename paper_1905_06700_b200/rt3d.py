@@ -66,6 +66,10 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_set_cube_spcb", _st, [SS, C.c_void_p, _u64])
     _bind(L, "rt3d_reconstruct", _st, [SS, P(ReconConfig)])
     _bind(L, "rt3d_reconstruct_batch", _st, [P(SS), _i32, P(ReconConfig)])
+    _bind(L, "rt3d_reconstruct_bands", _st, [P(SS), _i32, P(ReconConfig)])
+    _bind(L, "rt3d_band_pixels", _st, [SS, P(C.c_uint32), P(C.c_uint32)])
+    _bind(L, "rt3d_band_plan", _st, [C.c_uint32, C.c_uint32, _i32, _dbl, _dbl, _i32,
+                                     P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)])
     _bind(L, "rt3d_frame_submit", _st, [SS, P(Cube), P(ReconConfig), P(_u64)])
     _bind(L, "rt3d_frame_collect", _st, [SS, _u64, P(Point), _u64, P(_u64), P(_dbl), P(Report)])
     _bind(L, "rt3d_report_info", _st, [SS, P(Report)])
@@ -109,7 +113,9 @@ EXPORTED = [
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
-    "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
+    "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_reconstruct_bands", "rt3d_band_pixels",
+    "rt3d_band_plan",
+    "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
     "rt3d_grad_intensity", "rt3d_grad_background", "rt3d_block_curvatures", "rt3d_palm_step",
@@ -117,6 +123,17 @@ EXPORTED = [
     "rt3d_evaluate", "rt3d_encode_ply", "rt3d_encode_background_csv",
     "rt3d_simulate_cube", "rt3d_cube_copy",
 ]
+
+
+def band_plan(rows: int, cols: int, superres: int, pixel_pitch: float, apss_radius: float, n: int):
+    """rt3d_band_plan (host only): ([(begin, end)] pixel ranges of the n row
+    bands, halo rows read on either side)."""
+    b = (C.c_uint32 * n)()
+    e = (C.c_uint32 * n)()
+    h = C.c_uint32()
+    _check(lib().rt3d_band_plan(rows, cols, superres, pixel_pitch, apss_radius, n, b, e,
+                                C.byref(h)))
+    return [(int(b[k]), int(e[k])) for k in range(n)], int(h.value)
 
 
 def _two_call(fn, *args) -> bytes:
@@ -222,6 +239,28 @@ class Session:
         c = cfg.to_c()
         sessions[0]._cfg_c = c
         _check(lib().rt3d_reconstruct_batch(arr, len(sessions), C.byref(c)))
+
+    @staticmethod
+    def reconstruct_bands(sessions, cfg: Config) -> dict:
+        """rt3d_reconstruct_bands: one frame split into len(sessions) row
+        bands (every session holds the same sensor and cube); returns the
+        frame's cloud (the bands' clouds in order), background and report."""
+        arr = (C.c_void_p * len(sessions))(*[s.h for s in sessions])
+        c = cfg.to_c()
+        _check(lib().rt3d_reconstruct_bands(arr, len(sessions), C.byref(c)))
+        rep = sessions[0].report()
+        parts, bg = [], None
+        for s in sessions:
+            pts, b = s.state()
+            a, z = C.c_uint32(), C.c_uint32()
+            _check(lib().rt3d_band_pixels(s.h, C.byref(a), C.byref(z)))
+            if bg is None:
+                bg = np.zeros_like(b)
+            bg[a.value:z.value] = b[a.value:z.value]
+            parts.append(pts)
+        rep["points"] = np.concatenate(parts) if parts else np.zeros(0, POINT_DTYPE)
+        rep["background"] = bg
+        return rep
 
     @property
     def stream_ptr(self) -> int:
