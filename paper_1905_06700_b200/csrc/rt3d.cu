@@ -42,7 +42,10 @@ StageFn stage_fn_g1(int st);
 
 #define BATCH_FRAME(FB) (FB).f[(FB).n == 1 ? 0u : (FB).first + blockIdx.x / (FB).bpf]
 
-__global__ void __launch_bounds__(kNbrBlock, 4) apss_kernel(const __grid_constant__ FrameBatch FB) {
+#ifndef RT3D_APSS_MIN_BLOCKS
+#define RT3D_APSS_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kNbrBlock, RT3D_APSS_MIN_BLOCKS) apss_kernel(const __grid_constant__ FrameBatch FB) {
     const Frame& F = BATCH_FRAME(FB);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
@@ -114,26 +117,104 @@ __global__ void halo_kernel(const __grid_constant__ FrameBatch FB, int what) {
 }
 
 // ---------------------------------------------------------------------------
-// Operators on arbitrary clouds (denoise.hpp:159-248): neighbour sets by
-// brute force in ascending index order (identical to SpatialIndex::query's
-// sorted ball, spatial_index.hpp:31-47).
+// Operators on arbitrary clouds (denoise.hpp:159-248) through a device
+// SpatialIndex (spatial_index.hpp:18-77): the index cloud sorted by the
+// reference's cell key (cell = the index's cell size, 21-bit packing), stably
+// so a cell's points stay in ascending index order, plus the sorted unique
+// keys and their start slots.  A query visits the 27 cells around q, merges
+// their (ascending) slot runs by point index and keeps |q - p|^2 <= r^2: the
+// ball in ascending index order, SpatialIndex::query's answer.
 // ---------------------------------------------------------------------------
 struct CloudSoA {
-    const double* x;
+    const double* x;  // sorted slot order
     const double* y;
     const double* z;
     const double* r;
     uint32_t n;
+    const uint32_t* order;         // slot -> point index
+    const unsigned long long* ukey;  // ncell sorted unique cell keys
+    const uint32_t* ustart;        // ncell + 1 slot starts
+    uint32_t ncell;
+    double cell;
 };
 
+__host__ __device__ __forceinline__ unsigned long long cell_pack(long long x, long long y, long long z) {
+    auto u = [](long long v) {
+        return (unsigned long long)(v + (1ll << 20)) & ((1ull << 21) - 1);
+    };
+    return (u(x) << 42) | (u(y) << 21) | u(z);
+}
+__device__ __forceinline__ long long cell_coord(double v, double cell) {
+    return (long long)floor(v / cell);
+}
+
 template <typename Fn>
-__device__ __forceinline__ void for_each_brute(const CloudSoA& c, const Pos& q, double r2, Fn fn) {
-    for (uint32_t m = 0; m < c.n; ++m) {
-        Pos o{c.x[m], c.y[m], c.z[m]};
+__device__ __forceinline__ void for_each_grid(const CloudSoA& c, const Pos& q, double r2, Fn fn) {
+    uint32_t b[27], e[27];
+    const long long cx = cell_coord(q.x, c.cell), cy = cell_coord(q.y, c.cell),
+                    cz = cell_coord(q.z, c.cell);
+    int nr = 0;
+    for (long long a = cx - 1; a <= cx + 1; ++a)
+        for (long long bb = cy - 1; bb <= cy + 1; ++bb)
+            for (long long cc = cz - 1; cc <= cz + 1; ++cc) {
+                const unsigned long long k = cell_pack(a, bb, cc);
+                uint32_t lo = 0, hi = c.ncell;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    if (c.ukey[mid] < k) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < c.ncell && c.ukey[lo] == k) {
+                    b[nr] = c.ustart[lo];
+                    e[nr] = c.ustart[lo + 1];
+                    ++nr;
+                }
+            }
+    for (;;) {  // merge the runs by point index
+        int best = -1;
+        uint32_t bi = 0xffffffffu;
+        for (int t = 0; t < nr; ++t)
+            if (b[t] < e[t] && c.order[b[t]] < bi) {
+                bi = c.order[b[t]];
+                best = t;
+            }
+        if (best < 0) break;
+        const uint32_t slot = b[best]++;
+        Pos o{c.x[slot], c.y[slot], c.z[slot]};
         const double dx = o.x - q.x, dy = o.y - q.y, dz = o.z - q.z;
         const double d2 = dx * dx + dy * dy + dz * dz;
-        if (d2 <= r2) fn(m, o, d2);
+        if (d2 <= r2) fn(bi, o, d2);
     }
+}
+
+// the grid: keys, then (after the sort) run starts and the slot-ordered SoA
+__global__ void grid_keys_kernel(const rt3d_point* in, uint32_t n, double cell,
+                                 unsigned long long* key, uint32_t* idx) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    key[k] = cell_pack(cell_coord(in[k].x, cell), cell_coord(in[k].y, cell), cell_coord(in[k].z, cell));
+    idx[k] = k;
+}
+__global__ void grid_flags_kernel(const unsigned long long* key, uint32_t n, uint32_t* flag) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) flag[k] = (k == 0 || key[k] != key[k - 1]) ? 1u : 0u;
+}
+__global__ void grid_fill_kernel(const rt3d_point* in, const unsigned long long* key,
+                                 const uint32_t* order, const uint32_t* flag, const uint32_t* pos,
+                                 uint32_t n, unsigned long long* ukey, uint32_t* ustart, double* x,
+                                 double* y, double* z, double* r) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    if (flag[k]) {
+        ukey[pos[k]] = key[k];
+        ustart[pos[k]] = k;
+    }
+    if (k == n - 1) ustart[pos[k] + flag[k]] = n;
+    const rt3d_point p = in[order[k]];
+    x[k] = p.x;
+    y[k] = p.y;
+    z[k] = p.z;
+    r[k] = p.intensity;
 }
 
 __global__ void apss_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA idx, double R,
@@ -144,7 +225,7 @@ __global__ void apss_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA i
     Pos q{p.x, p.y, p.z};
     uint8_t fl = p.flags & (uint8_t)~(1u | 4u);
     Pos o;
-    auto each = [&](double r2, auto fn) { for_each_brute(idx, q, r2, fn); };
+    auto each = [&](double r2, auto fn) { for_each_grid(idx, q, r2, fn); };
     if (apss_point(each, q, R, min_nbrs, eps, fl, o)) {
         p.x = o.x;
         p.y = o.y;
@@ -155,14 +236,14 @@ __global__ void apss_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA i
 }
 
 __global__ void knn_general_kernel(const rt3d_point* in, uint32_t n, CloudSoA idx, int kk,
-                                   double radius, rt3d_point* out) {
+                                   double radius, const rt3d_point* index_aos, rt3d_point* out) {
     uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     rt3d_point p = in[k];
     Pos q{p.x, p.y, p.z};
-    auto each = [&](double r2, auto fn) { for_each_brute(idx, q, r2, fn); };
+    auto each = [&](double r2, auto fn) { for_each_grid(idx, q, r2, fn); };
     p.intensity = knn_mean(each, kk, radius * radius, p.intensity,
-                           [&](uint32_t m) { return idx.r[m]; });
+                           [&](uint32_t m) { return index_aos[m].intensity; });
     out[k] = p;
 }
 
@@ -176,35 +257,18 @@ __global__ void split_cloud_kernel(const rt3d_point* in, uint32_t n, double* x, 
     r[k] = in[k].intensity;
 }
 
-// prune on an arbitrary cloud: keep flags + per-block counts, then scatter
-__global__ void prune_count_kernel(const rt3d_point* in, uint32_t n, double rmin, uint32_t* bcnt) {
-    __shared__ unsigned int c;
-    if (threadIdx.x == 0) c = 0;
-    __syncthreads();
-    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < n && in[k].intensity >= rmin) atomicAdd(&c, 1u);
-    __syncthreads();
-    if (threadIdx.x == 0) bcnt[blockIdx.x] = c;
+// prune on an arbitrary cloud (denoise.hpp:241-248): keep flags, an
+// exclusive scan (CUB), a stable scatter
+__global__ void prune_flags_kernel(const rt3d_point* in, uint32_t n, double rmin, uint32_t* flag) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) flag[k] = in[k].intensity >= rmin ? 1u : 0u;
 }
-
-__global__ void prune_scatter_kernel(const rt3d_point* in, uint32_t n, double rmin,
-                                     const uint32_t* bcnt, rt3d_point* out, uint32_t* total) {
-    __shared__ unsigned int base;
-    __shared__ unsigned int keep[kBlock];
-    if (threadIdx.x == 0) {
-        unsigned int s = 0;
-        for (uint32_t b = 0; b < blockIdx.x; ++b) s += bcnt[b];
-        base = s;
-        if (blockIdx.x == gridDim.x - 1) *total = s + bcnt[blockIdx.x];
-    }
-    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    keep[threadIdx.x] = (k < n && in[k].intensity >= rmin) ? 1u : 0u;
-    __syncthreads();
-    if (keep[threadIdx.x]) {
-        unsigned int o = base;
-        for (unsigned int q = 0; q < threadIdx.x; ++q) o += keep[q];
-        out[o] = in[k];
-    }
+__global__ void prune_scatter_kernel(const rt3d_point* in, uint32_t n, const uint32_t* flag,
+                                     const uint32_t* pos, rt3d_point* out, uint32_t* total) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    if (flag[k]) out[pos[k]] = in[k];
+    if (k == n - 1) *total = pos[k] + flag[k];
 }
 
 __global__ void fft_kernel(const double* img, double* out, double* re, double* im, double* re2,
@@ -2298,25 +2362,72 @@ rt3d_status rt3d_matched_filter_peaks(rt3d_session* s, const rt3d_event* events,
 }
 
 // ---- arbitrary-cloud operators --------------------------------------------
-static rt3d_status upload_cloud_soa(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
-                                    DevBuf& aos, CloudSoA& soa, DevBuf& soabuf) {
+// The device SpatialIndex of an index cloud (see for_each_grid): upload,
+// cell keys, a stable radix sort of (key, index), run starts, the SoA in slot
+// order.  `aos` keeps the index cloud in point order.
+struct GridBufs {
+    DevBuf aos, keys, idx, flag, pos, ukey, ustart, soa, tmp;
+};
+static rt3d_status build_grid(rt3d_session* s, const rt3d_point* cloud, uint64_t n, double cell,
+                              GridBufs& g, CloudSoA& c) {
+    const size_t nn = std::max<uint64_t>(n, 1);
+    CUDA_TRY(g.aos.ensure(nn * sizeof(rt3d_point)));
+    CUDA_TRY(g.keys.ensure(2 * nn * 8));
+    CUDA_TRY(g.idx.ensure(2 * nn * 4));
+    CUDA_TRY(g.flag.ensure(nn * 4));
+    CUDA_TRY(g.pos.ensure(nn * 4));
+    CUDA_TRY(g.ukey.ensure(nn * 8));
+    CUDA_TRY(g.ustart.ensure((nn + 1) * 4));
+    CUDA_TRY(g.soa.ensure(nn * 32));
+    std::memset(&c, 0, sizeof c);
+    c.cell = cell;
+    c.n = (uint32_t)n;
+    double* base = g.soa.as<double>();
+    c.x = base;
+    c.y = base + nn;
+    c.z = base + 2 * nn;
+    c.r = base + 3 * nn;
+    c.ukey = g.ukey.as<unsigned long long>();
+    c.ustart = g.ustart.as<uint32_t>();
+    if (!n) return RT3D_OK;
+    CUDA_TRY(cudaMemcpyAsync(g.aos.p, cloud, n * sizeof(rt3d_point), cudaMemcpyHostToDevice, s->stream));
+    unsigned long long* k0 = g.keys.as<unsigned long long>();
+    uint32_t* i0 = g.idx.as<uint32_t>();
+    const uint32_t nb = (uint32_t)((n + 255) / 256);
+    grid_keys_kernel<<<nb, 256, 0, s->stream>>>(g.aos.as<rt3d_point>(), (uint32_t)n, cell, k0, i0);
+    CUDA_TRY(cudaGetLastError());
+    cub::DoubleBuffer<unsigned long long> kb(k0, k0 + nn);
+    cub::DoubleBuffer<uint32_t> vb(i0, i0 + nn);
+    size_t tb = 0, ts = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, kb, vb, (int)n, 0, 64, s->stream));
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, ts, g.flag.as<uint32_t>(), g.pos.as<uint32_t>(),
+                                           (int)n, s->stream));
+    CUDA_TRY(g.tmp.ensure(std::max(tb, ts)));
+    tb = ts = g.tmp.cap;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(g.tmp.p, tb, kb, vb, (int)n, 0, 64, s->stream));
+    grid_flags_kernel<<<nb, 256, 0, s->stream>>>(kb.Current(), (uint32_t)n, g.flag.as<uint32_t>());
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(g.tmp.p, ts, g.flag.as<uint32_t>(), g.pos.as<uint32_t>(),
+                                           (int)n, s->stream));
+    grid_fill_kernel<<<nb, 256, 0, s->stream>>>(
+        g.aos.as<rt3d_point>(), kb.Current(), vb.Current(), g.flag.as<uint32_t>(),
+        g.pos.as<uint32_t>(), (uint32_t)n, g.ukey.as<unsigned long long>(), g.ustart.as<uint32_t>(),
+        (double*)c.x, (double*)c.y, (double*)c.z, (double*)c.r);
+    CUDA_TRY(cudaGetLastError());
+    c.order = vb.Current();
+    uint32_t last_pos = 0, last_flag = 0;
+    CUDA_TRY(cudaMemcpyAsync(&last_pos, g.pos.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaMemcpyAsync(&last_flag, g.flag.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    c.ncell = last_pos + last_flag;
+    return RT3D_OK;
+}
+
+static rt3d_status upload_points(rt3d_session* s, const rt3d_point* cloud, uint64_t n, DevBuf& aos) {
     CUDA_TRY(aos.ensure(std::max<uint64_t>(n, 1) * sizeof(rt3d_point)));
     if (n)
         CUDA_TRY(cudaMemcpyAsync(aos.p, cloud, n * sizeof(rt3d_point), cudaMemcpyHostToDevice,
                                  s->stream));
-    CUDA_TRY(soabuf.ensure(std::max<uint64_t>(n, 1) * 32));
-    double* base = soabuf.as<double>();
-    soa.x = base;
-    soa.y = base + n;
-    soa.z = base + 2 * n;
-    soa.r = base + 3 * n;
-    soa.n = (uint32_t)n;
-    if (n) {
-        split_cloud_kernel<<<(n + 255) / 256, 256, 0, s->stream>>>(
-            aos.as<rt3d_point>(), (uint32_t)n, (double*)soa.x, (double*)soa.y, (double*)soa.z,
-            (double*)soa.r);
-        CUDA_TRY(cudaGetLastError());
-    }
     return RT3D_OK;
 }
 
@@ -2338,11 +2449,11 @@ rt3d_status rt3d_apss_project(rt3d_session* s, const rt3d_point* cloud, uint64_t
     if (n >= (1ull << 32) || n_index >= (1ull << 32))
         return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
     if (!n) return RT3D_OK;
-    CloudSoA idx, dummy;
+    CloudSoA idx;
     DevBuf& aos_in = s->misc;
-    static thread_local DevBuf idx_aos, idx_soa, tmp_soa;
-    if ((st = upload_cloud_soa(s, index_cloud, n_index, idx_aos, idx, idx_soa))) return st;
-    if ((st = upload_cloud_soa(s, cloud, n, aos_in, dummy, tmp_soa))) return st;
+    static thread_local GridBufs grid;
+    if ((st = build_grid(s, index_cloud, n_index, cell, grid, idx))) return st;
+    if ((st = upload_points(s, cloud, n, aos_in))) return st;
     CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point)));
     apss_general_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(
         aos_in.as<rt3d_point>(), (uint32_t)n, idx, prm->kernel_radius, prm->min_neighbors,
@@ -2368,13 +2479,14 @@ rt3d_status rt3d_knn_intensity_filter(rt3d_session* s, const rt3d_point* cloud, 
     if (n >= (1ull << 32) || n_index >= (1ull << 32))
         return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
     if (!n) return RT3D_OK;
-    CloudSoA idx, dummy;
-    static thread_local DevBuf idx_aos, idx_soa, tmp_soa;
-    if ((st = upload_cloud_soa(s, index_cloud, n_index, idx_aos, idx, idx_soa))) return st;
-    if ((st = upload_cloud_soa(s, cloud, n, s->misc, dummy, tmp_soa))) return st;
+    CloudSoA idx;
+    static thread_local GridBufs grid;
+    if ((st = build_grid(s, index_cloud, n_index, cell, grid, idx))) return st;
+    if ((st = upload_points(s, cloud, n, s->misc))) return st;
     CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point)));
     knn_general_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(
-        s->misc.as<rt3d_point>(), (uint32_t)n, idx, k, radius, s->outpts.as<rt3d_point>());
+        s->misc.as<rt3d_point>(), (uint32_t)n, idx, k, radius, grid.aos.as<rt3d_point>(),
+        s->outpts.as<rt3d_point>());
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out, s->outpts.p, n * sizeof(rt3d_point), cudaMemcpyDeviceToHost,
                              s->stream));
@@ -2391,18 +2503,24 @@ rt3d_status rt3d_prune(rt3d_session* s, const rt3d_point* cloud, uint64_t n, dou
     *n_out = 0;
     if (!n) return RT3D_OK;
     if (n >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: cloud too large");
-    const uint32_t blocks = (uint32_t)((n + kBlock - 1) / kBlock);
     CUDA_TRY(s->misc.ensure(n * sizeof(rt3d_point)));
-    CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point) + 4 * blocks + 64));
+    CUDA_TRY(s->outpts.ensure(n * sizeof(rt3d_point)));
     CUDA_TRY(cudaMemcpyAsync(s->misc.p, cloud, n * sizeof(rt3d_point), cudaMemcpyHostToDevice, s->stream));
-    static thread_local DevBuf cnts;
-    CUDA_TRY(cnts.ensure(4 * blocks + 16));
-    uint32_t* total = cnts.as<uint32_t>() + blocks;
-    prune_count_kernel<<<blocks, kBlock, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, r_min,
-                                                         cnts.as<uint32_t>());
-    prune_scatter_kernel<<<blocks, kBlock, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, r_min,
-                                                           cnts.as<uint32_t>(),
-                                                           s->outpts.as<rt3d_point>(), total);
+    static thread_local DevBuf flags, tmp;
+    CUDA_TRY(flags.ensure(8 * n + 16));
+    uint32_t* flag = flags.as<uint32_t>();
+    uint32_t* pos = flag + n;
+    uint32_t* total = pos + n;
+    const uint32_t nb = (uint32_t)((n + 255) / 256);
+    prune_flags_kernel<<<nb, 256, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, r_min, flag);
+    CUDA_TRY(cudaGetLastError());
+    size_t tb = 0;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, pos, (int)n, s->stream));
+    CUDA_TRY(tmp.ensure(tb));
+    tb = tmp.cap;
+    CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag, pos, (int)n, s->stream));
+    prune_scatter_kernel<<<nb, 256, 0, s->stream>>>(s->misc.as<rt3d_point>(), (uint32_t)n, flag, pos,
+                                                    s->outpts.as<rt3d_point>(), total);
     CUDA_TRY(cudaGetLastError());
     uint32_t h_total = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_total, total, 4, cudaMemcpyDeviceToHost, s->stream));
