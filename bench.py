@@ -193,10 +193,8 @@ def load_measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-B200_FP64_NOMINAL_TFLOPS = 37.0  # NVIDIA B200 datasheet (vector FP64); not measured here
-
-
-def apss_fp64(points, radius: float, us_per_launch: float, frames: int = 1):
+def apss_fp64(points, radius: float, us_per_launch: float, frames: int = 1,
+              peak_tflops: float = None):
     """The APSS kernel against the FP64 roof: ~70 flop per
     (point, neighbour) pair for distance, weight, mean, covariance and the
     Pratt moments, plus ~3000 flop per point for the 3x3 and 5x5 eigensolves.
@@ -213,12 +211,13 @@ def apss_fp64(points, radius: float, us_per_launch: float, frames: int = 1):
     nbrs = cKDTree(xyz).query_ball_point(xyz, radius, return_length=True)
     flops = frames * (70.0 * float(np.sum(nbrs)) + 3000.0 * len(points))
     achieved = flops / (us_per_launch * 1e-6) / 1e12
-    return {"achieved": achieved, "unit": "TFLOP/s", "peak": B200_FP64_NOMINAL_TFLOPS,
-            "frac": achieved / B200_FP64_NOMINAL_TFLOPS, "flops_per_launch": flops,
+    return {"achieved": achieved, "unit": "TFLOP/s", "peak": peak_tflops,
+            "frac": achieved / peak_tflops, "flops_per_launch": flops,
             "mean_neighbours": float(np.mean(nbrs)),
-            "peak_source": "nominal B200 FP64 (datasheet), not measured",
-            "note": "APSS is FP64-issue-bound at this size; the HBM fraction above is "
-                    "~0 because its working set stays in L2"}
+            "peak_source": "measured in this run: rt3d_measure_fp64_peak (DFMA chains, "
+                           "full device, best of 5)",
+            "note": "APSS is FP64-issue-bound; its HBM fraction is ~0 because its working "
+                    "set stays in L2"}
 
 
 def ncu_traffic_per_launch(cls: str):
@@ -299,6 +298,62 @@ def run_reference_arm(args, world, rank):
     return 0
 
 
+def large_array_leg(local: int, frames: int = 3) -> dict:
+    """Config E (1024x1024 px x 2048 bins, ~68M events, 548 MB
+    of CSR events, HBM-resident) on one GPU: ms/frame, and per kernel class
+    the algorithmic bytes per launch (class_bytes) over the CUDA-event launch
+    time.  The likelihood sweeps (stage kernels) are the north star's
+    'gradient kernels' measured where HBM binds."""
+    import torch
+    from paper_1905_06700_b200.rt3d import Session
+    from scenegen.scene import simulate
+    name, spec, seed, cfg = workloads.config_e()
+    t0 = time.perf_counter()
+    sc = simulate(spec, seed)
+    sim_s = time.perf_counter() - t0
+    out = {"workload": name, "pixels": sc.n_pixels, "bins": sc.n_bins,
+           "events": int(len(sc.events)), "event_bytes": int(len(sc.events)) * 8,
+           "palm_iterations": cfg.max_iters, "host_simulate_s": sim_s}
+    with Session(local) as s:
+        s.set_scene(sc)
+        s.reconstruct_async(cfg)
+        s.synchronize()
+        stream = torch.cuda.ExternalStream(s.stream_ptr, device=torch.device("cuda", local))
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(frames)]
+        with torch.cuda.stream(stream):
+            for a, b in evs:
+                a.record(stream)
+                s.reconstruct_async(cfg)
+                b.record(stream)
+        stream.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        rep = s.report()
+        s.time_kernels(True)
+        s.reconstruct_async(cfg)
+        kt = s.kernel_times()
+        s.time_kernels(False)
+    cb = class_bytes(sc, rep, fused_depth=kt["stage_depth"][1] == 0)
+    peak, src = load_measured_peaks()
+    classes = {}
+    for cls, (kms, n) in kt.items():
+        if not n:
+            continue
+        per = cb[cls] / n
+        gbs = per / (kms / n) / 1e6
+        classes[cls] = {"ms_per_frame": kms, "launches": n, "us_per_launch": 1e3 * kms / n,
+                        "algorithmic_bytes_per_launch": per, "gbs": gbs, "hbm_frac": gbs / peak}
+    out.update({"ms_per_frame": statistics.mean(ms), "frames_per_s": 1e3 / statistics.mean(ms),
+                "points_final": int(rep["points"]), "kernel_classes": classes,
+                "sweep_roofline": {"kernel": KERNEL_NAMES["stage_tail"], "bound": "hbm",
+                                   "achieved": classes["stage_tail"]["gbs"], "peak": peak,
+                                   "unit": "GB/s", "frac": classes["stage_tail"]["hbm_frac"],
+                                   "peak_source": src},
+                "note": "frames measured with CUDA events on the session stream, inputs "
+                        "resident; the working set (548 MB of events) exceeds L2"})
+    return out
+
+
 def parity_block(sess, sc, cfg, ref_cloud, gpu_cloud) -> dict:
     """bench-time parity at the benchmarked workload (tests/parity.py): the
     GPU cloud of the timed frames against the reference's own cloud from the
@@ -335,6 +390,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
     ap.add_argument("--batch", type=int, default=8,
                     help="frames per step (rt3d_reconstruct_batch), 1..8")
     args = ap.parse_args()
@@ -403,6 +459,7 @@ def main():
     timed_ms = timed(run_batch, K)
     ktimes = sess.kernel_times()
     sess.time_kernels(False)
+    fp64_peak = sess.measure_fp64_peak()
     dev_s = sum(step_ms) / 1e3
     dev_s_max = barrier_max(dev_s, world, local)
     value = world * K * NB / dev_s_max
@@ -486,6 +543,9 @@ def main():
                          "reference headers compiled unchanged (oracle/_ref), all host threads"}
         if not args.no_parity:
             parity = parity_block(sess, sc, cfg, ref_cloud, pts)
+    large = None
+    if rank == 0 and world == 1 and not args.no_large:
+        large = large_array_leg(local)
 
     if rank == 0:
         line = {
@@ -537,8 +597,10 @@ def main():
             line["cpu_baseline"] = cpu
         if parity:
             line["parity"] = parity
+        if large:
+            line["large_array"] = large
         if dom == "apss":
-            fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"], NB)
+            fp = apss_fp64(pts, cfg.apss_radius, dc["us_per_launch"], NB, fp64_peak)
             if fp:
                 line["roofline"]["fp64"] = fp
         print(json.dumps(line), flush=True)

@@ -208,6 +208,9 @@ void* rt3d_session_stream(rt3d_session* s);
  * pairs of the last launch.  Off by default (bench.py's breakdown only). */
 rt3d_status rt3d_session_profile(rt3d_session* s, int enable);
 rt3d_status rt3d_profile_copy(rt3d_session* s, uint64_t* pairs, uint32_t cap, uint32_t* n);
+/* Measured FP64 vector throughput of the session's device (DFMA chains,
+ * best of 5, TFLOP/s): the roof the bench reports FP64-bound kernels against. */
+rt3d_status rt3d_measure_fp64_peak(rt3d_session* s, double* tflops);
 /* Kernel-class timing: with it enabled every launch of a frame is bracketed
  * by CUDA events recorded on the session stream; rt3d_kernel_times
  * synchronizes and returns the summed milliseconds and launch counts per

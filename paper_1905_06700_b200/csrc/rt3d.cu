@@ -105,6 +105,7 @@ __global__ void halo_kernel(const __grid_constant__ FrameBatch FB, int what) {
                 obo[p] = ld_cg(&nbo[p]);
             }
         const uint32_t n0 = ld_cg(&nbo[p0]), n1 = ld_cg(&nbo[p1]);
+        RT3D_CHECK(n0 <= n1 && n1 <= F.pcap && p1 <= F.npix);
         for (uint32_t n = n0 + tid; n < n1; n += nth) {
             F.t[tc][n] = ld_cg(&N.t[tc][n]);
             if (what & 2) F.r[rc][n] = ld_cg(&N.r[rc][n]);
@@ -114,6 +115,21 @@ __global__ void halo_kernel(const __grid_constant__ FrameBatch FB, int what) {
             }
         }
     }
+}
+
+// FP64 vector throughput probe (the roof of the FP64-issue-bound kernels,
+// rt3d_measure_fp64_peak): 8 independent DFMA chains per thread.
+__global__ void fp64_peak_kernel(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = 1e-3 * (threadIdx.x + k);
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __fma_rn(x[k], a, b);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += x[k];
+    if (acc == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = acc;  // keeps the chains live
 }
 
 // ---------------------------------------------------------------------------
@@ -674,6 +690,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     while (s->lam_cap < s->n_events) s->lam_cap = s->lam_cap ? 2 * s->lam_cap : 4096;
     CUDA_TRY(s->lam.ensure(std::max<uint64_t>(s->lam_cap, 1) * 32));
     F.nev = s->lam_cap;
+    F.pcap = (uint32_t)std::min<size_t>(s->pcap, 0xffffffffu);
     CUDA_TRY(s->blk.ensure((size_t)F.nbn * 8));
     CUDA_TRY(s->tblk.ensure((size_t)npix * 32 + 64));
     CUDA_TRY(s->tbmax.ensure((size_t)npix * 16 + 64));
@@ -1328,6 +1345,28 @@ void* rt3d_debug_buffer(rt3d_session* s) {
         return nullptr;
     cudaStreamSynchronize(s->side);
     return (void*)s->h_dbg;
+}
+
+rt3d_status rt3d_measure_fp64_peak(rt3d_session* s, double* tflops) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!tflops) return fail(RT3D_ERR_INVALID_ARGUMENT, "null output");
+    const int blocks = s->nsm * 16, threads = 128, iters = 1 << 14;
+    CUDA_TRY(s->misc.ensure((size_t)blocks * threads * 8));
+    fp64_peak_kernel<<<blocks, threads, 0, s->stream>>>(s->misc.as<double>(), 64, 0.999, 1e-3);
+    CUDA_TRY(cudaGetLastError());
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        CUDA_TRY(cudaEventRecord(s->ev0, s->stream));
+        fp64_peak_kernel<<<blocks, threads, 0, s->stream>>>(s->misc.as<double>(), iters, 0.999, 1e-3);
+        CUDA_TRY(cudaEventRecord(s->ev1, s->stream));
+        CUDA_TRY(cudaEventSynchronize(s->ev1));
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+        best = std::min(best, ms);
+    }
+    *tflops = 2.0 * 8.0 * iters * (double)blocks * threads / (best * 1e-3) / 1e12;
+    return RT3D_OK;
 }
 
 rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable) {

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "rt3d_math.cuh"
 
@@ -160,6 +161,7 @@ struct Frame {
     int tc0, rc0, bc0, sc0;  // initial buffer toggles
     uint32_t P0;             // initial point count (resident state)
     uint32_t prof_cap;
+    uint32_t pcap;           // point capacity of the state buffers (bounds checks)
     // scratch
     double* mig[2];   // per point mass_in_gate(t) of the current t (see SweepCtx)
     double* gt;
@@ -292,6 +294,25 @@ struct SmemT {
     IrfDev irf0;
     double irf_tab[2 * kIrfSmem];
 };
+
+// Bounds checks of the checked build (make checked: -DRT3D_CHECKS, the
+// librt3d_checked.so the test suite runs under with RT3D_LIB): a violated
+// index bound prints its site and traps, so the test fails with a CUDA error
+// instead of reading or writing out of bounds.  Compiled out otherwise.
+#ifdef RT3D_CHECKS
+#define RT3D_CHECK(cond)                                                                     \
+    do {                                                                                     \
+        if (!(cond)) {                                                                       \
+            printf("rt3d check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,     \
+                   __LINE__, (int)blockIdx.x, (int)threadIdx.x);                             \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define RT3D_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -663,6 +684,7 @@ __device__ void phase_spawn(const Frame& F, SM& sm, bool baseline) {
         F.bo[0][p] = o;
         const int i = (int)(p / F.cols), j = (int)(p % F.cols);
         const uint32_t nt = F.npk[p];
+        RT3D_CHECK(o + F.nval[p] * (uint32_t)(s * s) <= F.pcap && nt <= (uint32_t)K);
         for (uint32_t q = 0; q < nt; ++q) {
             const size_t slot = (size_t)p * K + q;
             const double inten = F.pk_int[slot];
@@ -956,9 +978,11 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
     // ---- meta, lane per pixel
     if ((uint32_t)lane < size) {
         const uint32_t p = lo + lane;
+        RT3D_CHECK(p >= F.bpix0 && p < F.bpix1);
         const uint32_t e0 = F.off[p], e1 = F.off[p + 1];
         const uint32_t* bo = F.bo[X.sc];
         const uint32_t n0 = bo[p], n1 = bo[p + 1];
+        RT3D_CHECK(e0 <= e1 && e1 <= F.off[F.npix] && n0 <= n1 && n1 <= F.pcap);
         const bool dead = F.dead[p] != 0;
         double b;
         if (KIND == K_CAND_B) {
@@ -997,6 +1021,7 @@ __device__ __forceinline__ void sweep_node(const Frame& F, SmemT<G>& sm, const S
         }
         const bool ev_smem = ne <= (uint32_t)kEvc;
         const uint32_t E0 = W.me0[q0], N0 = W.mn0[q0];
+        RT3D_CHECK(npt <= (uint32_t)kPvc && (ev_smem || q1 == q0 + 1));
         if (ev_smem)
             for (uint32_t k = lane; k < ne; k += 32) W.ev[k] = __ldg(&F.ev[E0 + k]);
         const int ncand = ((KIND == K_CAND_T || KIND == K_CAND_R) && X.two) ? 2 : 1;
@@ -1120,10 +1145,12 @@ __device__ __forceinline__ void sweep_node_thread(const Frame& F, SM& sm, const 
     const int lane = threadIdx.x & 31;
     if ((uint32_t)lane >= size) return;
     const uint32_t p = lo + (uint32_t)lane;
+    RT3D_CHECK(p >= F.bpix0 && p < F.bpix1);
     const uint32_t e0 = F.off[p], m = F.off[p + 1] - e0;
     const uint32_t* bo = F.bo[X.sc];
     const uint32_t n0 = bo[p];
     const int np = (int)(bo[p + 1] - n0);
+    RT3D_CHECK(e0 + m <= F.off[F.npix] && n0 + (uint32_t)np <= F.pcap && np <= kThreadPts);
     const bool dead = F.dead[p] != 0;
     const double gain = F.gain[p];
     const double g = dead ? 0.0 : gain;
@@ -2003,6 +2030,7 @@ __device__ void phase_prune_b(const Frame& F, SM& sm, int tc, int rc, int sc) {
     const double rmin = F.cfg.r_min;
     for (uint32_t p = c0 + threadIdx.x; p < c1; p += kBlock) {
         uint32_t o = base + ld_cg(&F.cnt[p]);
+        RT3D_CHECK(o <= F.pcap && bo[p] <= bo[p + 1] && bo[p + 1] <= F.pcap);
         F.bo[sc ^ 1][p] = o;
         for (uint32_t n = bo[p]; n < bo[p + 1]; ++n) {
             const double rv = F.r[rc][n];

@@ -138,6 +138,7 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
     int j = 0;
     auto locate = [&](uint32_t f) -> uint32_t {
         while (rt.pre[j + 1] <= f) ++j;
+        RT3D_CHECK(j < 32 && rt.m0[j] + (f - rt.pre[j]) < F.pcap);
         return rt.m0[j] + (f - rt.pre[j]);
     };
     bool v = (uint32_t)lane < total;
@@ -255,6 +256,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
     uint32_t j = 0;
     for (uint32_t nl = gw; nl < P; nl += nw, ++j) {
         const uint32_t n = pb + nl;
+        RT3D_CHECK(n < F.pcap);
         int fi, fj;
         double tq;
         point(j, fi, fj, tq);
@@ -398,6 +400,7 @@ static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P,
     (void)F.amom_stride;
     for (uint32_t nl = vblock(F) * blockDim.x + threadIdx.x; nl < P; nl += vgrid(F) * blockDim.x) {
         const uint32_t n = pb + nl;
+        RT3D_CHECK(n < F.pcap);
         const int fi = F.fi[sc][n], fj = F.fj[sc][n];
         const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
         uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
@@ -553,6 +556,7 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
     unsigned int kept = 0;
     for (uint32_t nl = gw; nl < P; nl += nw, ++jj) {
         const uint32_t n = pb + nl;
+        RT3D_CHECK(n < F.pcap);
         int fi, fj;
         double tq;
         point(jj, fi, fj, tq);

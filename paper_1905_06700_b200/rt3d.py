@@ -68,6 +68,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_reconstruct_batch", _st, [P(SS), _i32, P(ReconConfig)])
     _bind(L, "rt3d_reconstruct_bands", _st, [P(SS), _i32, P(ReconConfig)])
     _bind(L, "rt3d_band_pixels", _st, [SS, P(C.c_uint32), P(C.c_uint32)])
+    _bind(L, "rt3d_measure_fp64_peak", _st, [SS, P(_dbl)])
     _bind(L, "rt3d_band_plan", _st, [C.c_uint32, C.c_uint32, _i32, _dbl, _dbl, _i32,
                                      P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)])
     _bind(L, "rt3d_frame_submit", _st, [SS, P(Cube), P(ReconConfig), P(_u64)])
@@ -114,7 +115,7 @@ EXPORTED = [
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
     "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_reconstruct_bands", "rt3d_band_pixels",
-    "rt3d_band_plan",
+    "rt3d_band_plan", "rt3d_measure_fp64_peak",
     "rt3d_frame_submit", "rt3d_frame_collect", "rt3d_report_info", "rt3d_report_copy", "rt3d_state_size",
     "rt3d_state_copy", "rt3d_matched_filter_peaks", "rt3d_init_matched_filter",
     "rt3d_baseline_xcorr", "rt3d_state_upload", "rt3d_nll", "rt3d_grad_depth",
@@ -305,6 +306,12 @@ class Session:
 
     def synchronize(self):
         _check(lib().rt3d_session_synchronize(self.h))
+
+    def measure_fp64_peak(self) -> float:
+        """Measured FP64 vector throughput of the device, TFLOP/s."""
+        v = _dbl()
+        _check(lib().rt3d_measure_fp64_peak(self.h, C.byref(v)))
+        return v.value
 
     def set_sharing(self, n_sessions: int):
         """Size the cooperative grids so n sessions can run frames concurrently."""

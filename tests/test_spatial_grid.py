@@ -77,7 +77,7 @@ def test_denoisers_with_a_separate_index_cloud(gpu):
 
 @pytest.mark.parametrize("n", [1, 255, 256, 257, 100000])
 def test_prune_general_cloud(gpu, n):
-    cloud = _cloud(max(n, 20), n)[:n]
+    cloud = _cloud(max(n, 60), n)[:n]
     for r_min in (0.0, 2.5, 6.0):
         got = gpu.prune(cloud, r_min)
         assert np.array_equal(got, cloud[cloud["intensity"] >= r_min])
