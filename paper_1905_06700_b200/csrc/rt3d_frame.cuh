@@ -1218,17 +1218,33 @@ __device__ __forceinline__ void sweep_node_thread(const Frame& F, SM& sm, const 
             for (int q = 0; q < np && q < kThreadPts; ++q) mass += P.r[q] * P.mig[q];
             acc = gain * mass;
         }
-        for (uint32_t k = 0; k < m; ++k) {
-            const uint2 e = __ldg(&ev[k]);
-            const double l = tp_rate(f, g, b, np, P, e.x);
-            const double z = (double)e.y;
-            if (!dead && !inf) {
-                if (l <= 0.0) inf = true;
-                else acc -= (l > 0.0) ? z * log(l) : 0.0;
+        // the pixel's events in groups of 4, the next group's loads issued
+        // before this group's arithmetic (each thread walks its own pixel, so
+        // the loads would otherwise wait one by one)
+        uint2 nxt[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) nxt[j] = (uint32_t)j < m ? __ldg(&ev[j]) : make_uint2(0u, 0u);
+        for (uint32_t k0 = 0; k0 < m; k0 += 4) {
+            uint2 cur[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                cur[j] = nxt[j];
+                nxt[j] = k0 + 4 + j < m ? __ldg(&ev[k0 + 4 + j]) : make_uint2(0u, 0u);
             }
-            if (KIND == K_GRAD_B && l > 0.0) {
-                gbv -= g * z / l;
-                bs += g * g * z / (l * l);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (k0 + j >= m) break;
+                const uint2 e = cur[j];
+                const double l = tp_rate(f, g, b, np, P, e.x);
+                const double z = (double)e.y;
+                if (!dead && !inf) {
+                    if (l <= 0.0) inf = true;
+                    else acc -= (l > 0.0) ? z * log(l) : 0.0;
+                }
+                if (KIND == K_GRAD_B && l > 0.0) {
+                    gbv -= g * z / l;
+                    bs += g * g * z / (l * l);
+                }
             }
         }
         const double part = dead ? 0.0 : (inf ? INFINITY : acc);
