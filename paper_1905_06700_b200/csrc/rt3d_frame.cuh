@@ -446,6 +446,16 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
         InitWarpSm& I = sm.u.init[threadIdx.x >> 5];
         uint32_t C = 0;
         bool listed = true;
+        // Per-lane top-K (sep <= 16, K <= 8): candidate g (in increasing lag
+        // order) belongs to lane g mod 32, so one lane's candidates lie >= 32
+        // lags apart and a taken peak excludes at most one of them (|dlag| <
+        // sep <= 16).  After r rounds a lane has lost at most r candidates, so
+        // its best non-clashing candidate is among its best r + 1 <= K: each
+        // lane keeps its K best (response desc, lag asc) at or above the
+        // threshold, every response is computed once, and the K rounds below
+        // give the reference's greedy picks (reconstruct.hpp:154-170).
+        const bool topk = sep <= 16 && K <= 8;
+        int nl = 0;  // this lane's list length (slots I.lag / I.resp [lane * 8, + K))
         for (uint32_t eb = 0; eb < m; eb += 32) {
             const uint32_t e = eb + lane;
             int lo = 0, hi = -1;
@@ -470,7 +480,7 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
                 if (lane >= o) inc += y;
             }
             const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-            if (C + total > (uint32_t)kInitCap) {
+            if (!topk && C + total > (uint32_t)kInitCap) {
                 listed = false;
                 break;
             }
@@ -479,11 +489,31 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
             if (lane == 31) I.pre[32] = total;
             __syncwarp();
             int j = 0;
-            for (uint32_t c = lane; c < total; c += 32) {
-                while (I.pre[j + 1] <= c) ++j;
-                const int t0 = I.lo[j] + (int)(c - I.pre[j]);
-                I.lag[C + c] = t0;
-                I.resp[C + c] = mf_response(F.ev, e0, m, f, (double)t0);
+            if (topk) {
+                for (uint32_t c = (uint32_t)((lane - (int)C) & 31); c < total; c += 32) {
+                    while (I.pre[j + 1] <= c) ++j;
+                    const int t0 = I.lo[j] + (int)(c - I.pre[j]);
+                    const double rr = mf_response(F.ev, e0, m, f, (double)t0);
+                    if (!(rr >= thr)) continue;
+                    int pos = nl < K ? nl : K;
+                    if (pos == K && !(rr > I.resp[lane * 8 + K - 1])) continue;  // not in the top K
+                    if (nl < K) ++nl;
+                    if (pos == K) pos = K - 1;
+                    while (pos > 0 && rr > I.resp[lane * 8 + pos - 1]) {
+                        I.resp[lane * 8 + pos] = I.resp[lane * 8 + pos - 1];
+                        I.lag[lane * 8 + pos] = I.lag[lane * 8 + pos - 1];
+                        --pos;
+                    }
+                    I.resp[lane * 8 + pos] = rr;
+                    I.lag[lane * 8 + pos] = t0;
+                }
+            } else {
+                for (uint32_t c = lane; c < total; c += 32) {
+                    while (I.pre[j + 1] <= c) ++j;
+                    const int t0 = I.lo[j] + (int)(c - I.pre[j]);
+                    I.lag[C + c] = t0;
+                    I.resp[C + c] = mf_response(F.ev, e0, m, f, (double)t0);
+                }
             }
             C += total;
             __syncwarp();
@@ -491,7 +521,20 @@ __device__ void phase_init_peaks(const Frame& F, SM& sm) {
         for (int round = 0; round < K; ++round) {
             double best_r = -INFINITY;
             int best_l = 0x7fffffff;
-            if (listed) {
+            if (topk) {
+                for (int q = 0; q < nl; ++q) {  // first non-clashing entry of the lane's list
+                    const int t0 = I.lag[lane * 8 + q];
+                    bool clash = false;
+                    for (int u = 0; u < nt; ++u) {
+                        const int dd = taken[u] - t0;
+                        if ((dd < 0 ? -dd : dd) < sep) clash = true;
+                    }
+                    if (clash) continue;
+                    best_r = I.resp[lane * 8 + q];
+                    best_l = t0;
+                    break;
+                }
+            } else if (listed) {
                 for (uint32_t c = lane; c < C; c += 32) {
                     const int t0 = I.lag[c];
                     bool clash = false;
