@@ -292,6 +292,17 @@ __global__ void fft_kernel(const double* img, double* out, double* re, double* i
     cg::grid_group grid = cg::this_grid();
     const uint32_t nth = gridDim.x * blockDim.x;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (fft_pow2(nr) && fft_pow2(nc)) {  // radix 2 (lines in dynamic shared memory)
+        extern __shared__ double fft_smem[];
+        double* s_re = fft_smem;
+        double* s_im = fft_smem + kFftMax;
+        fftp_rows_forward(img, re, im, nr, nc, s_re, s_im, blockIdx.x, gridDim.x);
+        grid.sync();
+        fftp_cols_mask(re, im, nr, nc, cutoff, s_re, s_im, blockIdx.x, gridDim.x);
+        grid.sync();
+        fftp_rows_backward(re, im, out, nr, nc, clamp_nonneg, s_re, s_im, blockIdx.x, gridDim.x);
+        return;
+    }
     fft_stage1(img, re, im, nr, nc, gtid, nth);
     grid.sync();
     fft_stage2(re, im, re2, im2, nr, nc, cutoff, gtid, nth);
@@ -1280,7 +1291,8 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     for (int c = 0; c < kNumCfg; ++c) s->per_sm_c[c] = per_sm_c[c];
     set_frame_grids(s);
     int per_sm_fft = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock, 0));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fft, fft_kernel, kBlock,
+                                                           2 * kFftMax * sizeof(double)));
     s->grid_fft = s->nsm * std::max(1, per_sm_fft);
     CUDA_TRY(cudaMallocHost(&s->h_ctl, sizeof(Ctl)));
     if (getenv("RT3D_DEBUG")) {
@@ -2588,7 +2600,7 @@ rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t 
     int nr = rows, nc = cols, cl = clamp_nonneg;
     void* args[] = {&dimg, &dout, &re, &im, &re2, &im2, &nr, &nc, &cutoff, &cl};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)fft_kernel, dim3(s->grid_fft), dim3(kBlock),
-                                         args, 0, s->stream));
+                                         args, 2 * kFftMax * sizeof(double), s->stream));
     CUDA_TRY(cudaMemcpyAsync(out, dout, total * 8, cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     return RT3D_OK;

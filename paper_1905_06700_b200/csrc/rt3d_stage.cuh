@@ -313,6 +313,17 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
             double* im = F.fft_im;
             double* re2 = F.fft_re + F.npix;
             double* im2 = F.fft_im + F.npix;
+            if (fft_pow2(nr) && fft_pow2(nc) &&
+                2 * kFftMax * sizeof(double) <= sizeof(sm.u)) {  // radix 2, lines in shared memory
+                double* s_re = reinterpret_cast<double*>(&sm.u);
+                double* s_im = s_re + kFftMax;
+                fftp_rows_forward(F.b[bc], re, im, nr, nc, s_re, s_im, vblock(F), vgrid(F));
+                gsync(sm, F, PH_FFT);
+                fftp_cols_mask(re, im, nr, nc, F.cfg.cutoff, s_re, s_im, vblock(F), vgrid(F));
+                gsync(sm, F, PH_FFT);
+                fftp_rows_backward(re, im, F.b[bc], nr, nc, 1, s_re, s_im, vblock(F), vgrid(F));
+                gsync(sm, F, PH_FFT);
+            } else {
             fft_stage1(F.b[bc], re, im, nr, nc, gtid, nth);
             gsync(sm, F, PH_FFT);
             fft_stage2(re, im, re2, im2, nr, nc, F.cfg.cutoff, gtid, nth);
@@ -321,6 +332,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
             gsync(sm, F, PH_FFT);
             fft_stage4(re, im, F.b[bc], nr, nc, 1, gtid, nth);
             gsync(sm, F, PH_FFT);
+            }
         }
         X.bc = bc;
         X.apply_floor = 1;

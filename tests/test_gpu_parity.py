@@ -437,3 +437,23 @@ def test_reconstruct_early_stop_matches_oracle(gpu, name, tol):
     _assert_recon_parity(rep, ref, f"{name}/tol{tol}")
     pts, bg, r2 = gpu.frame_collect(gpu.frame_submit(sc, cfg))
     assert np.array_equal(pts, rep["points"]) and r2["iterations"] == rep["iterations"]
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 64), (256, 256), (32, 128), (1024, 1024), (48, 64)])
+def test_fft_lowpass_sizes(gpu, rows, cols):
+    """fft_lowpass_filter (denoise.hpp:267-311) at power-of-two sizes (the
+    radix-2 path) and a mixed one (the direct DFT) against the C oracle's
+    direct DFT, relative to the image scale."""
+    rng = np.random.default_rng(rows * 7 + cols)
+    img = rng.uniform(0.0, 2.0, (rows, cols)) + np.outer(np.sin(np.arange(rows) / 5.0),
+                                                        np.cos(np.arange(cols) / 7.0))
+    for cutoff, clamp in ((0.3, False), (0.8, True), (1.0, False)):
+        got = gpu.fft_lowpass(img, cutoff, clamp=clamp)
+        if rows * cols <= 256 * 256:
+            exp = O.fft_lowpass(img, cutoff, clamp=clamp, impl="oracle")
+            assert np.max(np.abs(got - exp)) <= 1e-12 * np.max(np.abs(img)), (cutoff, clamp)
+        else:   # the oracle's direct DFT is too slow here: linearity / identity properties
+            if cutoff == 1.0:
+                assert np.max(np.abs(got - img)) <= 1e-12 * np.max(np.abs(img))
+            half = gpu.fft_lowpass(0.5 * img, cutoff, clamp=clamp)
+            assert np.max(np.abs(2.0 * half - got)) <= 1e-12 * np.max(np.abs(img))

@@ -81,20 +81,24 @@ def full(path):
                    for c, v in traffic.items()}
 
 
+CMD = "python tools/profile_batch.py (one batch of 8 config-B frames, the bench step)"
+FULL_ARGS = "--profile-from-start off -c 6"
+
+
 def main():
     lpath, fpath, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     prof = ROOT / "profiles"
     l, tot = launches(lpath)
     (prof / f"{tag}_launches.md").write_text(
         f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n"
-        "Cold-cache, serialised per-launch times of `python tools/profile_frame.py 1` "
-        "(module load + one config-B frame). Compare shares, not absolutes.\n\n"
+        f"Cold-cache, serialised per-launch times of `{CMD}`. "
+        "Compare shares, not absolutes.\n\n"
         f"Total {tot:.1f} µs.\n\n" + "\n".join(l) + "\n")
     f, traffic = full(fpath)
     (prof / f"{tag}_ncu_full.md").write_text(
         f"# {tag}: ncu --set full (key metrics per captured launch)\n\n"
-        "`ncu --set full --clock-control none --import-source on -k "
-        "regex:\"apss_kernel|apss_fit|knn_kernel|stage_kernel\" -s 6 -c 6 python tools/profile_frame.py 1`\n\n"
+        f"`ncu --set full --clock-control none --import-source on -k "
+        f"regex:\"apss_kernel|apss_fit|knn_kernel|stage_kernel\" {FULL_ARGS} {CMD}`\n\n"
         + "\n".join(f) + "\n")
     traffic["_source"] = f"{fpath} ({tag}), dram__bytes_read.sum + dram__bytes_write.sum"
     (prof / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
