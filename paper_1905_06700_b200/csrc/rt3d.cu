@@ -583,6 +583,7 @@ struct rt3d_session {
     bool state_pinned = true;
     uint32_t P = 0;
     uint32_t pbase = 0;        // first point of the state (row bands: the band's own)
+    int batch_hint = 1;        // frames per launch being prepared (build_frame's sweep layout)
     bool banded = false;       // the state is one row band of a frame (rt3d_reconstruct_bands)
     uint32_t band_pix0 = 0, band_pix1 = 0;
     int tc = 0, rc = 0, bc = 0, sc = 0;
@@ -803,7 +804,12 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
                         SmemT<32>::kPvc);
         // sparse pixels: lane groups; groups of 3 (10 pixels per warp chunk)
         // when groups of 4 would leave more chunks than warps
-        if (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) {
+        if (mpp <= (uint32_t)kThreadPts && s->batch_hint >= 4 && !getenv("RT3D_WARP_PER_PIXEL")) {
+            // frames batched 4 or more to a launch (rt3d_reconstruct_batch):
+            // each frame gets few blocks, and a thread per pixel at 3 blocks
+            // per SM keeps more pixels in flight than lane groups at 2
+            F.cfg.gsz = 1;
+        } else if (mpp <= 4 && mean_ev <= 12.0 && !getenv("RT3D_WARP_PER_PIXEL")) {
             const uint64_t warps4 = (uint64_t)s->grid_frame_c[0] * kWarps;
             const uint64_t chunks4 = (npix + 7) / 8;
             F.cfg.gsz = (chunks4 > warps4 && !getenv("RT3D_G4")) ? 3 : 4;
@@ -1945,8 +1951,12 @@ rt3d_status rt3d_reconstruct_batch(rt3d_session* const* ss, int n, const rt3d_re
     rt3d_session* s0 = ss[0];
     static thread_local Frame Fs[kMaxBatch];
     rt3d_status st;
-    for (int k = 0; k < n; ++k)
-        if ((st = prepare_init_like(ss[k], cfg, PROG_RECON, Fs[k]))) return st;
+    for (int k = 0; k < n; ++k) {
+        ss[k]->batch_hint = n;
+        st = prepare_init_like(ss[k], cfg, PROG_RECON, Fs[k]);
+        ss[k]->batch_hint = 1;
+        if (st) return st;
+    }
     for (int k = 1; k < n; ++k)
         if (std::memcmp(&Fs[k].cfg, &Fs[0].cfg, sizeof(Cfg)) != 0)
             return fail(RT3D_ERR_UNSUPPORTED,

@@ -129,7 +129,7 @@ struct Cfg {
     int two_cand;      // depth / intensity candidate sweeps evaluate alpha and alpha * beta
     int fuse_depth;    // depth block at the end of ST_FIRST / ST_TAIL (no ST_DEPTH launch)
     int fused_iter;    // one ST_ITER launch per iteration (APSS, fit, kNN as grid phases)
-    int gsz;           // lanes per pixel in the likelihood sweeps (4 or 32)
+    int gsz;           // lanes per pixel in the likelihood sweeps (1, 3, 4 or 32)
 };
 
 struct Frame {
