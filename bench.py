@@ -391,8 +391,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
-    ap.add_argument("--batch", type=int, default=8,
-                    help="frames per step (rt3d_reconstruct_batch), 1..8")
+    ap.add_argument("--batch", type=int, default=16,
+                    help="frames per step (rt3d_reconstruct_batch), 1..16")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_init()

@@ -1762,7 +1762,7 @@ rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
 // identical to rt3d_reconstruct for any n.
 rt3d_status rt3d_reconstruct_bands(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
     if (!ss || n < 1 || n > kMaxBatch || (n & (n - 1)))
-        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: 1, 2, 4 or 8 row bands");
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: row bands: a power of two up to 16");
     for (int k = 0; k < n; ++k) {
         if (!ss[k]) return fail(RT3D_ERR_INVALID_ARGUMENT, "null session in bands");
         for (int j = 0; j < k; ++j)
@@ -1907,7 +1907,7 @@ rt3d_status rt3d_band_plan(uint32_t n_rows, uint32_t n_cols, int32_t superres, d
                            double apss_radius, int32_t n, uint32_t* begin, uint32_t* end,
                            uint32_t* halo_rows) {
     if (n < 1 || n > kMaxBatch || (n & (n - 1)))
-        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: 1, 2, 4 or 8 row bands");
+        return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: row bands: a power of two up to 16");
     if (!begin || !end || !halo_rows || superres < 1 || !(pixel_pitch > 0.0) || !(apss_radius > 0.0))
         return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: bad band plan arguments");
     int d = 0;

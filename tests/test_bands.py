@@ -43,7 +43,7 @@ def _scene(rows, bins, seed, ppp=30.0):
     return simulate(spec, seed)
 
 
-@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16])
 def test_bands_equal_single_frame_large_array(gpu, n):
     """256x256x2048 (config D, thread-per-pixel sweeps)."""
     name, spec, seed, cfg = W.config_d()

@@ -2,6 +2,7 @@
 and C at batch sizes 1, 2, 4, 8: CUDA events around each batch, inputs
 resident, L2 flushed between batches."""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -18,9 +19,9 @@ keys = sys.argv[1:] or ["B", "C"]
 flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda:0")
 for key in keys:
     name, spec, seed, cfg = W.CONFIGS[key]()
-    cubes = [simulate(W.config_c(f)[1], 1000 + f) for f in range(8)] if key == "C" else \
-        [simulate(spec, seed)] * 8
-    for n in (1, 2, 4, 8):
+    cubes = [simulate(W.config_c(f)[1], 1000 + f) for f in range(16)] if key == "C" else \
+        [simulate(spec, seed)] * 16
+    for n in [int(x) for x in os.environ.get("BATCHES", "1,2,4,8").split(",")]:
         ss = [Session(0) for _ in range(n)]
         for s, c in zip(ss, cubes):
             s.set_scene(c)
