@@ -864,6 +864,7 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
     const int2* plh = W.plh + pbase;
 
     // rates at the active bins (detail::active_rates, likelihood.hpp:100-121)
+    bool bad = false;  // an active bin at rate <= 0 (the nll is +inf)
     for (uint32_t k = gl; k < m; k += G) {
         const uint2 e = EV[k];
         double l = 0.0;
@@ -876,27 +877,29 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
             }
         }
         LAM[k] = l;
+        bad |= l <= 0.0;
         const double z = (double)e.y;
         TN[k] = (l > 0.0) ? z * log(l) : 0.0;
-        if (KIND == K_GRAD_B) {
-            T1[k] = g * z / l;
-            T2[k] = g * g * z / (l * l);
+        if (KIND == K_GRAD_B) {  // zero terms where the reference skips the bin
+            T1[k] = (l > 0.0) ? g * z / l : 0.0;
+            T2[k] = (l > 0.0) ? g * g * z / (l * l) : 0.0;
         }
     }
+    const bool any_bad = __any_sync(gmask, bad);
     __syncwarp(gmask);
 
-    // nll partial, likelihood.hpp:141-165 (leader, reference order)
+    // nll partial, likelihood.hpp:141-165 (leader, reference order): +inf at
+    // the first bin with rate <= 0, else the sequential subtraction, now free
+    // of the per-bin branch so the shared-memory loads pipeline
     double part = 0.0;
     if (gl == 0 && !dead) {
         double mass = T * b;
         for (uint32_t qq = 0; qq < np; ++qq) mass += pr[qq] * W.pmig[pbase + qq];
         double acc = gain * mass;
-        for (uint32_t k = 0; k < m; ++k) {
-            if (LAM[k] <= 0.0) {
-                acc = INFINITY;
-                break;
-            }
-            acc -= TN[k];
+        if (any_bad) {
+            acc = INFINITY;
+        } else {
+            for (uint32_t k = 0; k < m; ++k) acc -= TN[k];
         }
         part = acc;
     }
@@ -911,10 +914,16 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
             if (!skip) {
                 const double t = pt[k], r = pr[k];
                 const int2 lh = plh[k];
-                // first staged event with bin >= lo
+                // first staged event with bin >= lo (binary search)
                 uint32_t kk = 0;
-                if (lh.x <= lh.y)
-                    while (kk < m && EV[kk].x < (uint32_t)lh.x) ++kk;
+                if (lh.x <= lh.y) {
+                    uint32_t hi = m;
+                    while (kk < hi) {
+                        const uint32_t mid = (kk + hi) >> 1;
+                        if (EV[mid].x < (uint32_t)lh.x) kk = mid + 1;
+                        else hi = mid;
+                    }
+                }
                 if (KIND == K_GRAD_T) {  // grad_depth + curvature().depth
                     if (lh.x > lh.y) {
                         og = 1;
@@ -971,11 +980,9 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
         double gval = 0.0, bs = 0.0;
         if (g != 0.0) {
             double acc = g * T;
-            for (uint32_t k = 0; k < m; ++k) {
-                if (LAM[k] > 0.0) {
-                    acc -= T1[k];
-                    bs += T2[k];
-                }
+            for (uint32_t k = 0; k < m; ++k) {  // T1 = T2 = 0 where LAM <= 0: same sums
+                acc -= T1[k];
+                bs += T2[k];
             }
             gval = acc;
         }

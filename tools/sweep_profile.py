@@ -1,6 +1,7 @@
-"""Per-transition timing of the in-kernel profile stamps of one config-B
-frame (sweep sub-phases 100..106 included when compiled in).
-usage: python tools/sweep_profile.py  (sub-phases 100..113 need a build with
+"""Per-transition timing of the in-kernel profile stamps of one frame of a
+workload (default config B; sweep sub-phases 100..113 included when compiled
+in: block 0's view, so 101->102 is the grid barrier's wait).
+usage: python tools/sweep_profile.py [A|B|C|D]  (sub-phases need a build with
   make -C paper_1905_06700_b200/csrc EXTRA=-DRT3D_SWEEP_PROF)"""
 import sys
 from collections import defaultdict
@@ -8,11 +9,12 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-import bench  # noqa: E402
+sys.path.insert(0, str(ROOT / "tools"))
+import workloads as W  # noqa: E402
 from paper_1905_06700_b200.rt3d import Session  # noqa: E402
 from scenegen.scene import simulate  # noqa: E402
 
-spec, seed, cfg, _ = bench.config_b()
+_, spec, seed, cfg = W.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "B"]()
 sc = simulate(spec, seed)
 with Session(0) as s:
     s.set_scene(sc)
