@@ -30,8 +30,10 @@ constexpr int kKnnCap = 384;     // per-warp ball list for the kNN selection
 constexpr int kFitBlock = 128;
 
 struct RowTab {
-    uint32_t pre[33];  // exclusive prefix of the window rows' candidate counts
-    uint32_t m0[32];   // first candidate index of each row
+    // the batch's non-empty rows, compacted in row order
+    uint32_t pre[32];  // rank of the row's first candidate (strictly increasing)
+    uint32_t m0[32];   // index of the row's first candidate
+    uint32_t n;        // number of non-empty rows
 };
 struct ApssMember {
     double z, w;
@@ -115,10 +117,14 @@ __device__ __forceinline__ uint32_t rows_finish(RowTab& rt, uint32_t m0, uint32_
         const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += y;
     }
-    rt.pre[lane] = inc - len;
-    rt.m0[lane] = m0;
+    const uint32_t ne = __ballot_sync(0xffffffffu, len != 0u);
+    if (len) {
+        const int cp = __popc(ne & lanemask_lt());
+        rt.pre[cp] = inc - len;
+        rt.m0[cp] = m0;
+    }
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    if (lane == 31) rt.pre[32] = total;
+    if (lane == 0) rt.n = (uint32_t)__popc(ne);
     __syncwarp();
     return total;
 }
@@ -135,20 +141,30 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
     const double* tt = F.t[tc];
     const int32_t* FI = F.fi[sc];
     const int32_t* FJ = F.fj[sc];
-    int j = 0;
-    auto locate = [&](uint32_t f) -> uint32_t {
-        while (rt.pre[j + 1] <= f) ++j;
-        RT3D_CHECK(j < 32 && rt.m0[j] + (f - rt.pre[j]) < F.pcap);
-        return rt.m0[j] + (f - rt.pre[j]);
+    // lane k holds non-empty row k: its first rank pk and rank -> index
+    // offset dk.  The row of candidate fb + l is the row holding fb plus the
+    // rows starting in (fb, fb + l]: a ballot, an OR-reduction of the start
+    // offsets inside the chunk and a popcount, then one shuffle.
+    const bool hr = (uint32_t)lane < rt.n;
+    const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
+    const uint32_t dk = hr ? rt.m0[lane] - pk : 0u;
+    const uint32_t lanes_le = lanemask_lt() | (1u << lane);
+    auto locate = [&](uint32_t fb) -> uint32_t {  // warp-collective: candidate fb + lane
+        const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= fb)) - 1;
+        const uint32_t bit = (pk > fb && pk - fb < 32u) ? 1u << (pk - fb) : 0u;
+        const int j = j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & lanes_le);
+        return fb + (uint32_t)lane + __shfl_sync(0xffffffffu, dk, j);
     };
     bool v = (uint32_t)lane < total;
-    uint32_t mm = v ? locate(lane) : 0u;
+    uint32_t mm = locate(0u);
+    RT3D_CHECK(!v || mm < F.pcap);
     int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
     double ctt = v ? tt[mm] : 0.0;
     for (uint32_t fb = 0; fb < total; fb += 32) {
         const uint32_t f2 = fb + 32 + lane;
         const bool v2 = f2 < total;
-        const uint32_t mm2 = v2 ? locate(f2) : 0u;
+        const uint32_t mm2 = locate(fb + 32u);
+        RT3D_CHECK(!v2 || mm2 < F.pcap);
         const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
         const double ntt = v2 ? tt[mm2] : 0.0;
         bool ok = false;
