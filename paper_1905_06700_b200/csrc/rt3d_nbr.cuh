@@ -132,8 +132,10 @@ __device__ __forceinline__ uint32_t rows_finish(RowTab& rt, uint32_t m0, uint32_
 // The candidates of one row batch (rt, total) against q: visit(rank, mm,
 // pos, d2, fi, fj) on member lanes, flush(n_members) once per chunk of 32
 // candidates (warp-synchronous); the next chunk's loads are issued before the
-// current chunk is processed.
-template <typename Visit, typename Flush>
+// current chunk is processed.  kXLane: flush reads what other lanes' visits
+// wrote (warp barriers around it); list builders that only write their own
+// slots skip those barriers and synchronise once after the scan.
+template <bool kXLane = true, typename Visit, typename Flush>
 __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const RowTab& rt,
                                           uint32_t total, const Pos& q, double r2, Visit visit,
                                           Flush flush) {
@@ -181,9 +183,9 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
         const uint32_t bal = __ballot_sync(0xffffffffu, ok);
         if (bal) {
             if (ok) visit(__popc(bal & lanemask_lt()), mm, o, d2, cfi, cfj);
-            __syncwarp();
+            if (kXLane) __syncwarp();
             flush(__popc(bal));
-            __syncwarp();
+            if (kXLane) __syncwarp();
         }
         v = v2;
         mm = mm2;
@@ -195,7 +197,7 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
 }
 
 // Ball of q over the window, all row batches.
-template <typename Visit, typename Flush>
+template <bool kXLane = true, typename Visit, typename Flush>
 __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab& rt, int fi,
                                           int fj, const Pos& q, double r2, Visit visit,
                                           Flush flush, int Wq = -1) {
@@ -207,7 +209,7 @@ __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab
         uint32_t m0, len;
         rows_load(F, sc, fi, fj, W, rb, ci1, m0, len);
         const uint32_t total = rows_finish(rt, m0, len);
-        rows_scan(F, tc, sc, rt, total, q, r2, visit, flush);
+        rows_scan<kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
     }
 }
 
@@ -304,8 +306,8 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, d2, mfi, mfj};
         };
         auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
-        if (single) rows_scan(F, tc, sc, rcur, total, q, r2, visitA, flushA);
-        else ball_scan(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
+        if (single) rows_scan<false>(F, tc, sc, rcur, total, q, r2, visitA, flushA);
+        else ball_scan<false>(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
         if (has_next && single_next) rows_load(F, sc, nfi, nfj, W, nci0, nci1, nm0, nlen);
         auto advance = [&]() {
             single_cur = single_next;
@@ -604,8 +606,9 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
                 }
             };
             auto flushK = [&](int nm) { cnt += (unsigned int)nm; };
-            if (w == w0 && first_single) rows_scan(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
-            else ball_scan(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
+            if (w == w0 && first_single)
+                rows_scan<false>(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
+            else ball_scan<false>(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
             __syncwarp();
             if (!next_loaded && has_next && single_next) {
                 rows_load(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
