@@ -1971,7 +1971,7 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
     double pa[32][4];
     for (int l = 0; l < 32; ++l) pa[l][0] = pa[l][1] = pa[l][2] = pa[l][3] = 0.0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        const double w = apss_weight(R, sqrt(d2));
+        const double w = apss_weight_d2(R, d2);
         double* a = pa[cnt & 31u];
         ++cnt;
         a[0] += w;
@@ -1998,7 +1998,7 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
         for (int e = 0; e < kRedStride; ++e) pb[l][e] = 0.0;
     unsigned int c2 = 0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        apss_pass_b(pb[c2 & 31u], apss_weight(R, sqrt(d2)), o.x, o.y, o.z, m0, m1, m2);
+        apss_pass_b(pb[c2 & 31u], apss_weight_d2(R, d2), o.x, o.y, o.z, m0, m1, m2);
         ++c2;
     });
     double cv[6], M[15];

@@ -93,6 +93,20 @@ __device__ __forceinline__ double apss_weight(double radius, double dist) {
     return s * s;
 }
 
+// apss_weight(radius, sqrt(d2)) for d2 >= 0.  A zero operand sends both the
+// double sqrt and the division to their out-of-line slow paths, once per
+// point (the point is its own member) and serialised in the warp; d2 == 0
+// gives x = +0 either way, so it is routed around them with the same bits.
+__device__ __forceinline__ double apss_weight_d2(double radius, double d2) {
+    const bool self = d2 == 0.0;
+    double x = sqrt(self ? 1.0 : d2) / radius;
+    if (self) x = 0.0;
+    if (x >= 1.0) return 0.0;
+    double s = 1.0 - x * x;
+    s *= s;
+    return s * s;
+}
+
 // Eigenvalues of the weighted 3x3 covariance (lower triangle c00,c10,c11,
 // c20,c21,c22), ascending, by cyclic Jacobi.  Only the eigenvalues decide
 // anything in apss_project (denoise.hpp:197-203): the eigenvector orients

@@ -317,7 +317,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             __syncwarp();
             for (unsigned int g = lane; g < cnt; g += 32) {
                 ApssMember& mb = A.u.list[g];
-                const double w = apss_weight(R, sqrt(mb.w));
+                const double w = apss_weight_d2(R, mb.w);
                 mb.w = w;
                 a0 += w;
                 a1 += w * ((mb.fi + 0.5) * F.pitch);
@@ -331,7 +331,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                 F, tc, sc, A.rt, fi, fj, q, r2,
                 [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
                     double* c = A.chunk[rank];
-                    c[0] = apss_weight(R, sqrt(d2));
+                    c[0] = apss_weight_d2(R, d2);
                     c[1] = o.x;
                     c[2] = o.y;
                     c[3] = o.z;
@@ -376,7 +376,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                 F, tc, sc, A.rt, fi, fj, q, r2,
                 [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
                     double* c = A.chunk[rank];
-                    c[0] = apss_weight(R, sqrt(d2));
+                    c[0] = apss_weight_d2(R, d2);
                     c[1] = o.x;
                     c[2] = o.y;
                     c[3] = o.z;

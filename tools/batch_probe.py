@@ -1,6 +1,7 @@
 """Frames/s of batched reconstructs (rt3d_reconstruct_batch) for configs B
-and C at batch sizes 1, 2, 4, 8: CUDA events around each batch, inputs
-resident, L2 flushed between batches."""
+and C at batch sizes 1, 2, 4, 8 (BATCHES=...): CUDA events around each
+batch, inputs resident, L2 flushed between batches.  KT=1 adds the per-class
+kernel times per frame."""
 import json
 import os
 import sys
@@ -43,6 +44,14 @@ for key in keys:
             ms = sum(a.elapsed_time(b) for a, b in ev) / K
             print(json.dumps({"config": key, "batch": n, "ms_per_batch": ms,
                               "frames_per_s": 1e3 * n / ms}), flush=True)
+            if os.environ.get("KT"):  # per-class kernel ms per frame (events around each launch)
+                ss[0].time_kernels(True)
+                for _ in range(K):
+                    Session.reconstruct_batch_async(ss, cfg)
+                kt = ss[0].kernel_times()
+                ss[0].time_kernels(False)
+                print(json.dumps({"config": key, "batch": n, "kernel_ms_per_frame": {
+                    k: round(v[0] / (K * n), 4) for k, v in kt.items() if v[1]}}), flush=True)
         except Exception as e:  # noqa: BLE001
             print(json.dumps({"config": key, "batch": n, "error": str(e)}), flush=True)
         finally:
