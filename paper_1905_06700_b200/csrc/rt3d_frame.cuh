@@ -238,17 +238,20 @@ __device__ __forceinline__ uint32_t global_P(const Frame& F) { return __ldcg(&F.
 // <= kPvc points, then processed by lane groups (one pixel per group).
 // Staging capacities: lane groups of 4 (sparse frames, <= 4 points and ~12
 // events per pixel) stage 8 pixels per batch; a warp per pixel stages up to
-// 32.  The smaller footprint lets two 256-thread blocks share an SM.
+// 32 (176 events: two warp-per-pixel blocks still share an SM, see the
+// static_assert below SmemT).  The smaller footprint lets two 256-thread
+// blocks share an SM.
 // (G == 1, thread per pixel, reads the CSR directly: no staging)
 template <int G>
 struct SweepDims {
-    static constexpr int EVC = G >= 32 ? 192 : G == 1 ? 1 : 64;
+    static constexpr int EVC = G >= 32 ? 176 : G == 1 ? 1 : 64;
     static constexpr int PVC = G >= 32 ? 128 : G == 1 ? 1 : 32;
 };
 template <int EVC, int PVC>
 struct WarpSweepSmT {
     uint2 ev[EVC];
     double lam[EVC], tn[EVC], t1[EVC], t2[EVC];
+    uint32_t mk[EVC + 1];  // warp-per-pixel sweeps: the points whose support holds each event
     double pt[PVC], pr[PVC], pmig[PVC];
     int2 plh[PVC];
     uint32_t me0[32], mm[32], mn0[32], mnp[32];
@@ -294,6 +297,10 @@ struct SmemT {
     IrfDev irf0;
     double irf_tab[2 * kIrfSmem];
 };
+
+// two blocks per SM: 228 KB of shared memory, 1 KB reserved per block
+static_assert(2 * (sizeof(SmemT<32>) + 1024) <= 233472, "warp-per-pixel stage blocks no longer pair on an SM");
+static_assert(2 * (sizeof(SmemT<4>) + 1024) <= 233472, "lane-group stage blocks no longer pair on an SM");
 
 // Bounds checks of the checked build (make checked: -DRT3D_CHECKS, the
 // librt3d_checked.so the test suite runs under with RT3D_LIB): a violated
@@ -863,6 +870,59 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
     const double* pr = W.pr + pbase;
     const int2* plh = W.plh + pbase;
 
+    // A warp per pixel (<= 32 points, events staged): the points whose IRF
+    // support holds event k as a bit mask MK[k], so each event visits only
+    // those points, still in cloud order.  Events are sorted by bin, so a
+    // point's support [lo, hi] is the event range [lower_bound(lo),
+    // lower_bound(hi + 1)); its bit is toggled at both ends and a prefix XOR
+    // over the events (a contiguous run per lane, then across lanes) gives
+    // the masks.
+    const bool use_mask = G == 32 && np <= 32u && m <= (uint32_t)SmemT<G>::kEvc && g != 0.0;
+    uint32_t* MK = W.mk;
+    if (use_mask) {
+        for (uint32_t k = gl; k <= m; k += G) MK[k] = 0u;
+        __syncwarp(gmask);
+        if ((uint32_t)gl < np) {
+            const int2 lh = plh[gl];
+            if (lh.x <= lh.y) {
+                uint32_t a = 0, hi = m;
+                while (a < hi) {
+                    const uint32_t mid = (a + hi) >> 1;
+                    if ((int)EV[mid].x < lh.x) a = mid + 1;
+                    else hi = mid;
+                }
+                uint32_t c = a;
+                hi = m;
+                while (c < hi) {
+                    const uint32_t mid = (c + hi) >> 1;
+                    if ((int)EV[mid].x <= lh.y) c = mid + 1;
+                    else hi = mid;
+                }
+                if (a < c) {
+                    atomicXor(&MK[a], 1u << gl);
+                    atomicXor(&MK[c], 1u << gl);
+                }
+            }
+        }
+        __syncwarp(gmask);
+        const uint32_t per = (m + 31u) >> 5;
+        const uint32_t c0 = min((uint32_t)gl * per, m), c1 = min(c0 + per, m);
+        uint32_t x = 0;
+        for (uint32_t k = c0; k < c1; ++k) x ^= MK[k];
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(gmask, inc, o);
+            if (gl >= o) inc ^= y;
+        }
+        uint32_t run = inc ^ x;  // exclusive
+        for (uint32_t k = c0; k < c1; ++k) {
+            run ^= MK[k];
+            MK[k] = run;
+        }
+        __syncwarp(gmask);
+    }
+
     // rates at the active bins (detail::active_rates, likelihood.hpp:100-121)
     bool bad = false;  // an active bin at rate <= 0 (the nll is +inf)
     for (uint32_t k = gl; k < m; k += G) {
@@ -870,10 +930,17 @@ __device__ __forceinline__ double sweep_staged_pixel(const Frame& F, typename Sm
         double l = 0.0;
         if (g != 0.0) {
             l = g * b;
-            for (uint32_t qq = 0; qq < np; ++qq) {
-                const int2 lh = plh[qq];
-                if ((int)e.x >= lh.x && (int)e.x <= lh.y)
+            if (use_mask) {
+                for (uint32_t mk = MK[k]; mk; mk &= mk - 1u) {
+                    const int qq = __ffs((int)mk) - 1;
                     l += g * pr[qq] * irf_value_fast(f, (double)e.x - pt[qq]);
+                }
+            } else {
+                for (uint32_t qq = 0; qq < np; ++qq) {
+                    const int2 lh = plh[qq];
+                    if ((int)e.x >= lh.x && (int)e.x <= lh.y)
+                        l += g * pr[qq] * irf_value_fast(f, (double)e.x - pt[qq]);
+                }
             }
         }
         LAM[k] = l;

@@ -1,5 +1,5 @@
 """Per-source-line instruction and stall-sample shares of one kernel in an
-.ncu-rep (`python tools/ncu_lines.py rep.ncu-rep [top]`)."""
+.ncu-rep (`python tools/ncu_lines.py rep.ncu-rep [top] [launch index]`)."""
 import csv
 import io
 import subprocess
@@ -7,8 +7,9 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+extra = ["--launch-skip", sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+                     + extra, capture_output=True, text=True).stdout
 fname, hdr, rows = None, None, []
 for x in csv.reader(io.StringIO(out)):
     if len(x) >= 2 and x[0] == "File Path":
