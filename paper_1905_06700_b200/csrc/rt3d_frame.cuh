@@ -786,16 +786,16 @@ struct SweepCtx {
 };
 
 // Irf::value / deriv (sensor.hpp:69-82), branch-free so that independent
-// evaluations overlap: for in-range tau, x >= 0 and
-// min((size_t)x, n-2) == min(trunc(x), n-2) as a double, so the segment and
-// the fraction x - k are bit-identical to the reference's; out-of-range taus
-// read a clamped segment and are discarded by the final select.
+// evaluations overlap: for in-range tau, 0 <= x <= n-1, so the saturating
+// conversion min((uint32)x, n-2) is the reference's segment
+// min((size_t)x, n-2), and converting it back gives the same x - k; out of
+// range taus read a clamped segment (the conversion saturates: negative and
+// NaN give 0) and are discarded by the final select.
 __device__ __forceinline__ double irf_value_fast(const IrfDev& f, double tau) {
     const bool in = (tau >= f.tau_min) && (tau <= f.tau_max);
     const double x = irf_x(f, tau);
-    const double kd = fmax(fmin(trunc(x), f.lim), 0.0);
-    const uint32_t k = __double2uint_rz(kd);
-    const double fr = x - kd;
+    const uint32_t k = min(__double2uint_rz(x), f.n - 2u);
+    const double fr = x - (double)k;
     const double s0 = f.s[k], s1 = f.s[k + 1];
     const double v = s0 + fr * (s1 - s0);
     return in ? v : 0.0;
@@ -803,8 +803,7 @@ __device__ __forceinline__ double irf_value_fast(const IrfDev& f, double tau) {
 __device__ __forceinline__ double irf_deriv_fast(const IrfDev& f, double tau) {
     const bool in = (tau > f.tau_min) && (tau < f.tau_max);
     const double x = irf_x(f, tau);
-    const double kd = fmax(fmin(trunc(x), f.lim), 0.0);
-    const double v = f.d[__double2uint_rz(kd)];
+    const double v = f.d[min(__double2uint_rz(x), f.n - 2u)];
     return in ? v : 0.0;
 }
 // sum of -deriv over the support bins (likelihood.hpp:205), evaluations
