@@ -679,6 +679,9 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.cols = s->cols;
     F.bins = s->bins;
     F.s = s->s;
+    if ((uint64_t)s->rows * (uint64_t)s->s >= (1ull << 20) || (uint64_t)s->cols * (uint64_t)s->s >= (1ull << 20))
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: fine grids of 2^20 or more rows or columns are not supported");
+    F.smag = s->s > 1 ? (uint32_t)(((1ull << 32) + (uint64_t)s->s - 1) / (uint64_t)s->s) : 0u;
     F.frows = s->rows * s->s;
     F.fcols = s->cols * s->s;
     F.pitch = s->pitch;

@@ -136,6 +136,7 @@ struct Frame {
     // sensor (sensor.hpp:131-170)
     int rows, cols, bins, s;
     int frows, fcols;
+    uint32_t smag;  // ceil(2^32 / s) (s > 1): a / s == umulhi(a, smag) for 0 <= a < 2^20
     double pitch, bres, tlim;
     const IrfDev* irfs;
     const uint32_t* irf_of_pix;  // nullptr: irfs[0] for every pixel
@@ -227,6 +228,13 @@ struct FrameBatch {
 };
 
 // this block's index / the block count within its frame
+// coarse index a / F.s of a fine index 0 <= a < 2^20 without an integer
+// division: with m = ceil(2^32 / s) = (2^32 + e) / s, 0 <= e < s,
+// a m / 2^32 = a / s + a e / (s 2^32) and a e < 2^32 keeps the floor exact
+__device__ __forceinline__ int coarse_of(const Frame& F, int a) {
+    return F.s == 1 ? a : (int)__umulhi((uint32_t)a, F.smag);
+}
+
 __device__ __forceinline__ uint32_t vblock(const Frame& F) { return blockIdx.x - F.blk0; }
 __device__ __forceinline__ uint32_t vgrid(const Frame& F) { return F.nblk; }
 // the frame's global point count (all bands)
@@ -1964,7 +1972,8 @@ __device__ __forceinline__ void for_each_pinned_neighbor(const Frame& F, int tc,
     b0 = b0 < 0 ? 0 : b0;
     a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
     b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
-    const int ci0 = a0 / s, ci1 = a1 / s, cj0 = b0 / s, cj1 = b1 / s;
+    const int ci0 = coarse_of(F, a0), ci1 = coarse_of(F, a1), cj0 = coarse_of(F, b0),
+              cj1 = coarse_of(F, b1);
     const uint32_t* bo = F.bo[sc];
     const double* tt = F.t[tc];
     const int32_t* FI = F.fi[sc];

@@ -70,10 +70,8 @@ __device__ __forceinline__ void window_rows(const Frame& F, int fi, int W, int& 
     int a0 = fi - W, a1 = fi + W;
     a0 = a0 < 0 ? 0 : a0;
     a1 = a1 > F.frows - 1 ? F.frows - 1 : a1;
-    // (integer division by the runtime superres factor is slow; s == 1 is
-    // the common case)
-    ci0 = F.s == 1 ? a0 : a0 / F.s;
-    ci1 = F.s == 1 ? a1 : a1 / F.s;
+    ci0 = coarse_of(F, a0);
+    ci1 = coarse_of(F, a1);
 }
 
 // Candidate range of window row ci = rb + lane (disc-culled columns): the
@@ -101,7 +99,7 @@ __device__ __forceinline__ void rows_load(const Frame& F, int sc, int fi, int fj
             b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
             const uint32_t prow = (uint32_t)ci * F.cols;
             const uint32_t* bo = F.bo[sc];
-            const int c0 = s == 1 ? b0 : b0 / s, c1 = s == 1 ? b1 : b1 / s;
+            const int c0 = coarse_of(F, b0), c1 = coarse_of(F, b1);
             m0 = bo[prow + c0];
             len = bo[prow + c1 + 1] - m0;
         }
@@ -454,25 +452,70 @@ static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P,
     }
 }
 
+// ascending bitonic sort of one double per lane across the warp
+__device__ __forceinline__ double warp_sort32(double x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int j = size >> 1; j > 0; j >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, x, j);
+            const bool up = (lane & size) == 0;  // this pair sorts ascending
+            const bool low = (lane & j) == 0;    // this lane keeps the smaller
+            x = (low == up) ? (y < x ? y : x) : (y > x ? y : x);
+        }
+    }
+    return x;
+}
+
 // k smallest (d^2, index) keys of the warp's list in rank order
 // (spatial_index.hpp:51-62) -> K.sel[0..taken); kth = the last key's d^2.
 __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k, double& kth) {
     const int lane = threadIdx.x & 31;
     if (cnt <= 64u) {
-        // rank counting: the list is in ascending index order, so the
-        // (d^2, index) order is (d^2, slot); ranks are a permutation
+        // The list is in ascending index order, so the (d^2, index) order is
+        // (d^2, slot).  Lists above 32: the k-th smallest of the 32 lane minima
+        // (a lane holds slots lane and lane + 32) bounds the k-th smallest
+        // key from above, so the keys above it rank >= k.  The keys at or
+        // below it are compacted in slot order (typically ~k of them) and
+        // ranked by counting; ranks are a permutation.
         const int taken = (unsigned int)k < cnt ? k : (int)cnt;
+        const bool v0 = (unsigned int)lane < cnt, v1 = (unsigned int)lane + 32u < cnt;
+        const double a0 = v0 ? K.d2[lane] : INFINITY, a1 = v1 ? K.d2[lane + 32] : INFINITY;
+        double tau = INFINITY;
+        if (k <= 32 && cnt > 32u) {  // (short lists: counting over all is cheaper)
+            const double srt = warp_sort32(a0 < a1 ? a0 : a1);
+            tau = __shfl_sync(0xffffffffu, srt, k - 1);
+        }
+        const bool in0 = v0 && a0 <= tau, in1 = v1 && a1 <= tau;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, in0), b1 = __ballot_sync(0xffffffffu, in1);
+        const unsigned int c0 = (unsigned int)__popc(b0), c = c0 + (unsigned int)__popc(b1);
+        // the compacted keys go to slots [64, 64 + c) of the list (cnt <= 64)
+        double* cd = K.d2 + 64;
+        uint32_t* ci = K.idx + 64;
+        const uint32_t idx0 = v0 ? K.idx[lane] : 0u, idx1 = v1 ? K.idx[lane + 32] : 0u;
+        if (in0) {
+            const unsigned int p = (unsigned int)__popc(b0 & lanemask_lt());
+            cd[p] = a0;
+            ci[p] = idx0;
+        }
+        if (in1) {
+            const unsigned int p = c0 + (unsigned int)__popc(b1 & lanemask_lt());
+            cd[p] = a1;
+            ci[p] = idx1;
+        }
+        __syncwarp();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const unsigned int sl = (unsigned int)lane + 32u * h;
-            if (sl < cnt) {
-                const double my = K.d2[sl];
+            if (sl < c) {
+                const double my = cd[sl];
                 int rank = 0;
-                for (unsigned int e = 0; e < cnt; ++e) {
-                    const double d = K.d2[e];
+                for (unsigned int e = 0; e < c; ++e) {
+                    const double d = cd[e];
                     rank += (d < my || (d == my && e < sl)) ? 1 : 0;
                 }
-                if (rank < taken) K.sel[rank] = K.idx[sl];
+                if (rank < taken) K.sel[rank] = ci[sl];
                 if (rank == taken - 1) K.kth = my;
             }
         }
