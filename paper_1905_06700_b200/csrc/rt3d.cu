@@ -71,6 +71,29 @@ __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant
               ld_cg(&F.ctl->tc), ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
 }
 
+// Depth intervals of the blocks of F.zbs consecutive points of each pixel
+// (thread per block) for the APSS scan's block culling (ball_scan_blocks)
+__global__ void zblock_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
+    const int tc = ld_cg(&F.ctl->tc), sc = ld_cg(&F.ctl->sc);
+    const uint32_t nb = F.npix * F.zkb;
+    const uint32_t* bo = F.bo[sc];
+    const double* t = F.t[tc];
+    for (uint32_t b = vblock(F) * blockDim.x + threadIdx.x; b < nb; b += vgrid(F) * blockDim.x) {
+        const uint32_t p = b / F.zkb, k = b - p * F.zkb;
+        const uint32_t n1 = bo[p + 1], lo = bo[p] + k * F.zbs;
+        const uint32_t hi = lo + F.zbs < n1 ? lo + F.zbs : n1;
+        double zmin = INFINITY, zmax = -INFINITY;
+        for (uint32_t n = lo; n < hi; ++n) {
+            const double z = t[n] * F.bres;
+            zmin = z < zmin ? z : zmin;
+            zmax = z > zmax ? z : zmax;
+        }
+        F.zb[b] = make_double2(zmin, zmax);
+    }
+}
+
 // Row bands: every band keeps full-size arrays in the global
 // index space (pixels and points), so a halo is a plain copy of the
 // neighbouring bands' rows into this band's arrays at the same indices:
@@ -573,7 +596,7 @@ struct rt3d_session {
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
     DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot, part, mig[2];
-    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom;
+    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom, zb;
     DevBuf ctl, diag, trace, outpts, misc, prof, tblk, tbmax;
     bool profile = false;
     Ctl* h_ctl = nullptr;  // pinned staging
@@ -763,6 +786,20 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     CUDA_TRY(s->amom.ensure(std::max<size_t>(s->pcap, 1) * kMom * 8));
     F.amom = s->amom.as<double>();
     F.amom_stride = (uint32_t)std::max<size_t>(s->pcap, 1);
+    // depth blocks for the neighbour scans of superres frames: blocks of s^2
+    // points (one spawned surface), at most 4 per pixel
+    F.zb = nullptr;
+    F.zkb = F.zbs = 0;
+    {
+        const uint32_t bs = (uint32_t)(s->s * s->s);
+        const uint32_t kb = (std::max<uint32_t>(s->max_pts_per_pixel, 1) + bs - 1) / bs;
+        if (s->s > 1 && kb <= 4 && !getenv("RT3D_NO_ZBLOCKS")) {
+            CUDA_TRY(s->zb.ensure((size_t)npix * kb * sizeof(double2)));
+            F.zb = s->zb.as<double2>();
+            F.zkb = kb;
+            F.zbs = bs;
+        }
+    }
     F.ctl = s->ctl.as<Ctl>();
     F.dbg = s->d_dbg;
     F.prof = nullptr;
@@ -778,6 +815,7 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     // opt-in (RT3D_FUSED_ITER=1): measured slower on config B, the neighbour
     // phases run at the stage kernels' occupancy
     F.cfg.fused_iter = (F.cfg.fuse_depth && getenv("RT3D_FUSED_ITER")) ? 1 : 0;
+    if (F.cfg.fused_iter) F.zb = nullptr;  // (no depth-block pass inside one-launch iterations)
     // two-candidate sweeps: bit 0 intensity, bit 1 depth (RT3D_TWO_CAND).
     // Default: two intensity candidates on frames below 2^20 events, where
     // the intensity block backtracks nearly every iteration and sweeps are
@@ -980,6 +1018,18 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int fi
         CUDA_TRY(cudaGetLastError());
         return RT3D_OK;
     };
+    static thread_local FrameBatch fb_zb;
+    const uint32_t zb_bpf = F.zb ? (F.npix * F.zkb + 255u) / 256u : 0u;
+    if (F.zb) make_batch(fb_zb, Fs, n, zb_bpf, first);
+    auto zblocks = [&]() -> rt3d_status {
+        if (!F.zb) return RT3D_OK;
+        // (timed with the APSS fit class)
+        return timed_launch(s, RT3D_KC_APSS_FIT, [&]() -> rt3d_status {
+            zblock_kernel<<<zb_bpf * (uint32_t)count, 256, 0, s->stream>>>(fb_zb);
+            CUDA_TRY(cudaGetLastError());
+            return RT3D_OK;
+        });
+    };
     make_batch(fb_apss, Fs, n, (uint32_t)s->grid_apss, first);
     make_batch(fb_fit, Fs, n, (uint32_t)s->grid_fit, first);
     make_batch(fb_knn, Fs, n, (uint32_t)s->grid_knn, first);
@@ -1003,6 +1053,7 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int fi
             }
             if (!F.cfg.fuse_depth && (st = stage(ST_DEPTH, it))) return st;
             if ((st = halo(1))) return st;  // t, cells, buckets of the halo rows
+            if ((st = zblocks())) return st;
             st = timed_launch(s, RT3D_KC_APSS, [&]() -> rt3d_status {
                 apss_kernel<<<s->grid_apss * count, kNbrBlock, sizeof(ApssWarpSm) * kNbrWarps,
                               s->stream>>>(fb_apss);
@@ -1808,6 +1859,7 @@ rt3d_status rt3d_reconstruct_bands(rt3d_session* const* ss, int n, const rt3d_re
         Frame& F = Fs[k];
         F.nbands = n;
         F.band = k;
+        if (n > 1) F.zb = nullptr;  // (the depth blocks would need halo rows too)
         F.bpix0 = lo;
         F.bpix1 = lo + size;
         F.bbn0 = (uint32_t)k * (F.tb_nbn / (uint32_t)n);

@@ -193,6 +193,12 @@ struct Frame {
     uint32_t* nval;
     double* amom;     // APSS moments, kMom x amom_stride (SoA): apss_kernel -> apss_fit_kernel
     uint32_t amom_stride;
+    // depth blocks (superres frames): each pixel's points in blocks of zbs
+    // consecutive points (spawned surface by surface, s^2 per surface), the
+    // block's depth interval [min z, max z] at zb[p * zkb + k] (zblock_kernel,
+    // before each APSS launch; empty blocks (+inf, -inf)); nullptr: off
+    double2* zb;
+    uint32_t zkb, zbs;
     double* fft_re;   // 2*npix complex scratch (fft background mode)
     double* fft_im;
     // launch geometry: this frame's blocks are blk0 .. blk0 + nblk - 1 of the
@@ -269,7 +275,7 @@ struct WarpSweepSmT {
 };
 constexpr int kTopMin = 1024;  // top-of-tree values always reducible in shared memory
 constexpr int kInitCap = 256;  // matched-filter candidate lags cached per warp
-constexpr int kNbrWarpBytes = 11264;  // APSS / kNN warp scratch inside the stage kernels (ST_ITER)
+constexpr int kNbrWarpBytes = 12288;  // APSS / kNN warp scratch inside the stage kernels (ST_ITER)
 struct InitWarpSm {
     int lag[kInitCap];
     double resp[kInitCap];

@@ -48,6 +48,7 @@ struct ApssWarpSm {
     double chunk[32][4];  // the current scan chunk's members (w, x, y, z)
     RowTab rt;
     RowTab rtn[2];  // single-batch windows: this point's and the next point's rows
+    uint2 rng[128];  // depth-block candidate ranges (ball_scan_blocks)
 };
 struct KnnWarpSm {
     double d2[kKnnCap];
@@ -211,6 +212,114 @@ __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab
     }
 }
 
+// Ball of q over the window through the depth blocks (superres frames,
+// F.zb): the window's (coarse row, coarse pixel) pairs one per lane, each
+// pixel's blocks of F.zbs consecutive points whose depth interval reaches
+// [q.z - R, q.z + R] become candidate ranges (adjacent kept blocks merged),
+// compacted in ascending index order and scanned 32 ranges at a time.  A
+// block is dropped only when fl(zmin - q.z) or fl(q.z - zmax) exceeds
+// R (1 + 1e-9): by monotone rounding every point in it has dz beyond that,
+// so d^2 >= fl(dz^2) > R^2 (1 + 2^-53) >= fl(R R): no member is lost, and the
+// members come in the same ascending index order as ball_scan's.
+template <bool kXLane = true, typename Visit, typename Flush>
+__device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc, RowTab& rt,
+                                                 uint2* rng, int fi, int fj, const Pos& q,
+                                                 double r2, Visit visit, Flush flush, int Wq = -1) {
+    const int lane = threadIdx.x & 31;
+    const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W;
+    const double rw = F.cfg.R / F.pitch;
+    const double lim2 = rw * rw * (1.0 + 1e-9);
+    const double zc = F.cfg.R * (1.0 + 1e-9);
+    const uint32_t* bo = F.bo[sc];
+    const uint32_t KB = F.zkb, BS = F.zbs;
+    const int s = F.s;
+    const uint32_t lanes_le = lanemask_lt() | (1u << lane);
+    int ci0, ci1;
+    window_rows(F, fi, W, ci0, ci1);
+    for (int rb = ci0; rb <= ci1; rb += 32) {
+        // lane r: coarse row rb + r and its disc-culled coarse columns
+        // [c0, c0 + npx) (rows_load's bounds)
+        const int ci = rb + lane;
+        int c0 = 0;
+        uint32_t npx = 0;
+        if (ci <= ci1) {
+            const int r_lo = ci * s, r_hi = r_lo + s - 1;
+            const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
+            const double rem = lim2 - (double)dmin * (double)dmin;
+            if (rem >= 0.0) {
+                int wj = (int)floor(sqrt(rem));
+                wj = wj > W ? W : wj;
+                int b0 = fj - wj, b1 = fj + wj;
+                b0 = b0 < 0 ? 0 : b0;
+                b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
+                c0 = coarse_of(F, b0);
+                npx = (uint32_t)(coarse_of(F, b1) - c0 + 1);
+            }
+        }
+        uint32_t inc = npx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t ppre = inc - npx, P = __shfl_sync(0xffffffffu, inc, 31);
+        // rows with pixels are a contiguous run of lanes from the first one
+        const uint32_t pk = npx ? ppre : 0xffffffffu;
+        const uint32_t nem = __ballot_sync(0xffffffffu, npx != 0u);
+        const int fne = nem ? __ffs((int)nem) - 1 : 0;
+        for (uint32_t ub = 0; ub < P; ub += 32) {
+            // pair ub + lane: its row lane (locate's ballot / OR-reduction)
+            const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= ub)) - 1;
+            const uint32_t bit = (pk > ub && pk - ub < 32u) ? 1u << (pk - ub) : 0u;
+            const int L = fne + j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & lanes_le);
+            const uint32_t Lpre = __shfl_sync(0xffffffffu, ppre, L & 31);
+            const int Lc0 = __shfl_sync(0xffffffffu, c0, L & 31);
+            const uint32_t u = ub + (uint32_t)lane;
+            // the pixel's kept blocks as a bit mask (empty blocks hold
+            // (+inf, -inf) and are never kept), runs of kept blocks merged
+            uint32_t n0 = 0, n1 = 0, keep = 0;
+            if (u < P) {
+                const uint32_t p = (uint32_t)(rb + L) * (uint32_t)F.cols + (uint32_t)Lc0 + (u - Lpre);
+                const double2* zp = F.zb + (size_t)p * KB;
+#pragma unroll
+                for (uint32_t k = 0; k < 4u; ++k) {
+                    if (k < KB) {
+                        const double2 zz = zp[k];
+                        if (!(zz.x - q.z > zc || q.z - zz.y > zc)) keep |= 1u << k;
+                    }
+                }
+                n0 = bo[p];
+                n1 = bo[p + 1];
+            }
+            const uint32_t starts = keep & ~(keep << 1);
+            const uint32_t kc = (uint32_t)__popc(starts);
+            uint32_t kinc = kc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, kinc, o);
+                if (lane >= o) kinc += y;
+            }
+            const uint32_t KT = __shfl_sync(0xffffffffu, kinc, 31);
+            uint32_t wpos = kinc - kc;
+            for (uint32_t st = starts; st; st &= st - 1u) {
+                const int a = __ffs((int)st) - 1;
+                const int e = __ffs((int)(~keep & ~((1u << a) - 1u))) - 1;  // first dropped block after a
+                const uint32_t lo = n0 + (uint32_t)a * BS;
+                const uint32_t hi = min(n0 + (uint32_t)e * BS, n1);
+                rng[wpos++] = make_uint2(lo, hi - lo);
+            }
+            __syncwarp();
+            for (uint32_t gb = 0; gb < KT; gb += 32) {
+                const uint32_t g = gb + (uint32_t)lane;
+                const uint2 rg = g < KT ? rng[g] : make_uint2(0u, 0u);
+                const uint32_t total = rows_finish(rt, rg.x, rg.y);
+                rows_scan<kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // p[l] = p[l] + p[l+o], o = 16..1, over the warp's lanes; the sum lands in
 // lane 0 and is broadcast (oracle: lane_tree)
 __device__ __forceinline__ double warp_halving_sum(double v) {
@@ -261,7 +370,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             point(0, fi, fj, t);
             int ci0, ci1;
             window_rows(F, fi, W, ci0, ci1);
-            single_cur = ci1 - ci0 < 32;
+            single_cur = !F.zb && ci1 - ci0 < 32;
             if (single_cur) {
                 uint32_t m0r, lenr;
                 rows_load(F, sc, fi, fj, W, ci0, ci1, m0r, lenr);
@@ -289,7 +398,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         if (has_next) {
             point(j + 1, nfi, nfj, ntq);
             window_rows(F, nfi, W, nci0, nci1);
-            single_next = nci1 - nci0 < 32;
+            single_next = !F.zb && nci1 - nci0 < 32;
         }
         // pass A (denoise.hpp:172-186): the scan only collects the ball (member
         // rank order = ascending index) with its d^2 into the list; the weights
@@ -304,7 +413,8 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, d2, mfi, mfj};
         };
         auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
-        if (single) rows_scan<false>(F, tc, sc, rcur, total, q, r2, visitA, flushA);
+        if (F.zb) ball_scan_blocks<false>(F, tc, sc, A.rt, A.rng, fi, fj, q, r2, visitA, flushA);
+        else if (single) rows_scan<false>(F, tc, sc, rcur, total, q, r2, visitA, flushA);
         else ball_scan<false>(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
         if (has_next && single_next) rows_load(F, sc, nfi, nfj, W, nci0, nci1, nm0, nlen);
         auto advance = [&]() {

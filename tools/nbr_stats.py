@@ -62,3 +62,36 @@ print(json.dumps({"config": key, "points": int(len(pts)), "W": Wd,
                   "cand_mean": float(cand.mean()), "cand_p90": float(np.percentile(cand, 90)),
                   "mem_mean": float(mem.mean()), "mem_p90": float(np.percentile(mem, 90)),
                   "mem_max": int(mem.max()), "frac_mem_gt_384": float((mem > 384).mean())}))
+
+# candidates left after culling blocks of B consecutive points (aligned to
+# each coarse pixel's first point) whose depth interval misses [z - R, z + R]
+pix = pts["i"].astype(np.int64) * cols + pts["j"]
+start = np.concatenate([[0], np.cumsum(cnt.ravel())])
+z = pts["z"]
+for B in (4, 8, 9):
+    blk = (np.arange(len(pts)) - start[pix]) // B
+    key = pix * 64 + blk
+    uk, inv = np.unique(key, return_inverse=True)
+    zmin = np.full(len(uk), np.inf)
+    zmax = np.full(len(uk), -np.inf)
+    np.minimum.at(zmin, inv, z)
+    np.maximum.at(zmax, inv, z)
+    kept = np.zeros(len(qs), np.int64)
+    for n, q in enumerate(qs[:3000]):
+        a0, a1 = max(fi[q] - Wd, 0), min(fi[q] + Wd, rows * S - 1)
+        tot = 0
+        for ci in range(a0 // S, a1 // S + 1):
+            rl, rh = ci * S, ci * S + S - 1
+            dmin = rl - fi[q] if fi[q] < rl else (fi[q] - rh if fi[q] > rh else 0)
+            rem = lim2 - dmin * dmin
+            if rem < 0:
+                continue
+            wj = min(int(np.floor(np.sqrt(rem))), Wd)
+            b0, b1 = max(fj[q] - wj, 0), min(fj[q] + wj, cols * S - 1)
+            lo, hi = start[ci * cols + b0 // S], start[ci * cols + b1 // S + 1]
+            if hi > lo:
+                ii = np.arange(lo, hi)
+                ok = (zmin[inv[ii]] <= z[q] + R) & (zmax[inv[ii]] >= z[q] - R)
+                tot += int(ok.sum())
+        kept[n] = tot
+    print(json.dumps({"block": B, "cand_kept_mean": float(kept[:3000].mean())}))
