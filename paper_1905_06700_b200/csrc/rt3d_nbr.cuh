@@ -562,17 +562,17 @@ static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P,
     }
 }
 
-// ascending bitonic sort of one double per lane across the warp
-__device__ __forceinline__ double warp_sort32(double x) {
+// ascending bitonic sort of one u32 per lane across the warp
+__device__ __forceinline__ uint32_t warp_sort32(uint32_t x) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
         for (int j = size >> 1; j > 0; j >>= 1) {
-            const double y = __shfl_xor_sync(0xffffffffu, x, j);
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
             const bool up = (lane & size) == 0;  // this pair sorts ascending
             const bool low = (lane & j) == 0;    // this lane keeps the smaller
-            x = (low == up) ? (y < x ? y : x) : (y > x ? y : x);
+            x = (low == up) ? min(x, y) : max(x, y);
         }
     }
     return x;
@@ -584,20 +584,24 @@ __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k,
     const int lane = threadIdx.x & 31;
     if (cnt <= 64u) {
         // The list is in ascending index order, so the (d^2, index) order is
-        // (d^2, slot).  Lists above 32: the k-th smallest of the 32 lane minima
-        // (a lane holds slots lane and lane + 32) bounds the k-th smallest
-        // key from above, so the keys above it rank >= k.  The keys at or
-        // below it are compacted in slot order (typically ~k of them) and
-        // ranked by counting; ranks are a permutation.
+        // (d^2, slot).  Lists above 32: a threshold from the lane minima (a
+        // lane holds slots lane and lane + 32) on the high words of the keys'
+        // bits (d^2 >= 0, so the high word is monotone in d^2): at least k
+        // keys have a high word at or below the k-th smallest minimum's, so
+        // the keys above it rank >= k.  The keys at or below it are
+        // compacted in slot order (typically ~k of them) and ranked by
+        // counting; ranks are a permutation.
         const int taken = (unsigned int)k < cnt ? k : (int)cnt;
         const bool v0 = (unsigned int)lane < cnt, v1 = (unsigned int)lane + 32u < cnt;
         const double a0 = v0 ? K.d2[lane] : INFINITY, a1 = v1 ? K.d2[lane + 32] : INFINITY;
-        double tau = INFINITY;
+        const uint32_t h0 = (uint32_t)((unsigned long long)__double_as_longlong(a0) >> 32);
+        const uint32_t h1 = (uint32_t)((unsigned long long)__double_as_longlong(a1) >> 32);
+        uint32_t tau = 0xffffffffu;
         if (k <= 32 && cnt > 32u) {  // (short lists: counting over all is cheaper)
-            const double srt = warp_sort32(a0 < a1 ? a0 : a1);
+            const uint32_t srt = warp_sort32(min(h0, h1));
             tau = __shfl_sync(0xffffffffu, srt, k - 1);
         }
-        const bool in0 = v0 && a0 <= tau, in1 = v1 && a1 <= tau;
+        const bool in0 = v0 && h0 <= tau, in1 = v1 && h1 <= tau;
         const uint32_t b0 = __ballot_sync(0xffffffffu, in0), b1 = __ballot_sync(0xffffffffu, in1);
         const unsigned int c0 = (unsigned int)__popc(b0), c = c0 + (unsigned int)__popc(b1);
         // the compacted keys go to slots [64, 64 + c) of the list (cnt <= 64)
