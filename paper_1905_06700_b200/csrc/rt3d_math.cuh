@@ -99,7 +99,11 @@ __device__ __forceinline__ double apss_weight(double radius, double dist) {
 // gives x = +0 either way, so it is routed around them with the same bits.
 __device__ __forceinline__ double apss_weight_d2(double radius, double d2) {
     const bool self = d2 == 0.0;
-    double x = sqrt(self ? 1.0 : d2) / radius;
+    // d2 == +0 becomes 1.0 by OR-ing in 1.0's bits (a select would be
+    // if-converted back into sqrt(0))
+    const double dd = __longlong_as_double(__double_as_longlong(d2) |
+                                           (self ? 0x3FF0000000000000ll : 0ll));
+    double x = sqrt(dd) / radius;
     if (self) x = 0.0;
     if (x >= 1.0) return 0.0;
     double s = 1.0 - x * x;

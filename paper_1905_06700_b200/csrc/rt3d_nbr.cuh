@@ -422,7 +422,8 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             if (has_next && single_next) ntot = rows_finish(A.rtn[(j + 1) & 1u], nm0, nlen);
         };
         if (cnt <= (unsigned int)kApssList) {
-            __syncwarp();
+            // (the scans end with a warp barrier; pass B reads back only the
+            // entries this lane rewrote)
             for (unsigned int g = lane; g < cnt; g += 32) {
                 ApssMember& mb = A.u.list[g];
                 const double w = apss_weight_d2(R, mb.w);
@@ -432,7 +433,6 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                 a2 += w * ((mb.fj + 0.5) * F.pitch);
                 a3 += w * mb.z;
             }
-            __syncwarp();
         } else {  // ball larger than the list: accumulate chunk by chunk on a rescan
             unsigned int c1 = 0;
             ball_scan(
