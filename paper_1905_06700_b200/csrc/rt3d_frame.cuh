@@ -99,6 +99,9 @@ struct Ctl {
     unsigned int pown, pbase;  // this frame's (band's) own points [pbase, pbase + pown)
     int abort_op, abort_it;
     unsigned int abort_count, abort_nsweep;
+    // blocktree sweeps: block nodes handed out by ticket (by sweep parity);
+    // the last block to leave a sweep resets them
+    unsigned int wq_ticket[2], wq_done[2];
 };
 constexpr unsigned long long kBarrierTimeoutNs = 2000000000ull;
 #ifndef RT3D_BARRIER_SLEEP_NS
@@ -302,6 +305,7 @@ struct SmemT {
     unsigned int scan[kWarps + 1];
     int is_last;
     unsigned int nsweep;  // sweeps run by this kernel (blocktree buffer parity)
+    unsigned int wq;      // the block's next block-node ticket
     int aborted;          // the frame was aborted by the barrier watchdog
     Ctl c;                // this block's replica of the controller state
     double bpart[kWarps * 32];  // blocktree: the block node's pixel partials
@@ -1813,7 +1817,20 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
         // recursion of <= 32 pixels
         const int dG = F.G > F.tb_G ? F.G - F.tb_G : 0;
         const bool sub = F.tb_G >= F.G;
-        for (uint32_t bn = F.bbn0 + vblock(F); bn < F.bbn1; bn += vgrid(F)) {
+        // Many block nodes per block (large frames): nodes by ticket (results
+        // are keyed by node, so who computes which does not matter), uneven
+        // pixels even out across blocks; the next ticket is fetched while the
+        // current node is swept.  Few nodes per block: the static
+        // round-robin (a ticket's latency would sit on the critical path).
+        unsigned int* const wt = &F.ctl->wq_ticket[par];
+        const uint32_t nn = F.bbn1 - F.bbn0;
+        const bool dyn = nn >= 8u * vgrid(F);
+        if (threadIdx.x == 0) sm.wq = dyn ? atomicAdd(wt, 1u) : vblock(F);
+        __syncthreads();
+        for (uint32_t tk = sm.wq; tk < nn; tk = sm.wq) {
+            unsigned int nxt = 0;
+            if (threadIdx.x == 0) nxt = dyn ? atomicAdd(wt, 1u) : tk + vgrid(F);
+            const uint32_t bn = F.bbn0 + tk;
             uint32_t blo, bsz;
             tree_node_range(F.npix, F.tb_G, bn, blo, bsz);
             const uint32_t nch = (bsz + NG - 1) / NG;
@@ -1856,8 +1873,16 @@ __device__ void tree_sweep_g(const Frame& F, SmemT<G>& sm, const SweepCtx& X,
                 double bm = 0.0;
                 for (int w = 0; w < kWarps; ++w) bm = std_max(bm, sm.wmax[w]);
                 bmx[bn] = bm;
+                sm.wq = nxt;
             }
             __syncthreads();
+        }
+        // every block has drawn its closing ticket: the last one out resets
+        // this parity's counters (its next use is two sweeps and a grid
+        // barrier away)
+        if (dyn && threadIdx.x == 0 && atomicAdd(&F.ctl->wq_done[par], 1u) == vgrid(F) - 1) {
+            atomicExch(wt, 0u);
+            atomicExch(&F.ctl->wq_done[par], 0u);
         }
         SWEEP_STAMP(b0t0, 101);
         if (gbar(F, sm, op, it)) {
