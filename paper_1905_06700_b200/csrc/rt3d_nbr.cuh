@@ -582,56 +582,74 @@ __device__ __forceinline__ uint32_t warp_sort32(uint32_t x) {
 // (spatial_index.hpp:51-62) -> K.sel[0..taken); kth = the last key's d^2.
 __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k, double& kth) {
     const int lane = threadIdx.x & 31;
-    if (cnt <= 64u) {
-        // The list is in ascending index order, so the (d^2, index) order is
-        // (d^2, slot).  Lists above 32: a threshold from the lane minima (a
-        // lane holds slots lane and lane + 32) on the high words of the keys'
-        // bits (d^2 >= 0, so the high word is monotone in d^2): at least k
-        // keys have a high word at or below the k-th smallest minimum's, so
-        // the keys above it rank >= k.  The keys at or below it are
-        // compacted in slot order (typically ~k of them) and ranked by
-        // counting; ranks are a permutation.
+    if (cnt <= 32u) {  // rank by counting, one key per lane
         const int taken = (unsigned int)k < cnt ? k : (int)cnt;
-        const bool v0 = (unsigned int)lane < cnt, v1 = (unsigned int)lane + 32u < cnt;
-        const double a0 = v0 ? K.d2[lane] : INFINITY, a1 = v1 ? K.d2[lane + 32] : INFINITY;
-        const uint32_t h0 = (uint32_t)((unsigned long long)__double_as_longlong(a0) >> 32);
-        const uint32_t h1 = (uint32_t)((unsigned long long)__double_as_longlong(a1) >> 32);
-        uint32_t tau = 0xffffffffu;
-        if (k <= 32 && cnt > 32u) {  // (short lists: counting over all is cheaper)
-            const uint32_t srt = warp_sort32(min(h0, h1));
-            tau = __shfl_sync(0xffffffffu, srt, k - 1);
-        }
-        const bool in0 = v0 && h0 <= tau, in1 = v1 && h1 <= tau;
-        const uint32_t b0 = __ballot_sync(0xffffffffu, in0), b1 = __ballot_sync(0xffffffffu, in1);
-        const unsigned int c0 = (unsigned int)__popc(b0), c = c0 + (unsigned int)__popc(b1);
-        // the compacted keys go to slots [64, 64 + c) of the list (cnt <= 64)
-        double* cd = K.d2 + 64;
-        uint32_t* ci = K.idx + 64;
-        const uint32_t idx0 = v0 ? K.idx[lane] : 0u, idx1 = v1 ? K.idx[lane + 32] : 0u;
-        if (in0) {
-            const unsigned int p = (unsigned int)__popc(b0 & lanemask_lt());
-            cd[p] = a0;
-            ci[p] = idx0;
-        }
-        if (in1) {
-            const unsigned int p = c0 + (unsigned int)__popc(b1 & lanemask_lt());
-            cd[p] = a1;
-            ci[p] = idx1;
+        if ((unsigned int)lane < cnt) {
+            const double my = K.d2[lane];
+            int rank = 0;
+            for (unsigned int e = 0; e < cnt; ++e) {
+                const double d = K.d2[e];
+                rank += (d < my || (d == my && e < (unsigned int)lane)) ? 1 : 0;
+            }
+            if (rank < taken) K.sel[rank] = K.idx[lane];
+            if (rank == taken - 1) K.kth = my;
         }
         __syncwarp();
+        kth = taken > 0 ? K.kth : 0.0;
+        __syncwarp();
+        return taken;
+    }
+    if (cnt <= 128u) {
+        // The list is in ascending index order, so the (d^2, index) order is
+        // (d^2, slot).  A threshold from the lane minima (a lane holds slots
+        // lane + 32 e) on the high words of the keys' bits
+        // (d^2 >= 0, so the high word is monotone in d^2): at least k keys
+        // have a high word at or below the k-th smallest minimum's, so the
+        // keys above it rank >= k.  The keys at or below it are compacted in
+        // slot order (typically ~k of them) and ranked by counting; ranks are
+        // a permutation.
+        constexpr int E = 4;
+        const int taken = (unsigned int)k < cnt ? k : (int)cnt;
+        double a[E];
+        uint32_t h[E];
+        uint32_t hmin = 0xffffffffu;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const unsigned int sl = (unsigned int)lane + 32u * h;
-            if (sl < c) {
-                const double my = cd[sl];
-                int rank = 0;
-                for (unsigned int e = 0; e < c; ++e) {
-                    const double d = cd[e];
-                    rank += (d < my || (d == my && e < sl)) ? 1 : 0;
-                }
-                if (rank < taken) K.sel[rank] = ci[sl];
-                if (rank == taken - 1) K.kth = my;
+        for (int e = 0; e < E; ++e) {
+            const bool v = (unsigned int)lane + 32u * e < cnt;
+            a[e] = v ? K.d2[lane + 32 * e] : INFINITY;
+            h[e] = v ? (uint32_t)((unsigned long long)__double_as_longlong(a[e]) >> 32) : 0xffffffffu;
+            hmin = min(hmin, h[e]);
+        }
+        uint32_t tau = 0xffffffffu;
+        if (k <= 32) {
+            const uint32_t srt = warp_sort32(hmin);
+            tau = __shfl_sync(0xffffffffu, srt, k - 1);
+        }
+        // the compacted keys go to slots [128, 128 + c) of the list
+        double* cd = K.d2 + 128;
+        uint32_t* ci = K.idx + 128;
+        unsigned int c = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const bool in = (unsigned int)lane + 32u * e < cnt && h[e] <= tau;
+            const uint32_t bal = __ballot_sync(0xffffffffu, in);
+            if (in) {
+                const unsigned int p = c + (unsigned int)__popc(bal & lanemask_lt());
+                cd[p] = a[e];
+                ci[p] = K.idx[lane + 32 * e];
             }
+            c += (unsigned int)__popc(bal);
+        }
+        __syncwarp();
+        for (unsigned int sl = (unsigned int)lane; sl < c; sl += 32u) {
+            const double my = cd[sl];
+            int rank = 0;
+            for (unsigned int e = 0; e < c; ++e) {
+                const double d = cd[e];
+                rank += (d < my || (d == my && e < sl)) ? 1 : 0;
+            }
+            if (rank < taken) K.sel[rank] = ci[sl];
+            if (rank == taken - 1) K.kth = my;
         }
         __syncwarp();
         kth = taken > 0 ? K.kth : 0.0;
