@@ -1056,8 +1056,8 @@ static int project_sphere(const sphere_t* s, double eps, const double p[3], doub
     return 1;
 }
 
-#define APSS_LANES 32
-/* the halving tree over 32 lane partials: p[l] += p[l + o], o = 16 .. 1 */
+#define APSS_LANES 16
+/* the halving tree over APSS_LANES lane partials: p[l] += p[l + o], o = APSS_LANES/2 .. 1 */
 static double lane_tree(const double* base, int stride, int col) {
     double p[APSS_LANES];
     for (int l = 0; l < APSS_LANES; ++l) p[l] = base[l * stride + col];
@@ -1098,8 +1098,8 @@ int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_par
             w = (double*)realloc(w, sizeof(double) * qcap);
         }
         /* Summation order (shared with the device kernel, rt3d_nbr.cuh): ball
-         * member m (ascending index) is accumulated into lane m mod 32,
-         * sequentially; the 32 lane partials are then combined by the halving
+         * member m (ascending index) is accumulated into lane m mod APSS_LANES (16),
+         * sequentially; the lane partials are then combined by the halving
          * tree of lane_tree().  The reference sums each moment sequentially
          * (denoise.hpp:174-180, 191-194, 74-80); the reassociation moves the
          * moments at the 1e-16 relative level, far below the eigen-solver

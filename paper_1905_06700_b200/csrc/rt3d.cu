@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kNbrBlock, RT3D_APSS_MIN_BLOCKS) apss_kernel(c
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_APSS);
     apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase),
-                      ld_cg(&F.ctl->pown), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc));
+                      ld_cg(&F.ctl->pown), ld_cg(&F.ctl->tc), ld_cg(&F.ctl->sc), kNbrWarps);
 }
 
 __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(const __grid_constant__ FrameBatch FB) {
@@ -702,8 +702,9 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     F.cols = s->cols;
     F.bins = s->bins;
     F.s = s->s;
-    if ((uint64_t)s->rows * (uint64_t)s->s >= (1ull << 20) || (uint64_t)s->cols * (uint64_t)s->s >= (1ull << 20))
-        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: fine grids of 2^20 or more rows or columns are not supported");
+    // (APSS packs a member's fine cell into 16 + 16 bits)
+    if ((uint64_t)s->rows * (uint64_t)s->s > 65535ull || (uint64_t)s->cols * (uint64_t)s->s > 65535ull)
+        return fail(RT3D_ERR_UNSUPPORTED, "rt3d: fine grids of more than 65535 rows or columns are not supported");
     F.smag = s->s > 1 ? (uint32_t)(((1ull << 32) + (uint64_t)s->s - 1) / (uint64_t)s->s) : 0u;
     F.frows = s->rows * s->s;
     F.fcols = s->cols * s->s;

@@ -278,7 +278,9 @@ struct WarpSweepSmT {
 };
 constexpr int kTopMin = 1024;  // top-of-tree values always reducible in shared memory
 constexpr int kInitCap = 256;  // matched-filter candidate lags cached per warp
-constexpr int kNbrWarpBytes = 12288;  // APSS / kNN warp scratch inside the stage kernels (ST_ITER)
+// APSS / kNN scratch inside the stage kernels (ST_ITER): a block's worth, the
+// kNN's 8 warps or the APSS's first kNbrBlockBytes / sizeof(ApssWarpSm) warps
+constexpr int kNbrBlockBytes = 57344;
 struct InitWarpSm {
     int lag[kInitCap];
     double resp[kInitCap];
@@ -298,7 +300,7 @@ struct SmemT {
         InitWarpSm init[kWarps];
         // APSS / kNN phases of ST_ITER (not instantiated for G == 1, whose
         // small footprint lets more blocks share an SM)
-        alignas(16) unsigned char nbr[G == 1 ? 16 : kWarps * kNbrWarpBytes];
+        alignas(16) unsigned char nbr[G == 1 ? 16 : kNbrBlockBytes];
     } u;
     double node[kWarps];
     double wmax[kWarps];
@@ -2025,6 +2027,10 @@ __device__ __forceinline__ void for_each_pinned_neighbor(const Frame& F, int tc,
 }
 
 constexpr int kMom = 19;        // APSS moments: wsum, mean(3), M(15)
+// APSS summation lanes: ball member m is accumulated into lane partial
+// m mod kApssLanes, the partials combined by the halving tree (the oracle's
+// APSS_LANES); the device kernel runs 16 lanes per point
+constexpr int kApssLanes = 16;
 constexpr int kRedStride = 15;  // APSS pass-B partials per lane (M, lower triangle)
 
 // Pratt moments of one member centred on the mean, (w d_r) d_c with
@@ -2059,8 +2065,8 @@ __device__ __forceinline__ void cov_from_moments(const double* M, double wsum, d
 
 // the halving tree over 32 lane partials (column `col` of p[32][stride]):
 // p[l] = p[l] + p[l+o], o = 16..1 (oracle: lane_tree)
-__device__ __forceinline__ double halving_sum32(double* p, int stride, int col) {
-    for (int o = 16; o > 0; o >>= 1)
+__device__ __forceinline__ double halving_sum_lanes(double* p, int stride, int col) {
+    for (int o = kApssLanes / 2; o > 0; o >>= 1)
         for (int l = 0; l < o; ++l) p[l * stride + col] = p[l * stride + col] + p[(l + o) * stride + col];
     return p[col];
 }
@@ -2074,11 +2080,11 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
                                            double eps, uint8_t& flags, Pos& out) {
     const double r2 = R * R;
     unsigned int cnt = 0;
-    double pa[32][4];
-    for (int l = 0; l < 32; ++l) pa[l][0] = pa[l][1] = pa[l][2] = pa[l][3] = 0.0;
+    double pa[kApssLanes][4];
+    for (int l = 0; l < kApssLanes; ++l) pa[l][0] = pa[l][1] = pa[l][2] = pa[l][3] = 0.0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
         const double w = apss_weight_d2(R, d2);
-        double* a = pa[cnt & 31u];
+        double* a = pa[cnt % (unsigned int)kApssLanes];
         ++cnt;
         a[0] += w;
         a[1] += w * o.x;
@@ -2089,9 +2095,9 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
         flags |= 1u;
         return false;
     }
-    const double wsum = halving_sum32(&pa[0][0], 4, 0);
-    double m0 = halving_sum32(&pa[0][0], 4, 1), m1 = halving_sum32(&pa[0][0], 4, 2),
-           m2 = halving_sum32(&pa[0][0], 4, 3);
+    const double wsum = halving_sum_lanes(&pa[0][0], 4, 0);
+    double m0 = halving_sum_lanes(&pa[0][0], 4, 1), m1 = halving_sum_lanes(&pa[0][0], 4, 2),
+           m2 = halving_sum_lanes(&pa[0][0], 4, 3);
     if (wsum <= 0.0) {
         flags |= 4u;
         return false;
@@ -2099,16 +2105,16 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
     m0 /= wsum;
     m1 /= wsum;
     m2 /= wsum;
-    double pb[32][kRedStride];
-    for (int l = 0; l < 32; ++l)
+    double pb[kApssLanes][kRedStride];
+    for (int l = 0; l < kApssLanes; ++l)
         for (int e = 0; e < kRedStride; ++e) pb[l][e] = 0.0;
     unsigned int c2 = 0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        apss_pass_b(pb[c2 & 31u], apss_weight_d2(R, d2), o.x, o.y, o.z, m0, m1, m2);
+        apss_pass_b(pb[c2 % (unsigned int)kApssLanes], apss_weight_d2(R, d2), o.x, o.y, o.z, m0, m1, m2);
         ++c2;
     });
     double cv[6], M[15];
-    for (int e = 0; e < 15; ++e) M[e] = halving_sum32(&pb[0][0], kRedStride, e);
+    for (int e = 0; e < 15; ++e) M[e] = halving_sum_lanes(&pb[0][0], kRedStride, e);
     cov_from_moments(M, wsum, cv);
     double e0, e1, e2;
     sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);

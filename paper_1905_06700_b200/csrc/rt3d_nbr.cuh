@@ -3,21 +3,22 @@
 // as stand-alone high-occupancy kernels, launched between the cooperative
 // stage kernels of a frame.
 //
-// Work mapping: one warp per point.  Inside PALM every point sits at its
-// fine-pixel centre, so SpatialIndex::query's ball (spatial_index.hpp:31-47,
-// exact |q-p|^2 <= R^2, ascending index) is found among the points of the
-// coarse pixels under the fine window [fi-W, fi+W] x [fj-W, fj+W],
-// W = floor(R/pitch)+1.  The window's rows are contiguous index ranges (the
-// cloud is pixel-major); the warp concatenates them and scans 32 candidates
-// at a time (coalesced loads), compacting the members of each chunk with a
-// ballot in ascending index order.
+// Work mapping: a lane group per point (kNN: a warp; APSS: 16 lanes, two
+// points per warp).  Inside PALM every point sits at its fine-pixel centre, so
+// SpatialIndex::query's ball (spatial_index.hpp:31-47, exact |q-p|^2 <= R^2,
+// ascending index) is found among the points of the coarse pixels under the
+// fine window [fi-W, fi+W] x [fj-W, fj+W], W = floor(R/pitch)+1.  The
+// window's rows are contiguous index ranges (the cloud is pixel-major); the
+// group concatenates them and scans one candidate per lane at a time
+// (coalesced loads), compacting the members of each chunk with a ballot in
+// ascending index order.
 //
-// APSS moments: ball member m (ascending index) is accumulated by lane
-// m mod 32, sequentially; the 32 lane partials are combined by the halving
-// tree p[l] += p[l+o], o = 16..1.  The oracle uses the same order
-// (oracle/rt3d_oracle.c, lane_tree), so device and oracle agree bit for bit.
-// The sphere fit and projection then run one thread per point
-// (apss_fit_kernel) from the moments staged in HBM/L2.
+// APSS moments: ball member m (ascending index) is accumulated by the group's
+// lane m mod 16, sequentially; the 16 lane partials are combined by the
+// halving tree p[l] += p[l+o], o = 8..1.  The oracle uses the same order
+// (oracle/rt3d_oracle.c, lane_tree, APSS_LANES), so device and oracle agree
+// bit for bit.  The sphere fit and projection then run one thread per point
+// (apss_fit_kernel) from the moments staged in L2.
 #pragma once
 
 #include "rt3d_frame.cuh"
@@ -29,26 +30,50 @@ constexpr int kNbrWarps = kNbrBlock / 32;
 constexpr int kKnnCap = 384;     // per-warp ball list for the kNN selection
 constexpr int kFitBlock = 128;
 
+// Lane groups of GW lanes scanning one point's window each: GW = 32 (kNN, a
+// warp per point) or 16 (APSS, two points per warp).  Warp-collective
+// operations run over the whole warp; each group reads its own field of a
+// ballot, and every loop that contains one runs to the larger of the two
+// groups' trip counts (the shorter group idles, predicated off).
+template <int GW>
+struct Grp {
+    static_assert(GW == 16 || GW == 32, "lane groups of 16 or 32");
+    __device__ static __forceinline__ int gl() { return (int)(threadIdx.x & (GW - 1)); }
+    __device__ static __forceinline__ int base() { return GW == 32 ? 0 : (int)(threadIdx.x & 16u); }
+    // this group's bits of a full-warp ballot
+    __device__ static __forceinline__ uint32_t field(uint32_t b) {
+        return GW == 32 ? b : (b >> base()) & 0xFFFFu;
+    }
+    __device__ static __forceinline__ uint32_t lt() { return (1u << gl()) - 1u; }
+    __device__ static __forceinline__ uint32_t le() { return (2u << gl()) - 1u; }
+    // the larger of the two groups' values (warp-uniform)
+    __device__ static __forceinline__ uint32_t wmax(uint32_t v) {
+        return GW == 32 ? v : max(v, __shfl_xor_sync(0xffffffffu, v, 16));
+    }
+};
+
 struct RowTab {
     // the batch's non-empty rows, compacted in row order
     uint32_t pre[32];  // rank of the row's first candidate (strictly increasing)
     uint32_t m0[32];   // index of the row's first candidate
     uint32_t n;        // number of non-empty rows
 };
-struct ApssMember {
-    double z, w;
-    int32_t fi, fj;
+
+// APSS: two points per warp, 16 lanes each (see apss_moment_warps)
+constexpr int kApssGW = kApssLanes;
+constexpr int kApssCap = 256;  // ball members kept per point for the dense passes
+struct ApssList {
+    double z[kApssCap], w[kApssCap];  // member depth, d^2 then weight
+    uint32_t fij[kApssCap];           // member fine cell, fi << 16 | fj
 };
-constexpr int kApssList = 384;  // ball members kept per warp for the second pass
 struct ApssWarpSm {
     union {
-        ApssMember list[kApssList];
-        double red[32][kRedStride];  // lane partials, after the list is consumed
+        ApssList list[2];            // one per lane group
+        double red[32][kRedStride];  // lane partials, after the lists are consumed
     } u;
-    double chunk[32][4];  // the current scan chunk's members (w, x, y, z)
-    RowTab rt;
-    RowTab rtn[2];  // single-batch windows: this point's and the next point's rows
-    uint2 rng[128];  // depth-block candidate ranges (ball_scan_blocks)
+    double chunk[32][4];  // the current scan chunk's members (w, x, y, z), a group's 16 slots
+    RowTab rt[2];
+    uint2 rng[2][64];  // depth-block candidate ranges (ball_scan_blocks)
 };
 struct KnnWarpSm {
     double d2[kKnnCap];
@@ -75,14 +100,16 @@ __device__ __forceinline__ void window_rows(const Frame& F, int fi, int W, int& 
     ci1 = coarse_of(F, a1);
 }
 
-// Candidate range of window row ci = rb + lane (disc-culled columns): the
-// global loads of a row batch, kept in registers until rows_finish.
+// Candidate range of window row ci = rb + (lane in group) (disc-culled
+// columns): the global loads of a row batch, kept in registers until
+// rows_finish.
+template <int GW>
 __device__ __forceinline__ void rows_load(const Frame& F, int sc, int fi, int fj, int W, int rb,
                                           int ci1, uint32_t& m0, uint32_t& len) {
-    const int lane = threadIdx.x & 31, s = F.s;
+    const int s = F.s;
     const double rw = F.cfg.R / F.pitch;
     const double lim2 = rw * rw * (1.0 + 1e-9);
-    const int ci = rb + lane;
+    const int ci = rb + Grp<GW>::gl();
     m0 = 0;
     len = 0;
     if (ci <= ci1) {
@@ -107,64 +134,70 @@ __device__ __forceinline__ void rows_load(const Frame& F, int sc, int fi, int fj
     }
 }
 
-// prefix of the row batch into rt; returns the batch's candidate count
+// prefix of the group's row batch into rt (non-empty rows compacted);
+// returns the batch's candidate count
+template <int GW>
 __device__ __forceinline__ uint32_t rows_finish(RowTab& rt, uint32_t m0, uint32_t len) {
-    const int lane = threadIdx.x & 31;
+    using G = Grp<GW>;
+    const int gl = G::gl();
     uint32_t inc = len;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
+    for (int o = 1; o < GW; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, GW);
+        if (gl >= o) inc += y;
     }
-    const uint32_t ne = __ballot_sync(0xffffffffu, len != 0u);
+    const uint32_t ne = G::field(__ballot_sync(0xffffffffu, len != 0u));
     if (len) {
-        const int cp = __popc(ne & lanemask_lt());
+        const int cp = __popc(ne & G::lt());
         rt.pre[cp] = inc - len;
         rt.m0[cp] = m0;
     }
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    if (lane == 0) rt.n = (uint32_t)__popc(ne);
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, GW - 1, GW);
+    if (gl == 0) rt.n = (uint32_t)__popc(ne);
     __syncwarp();
     return total;
 }
 
-// The candidates of one row batch (rt, total) against q: visit(rank, mm,
-// pos, d2, fi, fj) on member lanes, flush(n_members) once per chunk of 32
+// The candidates of the group's row batch (rt, total) against q: visit(rank,
+// mm, pos, d2, fi, fj) on member lanes, flush(n_members) once per chunk of GW
 // candidates (warp-synchronous); the next chunk's loads are issued before the
 // current chunk is processed.  kXLane: flush reads what other lanes' visits
 // wrote (warp barriers around it); list builders that only write their own
 // slots skip those barriers and synchronise once after the scan.
-template <bool kXLane = true, typename Visit, typename Flush>
+template <int GW, bool kXLane, typename Visit, typename Flush>
 __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const RowTab& rt,
                                           uint32_t total, const Pos& q, double r2, Visit visit,
                                           Flush flush) {
-    const int lane = threadIdx.x & 31;
+    using G = Grp<GW>;
+    const int gl = G::gl();
     const double* tt = F.t[tc];
     const int32_t* FI = F.fi[sc];
     const int32_t* FJ = F.fj[sc];
-    // lane k holds non-empty row k: its first rank pk and rank -> index
-    // offset dk.  The row of candidate fb + l is the row holding fb plus the
-    // rows starting in (fb, fb + l]: a ballot, an OR-reduction of the start
-    // offsets inside the chunk and a popcount, then one shuffle.
-    const bool hr = (uint32_t)lane < rt.n;
-    const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
-    const uint32_t dk = hr ? rt.m0[lane] - pk : 0u;
-    const uint32_t lanes_le = lanemask_lt() | (1u << lane);
-    auto locate = [&](uint32_t fb) -> uint32_t {  // warp-collective: candidate fb + lane
-        const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= fb)) - 1;
-        const uint32_t bit = (pk > fb && pk - fb < 32u) ? 1u << (pk - fb) : 0u;
-        const int j = j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & lanes_le);
-        return fb + (uint32_t)lane + __shfl_sync(0xffffffffu, dk, j);
+    // lane k of the group holds non-empty row k: its first rank pk and
+    // rank -> index offset dk.  The row of candidate fb + l is the row
+    // holding fb plus the rows starting in (fb, fb + l]: a ballot, an
+    // OR-reduction of the start offsets inside the chunk and a popcount,
+    // then one shuffle.
+    const bool hr = (uint32_t)gl < rt.n;
+    const uint32_t pk = hr ? rt.pre[gl] : 0xffffffffu;
+    const uint32_t dk = hr ? rt.m0[gl] - pk : 0u;
+    const uint32_t lanes_le = G::le();
+    auto locate = [&](uint32_t fb) -> uint32_t {  // warp-collective: candidate fb + gl
+        const int j0 = __popc(G::field(__ballot_sync(0xffffffffu, pk <= fb))) - 1;
+        const uint32_t bit = (pk > fb && pk - fb < (uint32_t)GW) ? 1u << (pk - fb + G::base()) : 0u;
+        const int j = j0 + __popc(G::field(__reduce_or_sync(0xffffffffu, bit)) & lanes_le);
+        return fb + (uint32_t)gl + __shfl_sync(0xffffffffu, dk, j & (GW - 1), GW);
     };
-    bool v = (uint32_t)lane < total;
+    const uint32_t tmax = G::wmax(total);
+    bool v = (uint32_t)gl < total;
     uint32_t mm = locate(0u);
     RT3D_CHECK(!v || mm < F.pcap);
     int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
     double ctt = v ? tt[mm] : 0.0;
-    for (uint32_t fb = 0; fb < total; fb += 32) {
-        const uint32_t f2 = fb + 32 + lane;
+    for (uint32_t fb = 0; fb < tmax; fb += GW) {
+        const uint32_t f2 = fb + GW + (uint32_t)gl;
         const bool v2 = f2 < total;
-        const uint32_t mm2 = locate(fb + 32u);
+        const uint32_t mm2 = locate(fb + GW);
         RT3D_CHECK(!v2 || mm2 < F.pcap);
         const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
         const double ntt = v2 ? tt[mm2] : 0.0;
@@ -179,9 +212,10 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
             d2 = dx * dx + dy * dy + dz * dz;
             ok = d2 <= r2;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, ok);
-        if (bal) {
-            if (ok) visit(__popc(bal & lanemask_lt()), mm, o, d2, cfi, cfj);
+        const uint32_t wb = __ballot_sync(0xffffffffu, ok);
+        if (wb) {
+            const uint32_t bal = G::field(wb);
+            if (ok) visit(__popc(bal & G::lt()), mm, o, d2, cfi, cfj);
             if (kXLane) __syncwarp();
             flush(__popc(bal));
             if (kXLane) __syncwarp();
@@ -195,20 +229,28 @@ __device__ __forceinline__ void rows_scan(const Frame& F, int tc, int sc, const 
     __syncwarp();
 }
 
-// Ball of q over the window, all row batches.
-template <bool kXLane = true, typename Visit, typename Flush>
+// Ball of q over the window, all row batches (act false: an empty window,
+// the group only takes part in the warp's collectives).
+template <int GW, bool kXLane, typename Visit, typename Flush>
 __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab& rt, int fi,
                                           int fj, const Pos& q, double r2, Visit visit,
-                                          Flush flush, int Wq = -1) {
+                                          Flush flush, int Wq = -1, bool act = true) {
     // Wq < W restricts the scan to the fine window of half-width Wq (kNN)
     const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W;
     int ci0, ci1;
     window_rows(F, fi, W, ci0, ci1);
-    for (int rb = ci0; rb <= ci1; rb += 32) {
+    if (!act) {
+        ci0 = 0;
+        ci1 = -1;
+    }
+    const uint32_t nb = ci1 >= ci0 ? (uint32_t)((ci1 - ci0) / GW + 1) : 0u;
+    const uint32_t nbm = Grp<GW>::wmax(nb);
+    for (uint32_t b = 0; b < nbm; ++b) {
+        const int rb = ci0 + (int)b * GW;
         uint32_t m0, len;
-        rows_load(F, sc, fi, fj, W, rb, ci1, m0, len);
-        const uint32_t total = rows_finish(rt, m0, len);
-        rows_scan<kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
+        rows_load<GW>(F, sc, fi, fj, W, rb, ci1, m0, len);
+        const uint32_t total = rows_finish<GW>(rt, m0, len);
+        rows_scan<GW, kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
     }
 }
 
@@ -216,16 +258,18 @@ __device__ __forceinline__ void ball_scan(const Frame& F, int tc, int sc, RowTab
 // F.zb): the window's (coarse row, coarse pixel) pairs one per lane, each
 // pixel's blocks of F.zbs consecutive points whose depth interval reaches
 // [q.z - R, q.z + R] become candidate ranges (adjacent kept blocks merged),
-// compacted in ascending index order and scanned 32 ranges at a time.  A
+// compacted in ascending index order and scanned GW ranges at a time.  A
 // block is dropped only when fl(zmin - q.z) or fl(q.z - zmax) exceeds
 // R (1 + 1e-9): by monotone rounding every point in it has dz beyond that,
 // so d^2 >= fl(dz^2) > R^2 (1 + 2^-53) >= fl(R R): no member is lost, and the
 // members come in the same ascending index order as ball_scan's.
-template <bool kXLane = true, typename Visit, typename Flush>
+template <int GW, bool kXLane, typename Visit, typename Flush>
 __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc, RowTab& rt,
                                                  uint2* rng, int fi, int fj, const Pos& q,
-                                                 double r2, Visit visit, Flush flush, int Wq = -1) {
-    const int lane = threadIdx.x & 31;
+                                                 double r2, Visit visit, Flush flush, int Wq = -1,
+                                                 bool act = true) {
+    using G = Grp<GW>;
+    const int gl = G::gl();
     const int W = Wq >= 0 && Wq < F.cfg.W ? Wq : F.cfg.W;
     const double rw = F.cfg.R / F.pitch;
     const double lim2 = rw * rw * (1.0 + 1e-9);
@@ -233,13 +277,20 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
     const uint32_t* bo = F.bo[sc];
     const uint32_t KB = F.zkb, BS = F.zbs;
     const int s = F.s;
-    const uint32_t lanes_le = lanemask_lt() | (1u << lane);
+    const uint32_t lanes_le = G::le();
     int ci0, ci1;
     window_rows(F, fi, W, ci0, ci1);
-    for (int rb = ci0; rb <= ci1; rb += 32) {
+    if (!act) {
+        ci0 = 0;
+        ci1 = -1;
+    }
+    const uint32_t nrb = ci1 >= ci0 ? (uint32_t)((ci1 - ci0) / GW + 1) : 0u;
+    const uint32_t nrbm = G::wmax(nrb);
+    for (uint32_t rbi = 0; rbi < nrbm; ++rbi) {
         // lane r: coarse row rb + r and its disc-culled coarse columns
         // [c0, c0 + npx) (rows_load's bounds)
-        const int ci = rb + lane;
+        const int rb = ci0 + (int)rbi * GW;
+        const int ci = rb + gl;
         int c0 = 0;
         uint32_t npx = 0;
         if (ci <= ci1) {
@@ -258,23 +309,24 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
         }
         uint32_t inc = npx;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+        for (int o = 1; o < GW; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o, GW);
+            if (gl >= o) inc += y;
         }
-        const uint32_t ppre = inc - npx, P = __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t ppre = inc - npx, P = __shfl_sync(0xffffffffu, inc, GW - 1, GW);
         // rows with pixels are a contiguous run of lanes from the first one
         const uint32_t pk = npx ? ppre : 0xffffffffu;
-        const uint32_t nem = __ballot_sync(0xffffffffu, npx != 0u);
+        const uint32_t nem = G::field(__ballot_sync(0xffffffffu, npx != 0u));
         const int fne = nem ? __ffs((int)nem) - 1 : 0;
-        for (uint32_t ub = 0; ub < P; ub += 32) {
-            // pair ub + lane: its row lane (locate's ballot / OR-reduction)
-            const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= ub)) - 1;
-            const uint32_t bit = (pk > ub && pk - ub < 32u) ? 1u << (pk - ub) : 0u;
-            const int L = fne + j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & lanes_le);
-            const uint32_t Lpre = __shfl_sync(0xffffffffu, ppre, L & 31);
-            const int Lc0 = __shfl_sync(0xffffffffu, c0, L & 31);
-            const uint32_t u = ub + (uint32_t)lane;
+        const uint32_t Pm = G::wmax(P);
+        for (uint32_t ub = 0; ub < Pm; ub += GW) {
+            // pair ub + gl: its row lane (locate's ballot / OR-reduction)
+            const int j0 = __popc(G::field(__ballot_sync(0xffffffffu, pk <= ub))) - 1;
+            const uint32_t bit = (pk > ub && pk - ub < (uint32_t)GW) ? 1u << (pk - ub + G::base()) : 0u;
+            const int L = fne + j0 + __popc(G::field(__reduce_or_sync(0xffffffffu, bit)) & lanes_le);
+            const uint32_t Lpre = __shfl_sync(0xffffffffu, ppre, L & (GW - 1), GW);
+            const int Lc0 = __shfl_sync(0xffffffffu, c0, L & (GW - 1), GW);
+            const uint32_t u = ub + (uint32_t)gl;
             // the pixel's kept blocks as a bit mask (empty blocks hold
             // (+inf, -inf) and are never kept), runs of kept blocks merged
             uint32_t n0 = 0, n1 = 0, keep = 0;
@@ -295,11 +347,11 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
             const uint32_t kc = (uint32_t)__popc(starts);
             uint32_t kinc = kc;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, kinc, o);
-                if (lane >= o) kinc += y;
+            for (int o = 1; o < GW; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, kinc, o, GW);
+                if (gl >= o) kinc += y;
             }
-            const uint32_t KT = __shfl_sync(0xffffffffu, kinc, 31);
+            const uint32_t KT = __shfl_sync(0xffffffffu, kinc, GW - 1, GW);
             uint32_t wpos = kinc - kc;
             for (uint32_t st = starts; st; st &= st - 1u) {
                 const int a = __ffs((int)st) - 1;
@@ -309,145 +361,125 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
                 rng[wpos++] = make_uint2(lo, hi - lo);
             }
             __syncwarp();
-            for (uint32_t gb = 0; gb < KT; gb += 32) {
-                const uint32_t g = gb + (uint32_t)lane;
+            const uint32_t KTm = G::wmax(KT);
+            for (uint32_t gb = 0; gb < KTm; gb += GW) {
+                const uint32_t g = gb + (uint32_t)gl;
                 const uint2 rg = g < KT ? rng[g] : make_uint2(0u, 0u);
-                const uint32_t total = rows_finish(rt, rg.x, rg.y);
-                rows_scan<kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
+                const uint32_t total = rows_finish<GW>(rt, rg.x, rg.y);
+                rows_scan<GW, kXLane>(F, tc, sc, rt, total, q, r2, visit, flush);
             }
             __syncwarp();
         }
     }
 }
 
-// p[l] = p[l] + p[l+o], o = 16..1, over the warp's lanes; the sum lands in
-// lane 0 and is broadcast (oracle: lane_tree)
-__device__ __forceinline__ double warp_halving_sum(double v) {
+// p[l] = p[l] + p[l+o], o = GW/2..1, over the group's lanes; the sum lands
+// in the group's lane 0 and is broadcast (oracle: lane_tree)
+template <int GW>
+__device__ __forceinline__ double group_halving_sum(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
-    return __shfl_sync(0xffffffffu, v, 0);
+    for (int o = GW / 2; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o, GW);
+    return __shfl_sync(0xffffffffu, v, 0, GW);
 }
 
-// APSS moments over the current state: warp per point, results to F.amom
-// (kMom doubles per point, one coalesced store per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower, row-major;
-// the covariance is read off M, see apss_pass_b).
-// points [pb, pb + P) (a band's own points; pb = 0 for a whole frame)
+// APSS moments over the current state, two points per warp (16 lanes each:
+// the per-point work that does not scale with the ball, row tables, the
+// reductions, the stores, is issued once for both), results to F.amom (kMom
+// doubles per point): [0] wsum (-1: isolated), [1..3] mean, [4..18] M (lower,
+// row-major; the covariance is read off M, see apss_pass_b).  Summation
+// order: ball member m (ascending index) on the group's lane m mod 16, the 16
+// lane partials combined by the halving tree (oracle: APSS_LANES 16).
+// Points [pb, pb + P) (a band's own points; pb = 0 for a whole frame); wpb:
+// warps per block taking part (the rest return).
 static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32_t pb, uint32_t P,
-                                         int tc, int sc) {
+                                         int tc, int sc, uint32_t wpb) {
+    using G = Grp<kApssGW>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if ((uint32_t)warp >= wpb) return;
+    const int gl = G::gl(), grp = lane >> 4;
     ApssWarpSm& A = wsm[warp];
-    const uint32_t wpb = blockDim.x >> 5;
+    ApssList& L = A.u.list[grp];
     const uint32_t gw = vblock(F) * wpb + warp, nw = vgrid(F) * wpb;
     const double R = F.cfg.R, r2 = R * R;
-    (void)F.amom_stride;
-    const int W = F.cfg.W;
-    // the warp's points n_j = gw + j nw: positions preloaded 32 at a time (lane
-    // j holds point j's), and a single-batch window's rows are loaded for the
-    // next point while this point's second pass computes
+    const double pitch = F.pitch;
+    // the warp's pairs gw + j nw, points 2 pair + group: positions preloaded
+    // 16 pairs at a time (lane 2 i + g holds pair jbase + i's point g)
     int pfi = 0, pfj = 0;
     double pt = 0.0;
     uint32_t jbase = 0xffffffffu;
-    auto point = [&](uint32_t j, int& fi, int& fj, double& t) {
-        if ((j & ~31u) != jbase) {
-            jbase = j & ~31u;
-            const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
+    for (uint32_t j = 0;; ++j) {
+        const uint32_t pair = gw + j * nw;
+        if (2u * pair >= P) break;  // (warp-uniform)
+        if ((j & ~15u) != jbase) {
+            jbase = j & ~15u;
+            const uint32_t nl = 2u * (gw + (jbase + (uint32_t)(lane >> 1)) * nw) + (uint32_t)(lane & 1);
             if (nl < P) {
                 pfi = F.fi[sc][pb + nl];
                 pfj = F.fj[sc][pb + nl];
                 pt = F.t[tc][pb + nl];
             }
         }
-        fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
-        fj = __shfl_sync(0xffffffffu, pfj, (int)(j & 31u));
-        t = __shfl_sync(0xffffffffu, pt, (int)(j & 31u));
-    };
-    uint32_t ntot = 0;     // rows of the current point when single_cur
-    bool single_cur = false;
-    {
-        if (gw < P) {
-            int fi, fj;
-            double t;
-            point(0, fi, fj, t);
-            int ci0, ci1;
-            window_rows(F, fi, W, ci0, ci1);
-            single_cur = !F.zb && ci1 - ci0 < 32;
-            if (single_cur) {
-                uint32_t m0r, lenr;
-                rows_load(F, sc, fi, fj, W, ci0, ci1, m0r, lenr);
-                ntot = rows_finish(A.rtn[0], m0r, lenr);
-            }
-        }
-    }
-    uint32_t j = 0;
-    for (uint32_t nl = gw; nl < P; nl += nw, ++j) {
+        const int src = (int)((j & 15u) << 1) | grp;
+        const int fi = __shfl_sync(0xffffffffu, pfi, src);
+        const int fj = __shfl_sync(0xffffffffu, pfj, src);
+        const double tq = __shfl_sync(0xffffffffu, pt, src);
+        const uint32_t nl = 2u * pair + (uint32_t)grp;
+        const bool act = nl < P;
         const uint32_t n = pb + nl;
-        RT3D_CHECK(n < F.pcap);
-        int fi, fj;
-        double tq;
-        point(j, fi, fj, tq);
-        const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, tq * F.bres};
-        RowTab& rcur = A.rtn[j & 1u];
-        const bool single = single_cur;
-        const uint32_t total = ntot;
-        // next point: positions and (single batch) row loads, finished after pass B
-        const bool has_next = nl + nw < P;
-        int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
-        double ntq = 0.0;
-        bool single_next = false;
-        uint32_t nm0 = 0, nlen = 0;
-        if (has_next) {
-            point(j + 1, nfi, nfj, ntq);
-            window_rows(F, nfi, W, nci0, nci1);
-            single_next = !F.zb && nci1 - nci0 < 32;
-        }
+        RT3D_CHECK(!act || n < F.pcap);
+        const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, tq * F.bres};
         // pass A (denoise.hpp:172-186): the scan only collects the ball (member
-        // rank order = ascending index) with its d^2 into the list; the weights
-        // and the weighted sums then run densely over the list, member m on
-        // lane m mod 32 in increasing m: the same per-lane sequences as
-        // accumulating chunk by chunk, with every lane busy in the costly
-        // sqrt / division / weight work
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        // rank order = ascending index) with its d^2 into the group's list;
+        // the weights and the weighted sums then run densely over the list,
+        // member m on the group's lane m mod 16 in increasing m
         unsigned int cnt = 0;
         auto visitA = [&](int rank, uint32_t, const Pos& o, double d2, int mfi, int mfj) {
             const unsigned int g = cnt + (unsigned int)rank;
-            if (g < (unsigned int)kApssList) A.u.list[g] = ApssMember{o.z, d2, mfi, mfj};
+            if (g < (unsigned int)kApssCap) {
+                L.z[g] = o.z;
+                L.w[g] = d2;
+                L.fij[g] = ((uint32_t)mfi << 16) | (uint32_t)mfj;
+            }
         };
         auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
-        if (F.zb) ball_scan_blocks<false>(F, tc, sc, A.rt, A.rng, fi, fj, q, r2, visitA, flushA);
-        else if (single) rows_scan<false>(F, tc, sc, rcur, total, q, r2, visitA, flushA);
-        else ball_scan<false>(F, tc, sc, A.rt, fi, fj, q, r2, visitA, flushA);
-        if (has_next && single_next) rows_load(F, sc, nfi, nfj, W, nci0, nci1, nm0, nlen);
-        auto advance = [&]() {
-            single_cur = single_next;
-            if (has_next && single_next) ntot = rows_finish(A.rtn[(j + 1) & 1u], nm0, nlen);
-        };
-        if (cnt <= (unsigned int)kApssList) {
+        if (F.zb)
+            ball_scan_blocks<kApssGW, false>(F, tc, sc, A.rt[grp], A.rng[grp], fi, fj, q, r2, visitA,
+                                             flushA, -1, act);
+        else
+            ball_scan<kApssGW, false>(F, tc, sc, A.rt[grp], fi, fj, q, r2, visitA, flushA, -1, act);
+        const bool over = cnt > (unsigned int)kApssCap;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (!over) {
             // (the scans end with a warp barrier; pass B reads back only the
             // entries this lane rewrote)
-            for (unsigned int g = lane; g < cnt; g += 32) {
-                ApssMember& mb = A.u.list[g];
-                const double w = apss_weight_d2(R, mb.w);
-                mb.w = w;
+            for (unsigned int g = gl; g < cnt; g += kApssGW) {
+                const double w = apss_weight_d2(R, L.w[g]);
+                const uint32_t c = L.fij[g];
+                L.w[g] = w;
                 a0 += w;
-                a1 += w * ((mb.fi + 0.5) * F.pitch);
-                a2 += w * ((mb.fj + 0.5) * F.pitch);
-                a3 += w * mb.z;
+                a1 += w * (((double)(int)(c >> 16) + 0.5) * pitch);
+                a2 += w * (((double)(int)(c & 0xFFFFu) + 0.5) * pitch);
+                a3 += w * L.z[g];
             }
-        } else {  // ball larger than the list: accumulate chunk by chunk on a rescan
+        }
+        // ball larger than the list (either group): accumulate chunk by chunk
+        // on a rescan, the other group idle
+        const bool anyover = __any_sync(0xffffffffu, over);
+        auto chunk_visit = [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
+            double* c = A.chunk[G::base() + rank];
+            c[0] = apss_weight_d2(R, d2);
+            c[1] = o.x;
+            c[2] = o.y;
+            c[3] = o.z;
+        };
+        if (anyover) {
             unsigned int c1 = 0;
-            ball_scan(
-                F, tc, sc, A.rt, fi, fj, q, r2,
-                [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
-                    double* c = A.chunk[rank];
-                    c[0] = apss_weight_d2(R, d2);
-                    c[1] = o.x;
-                    c[2] = o.y;
-                    c[3] = o.z;
-                },
+            ball_scan<kApssGW, true>(
+                F, tc, sc, A.rt[grp], fi, fj, q, r2, chunk_visit,
                 [&](int nm) {
-                    const int r = (lane - (int)c1) & 31;  // member c1 + r has lane (c1 + r) mod 32
+                    const int r = (gl - (int)c1) & (kApssGW - 1);  // member c1 + r: lane (c1 + r) mod 16
                     if (r < nm) {
-                        const double* c = A.chunk[r];
+                        const double* c = A.chunk[G::base() + r];
                         const double w = c[0];
                         a0 += w;
                         a1 += w * c[1];
@@ -455,16 +487,16 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                         a3 += w * c[3];
                     }
                     c1 += (unsigned int)nm;
-                });
+                },
+                -1, act && over);
         }
-        const double wsum = warp_halving_sum(a0);
-        double m0 = warp_halving_sum(a1), m1 = warp_halving_sum(a2), m2 = warp_halving_sum(a3);
-        if (cnt < (unsigned int)F.cfg.min_nbrs || wsum <= 0.0) {
-            if (lane == 0) F.amom[(size_t)n * kMom] = cnt < (unsigned int)F.cfg.min_nbrs ? -1.0 : wsum;
-            __syncwarp();
-            advance();
-            continue;
-        }
+        const double wsum = group_halving_sum<kApssGW>(a0);
+        double m0 = group_halving_sum<kApssGW>(a1), m1 = group_halving_sum<kApssGW>(a2),
+               m2 = group_halving_sum<kApssGW>(a3);
+        const bool isol = cnt < (unsigned int)F.cfg.min_nbrs;
+        const bool skip = !act || isol || wsum <= 0.0;
+        if (act && (isol || wsum <= 0.0) && gl == 0) F.amom[(size_t)n * kMom] = isol ? -1.0 : wsum;
+        if (__all_sync(0xffffffffu, skip)) continue;
         m0 /= wsum;
         m1 /= wsum;
         m2 /= wsum;
@@ -472,51 +504,49 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         double b[kRedStride];
 #pragma unroll
         for (int e = 0; e < kRedStride; ++e) b[e] = 0.0;
-        if (cnt <= (unsigned int)kApssList) {
-            for (unsigned int g = lane; g < cnt; g += 32) {
-                const ApssMember mb = A.u.list[g];
-                apss_pass_b(b, mb.w, (mb.fi + 0.5) * F.pitch, (mb.fj + 0.5) * F.pitch, mb.z, m0, m1,
-                            m2);
+        if (!skip && !over) {
+            for (unsigned int g = gl; g < cnt; g += kApssGW) {
+                const uint32_t c = L.fij[g];
+                apss_pass_b(b, L.w[g], ((double)(int)(c >> 16) + 0.5) * pitch,
+                            ((double)(int)(c & 0xFFFFu) + 0.5) * pitch, L.z[g], m0, m1, m2);
             }
-        } else {  // ball larger than the list: walk the window again
+        }
+        if (anyover) {  // walk the window again
             unsigned int c2 = 0;
-            ball_scan(
-                F, tc, sc, A.rt, fi, fj, q, r2,
-                [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
-                    double* c = A.chunk[rank];
-                    c[0] = apss_weight_d2(R, d2);
-                    c[1] = o.x;
-                    c[2] = o.y;
-                    c[3] = o.z;
-                },
+            ball_scan<kApssGW, true>(
+                F, tc, sc, A.rt[grp], fi, fj, q, r2, chunk_visit,
                 [&](int nm) {
-                    const int r = (lane - (int)c2) & 31;
+                    const int r = (gl - (int)c2) & (kApssGW - 1);
                     if (r < nm) {
-                        const double* c = A.chunk[r];
+                        const double* c = A.chunk[G::base() + r];
                         apss_pass_b(b, c[0], c[1], c[2], c[3], m0, m1, m2);
                     }
                     c2 += (unsigned int)nm;
-                });
+                },
+                -1, act && over && !skip);
         }
-        __syncwarp();  // the list is consumed: its storage takes the partials
+        __syncwarp();  // the lists are consumed: their storage takes the partials
 #pragma unroll
         for (int e = 0; e < kRedStride; ++e) A.u.red[lane][e] = b[e];
         __syncwarp();
-        if (lane < kRedStride) {
-            double v[16];
+        if (!skip) {
+            if (gl < kRedStride) {
+                double v[kApssGW];
 #pragma unroll
-            for (int l = 0; l < 16; ++l) v[l] = A.u.red[l][lane] + A.u.red[l + 16][lane];
+                for (int l = 0; l < kApssGW; ++l) v[l] = A.u.red[G::base() + l][gl];
 #pragma unroll
-            for (int o = 8; o > 0; o >>= 1)
+                for (int o = kApssGW / 2; o > 0; o >>= 1)
 #pragma unroll
-                for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
-            F.amom[(size_t)n * kMom + 4 + lane] = v[0];  // M, lower row-major
-        } else if (lane < kRedStride + 4) {
-            const int e = lane - kRedStride;
-            F.amom[(size_t)n * kMom + e] = e == 0 ? wsum : (e == 1 ? m0 : (e == 2 ? m1 : m2));
+                    for (int l = 0; l < o; ++l) v[l] = v[l] + v[l + o];
+                F.amom[(size_t)n * kMom + 4 + gl] = v[0];  // M, lower row-major
+            } else {
+                F.amom[(size_t)n * kMom + 0] = wsum;
+                F.amom[(size_t)n * kMom + 1] = m0;
+                F.amom[(size_t)n * kMom + 2] = m1;
+                F.amom[(size_t)n * kMom + 3] = m2;
+            }
         }
         __syncwarp();
-        advance();
     }
 }
 
@@ -741,8 +771,8 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
         single_cur = ci1 - ci0 < 32;
         if (single_cur) {
             uint32_t m0r, lenr;
-            rows_load(F, sc, fi, fj, w0, ci0, ci1, m0r, lenr);
-            ntot = rows_finish(K.rtn[0], m0r, lenr);
+            rows_load<32>(F, sc, fi, fj, w0, ci0, ci1, m0r, lenr);
+            ntot = rows_finish<32>(K.rtn[0], m0r, lenr);
         }
     }
     uint32_t jj = 0;
@@ -782,11 +812,11 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             };
             auto flushK = [&](int nm) { cnt += (unsigned int)nm; };
             if (w == w0 && first_single)
-                rows_scan<false>(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
-            else ball_scan<false>(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
+                rows_scan<32, false>(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
+            else ball_scan<32, false>(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
             __syncwarp();
             if (!next_loaded && has_next && single_next) {
-                rows_load(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
+                rows_load<32>(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
                 next_loaded = true;
             }
             if (cnt > (unsigned int)kKnnCap) break;  // overflow: exact rescan below
@@ -814,7 +844,7 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             for (; tk < k && (unsigned int)tk < cnt; ++tk) {
                 double bd = INFINITY;
                 uint32_t bi = 0xffffffffu;
-                ball_scan(
+                ball_scan<32, true>(
                     F, tc, sc, K.rt, fi, fj, q, r2,
                     [&](int, uint32_t mm, const Pos&, double d, int, int) {
                         const bool after = tk == 0 || d > last_d || (d == last_d && mm > last_i);
@@ -856,15 +886,16 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
         __syncwarp();
         single_cur = single_next;
         if (has_next && single_next) {
-            if (!next_loaded) rows_load(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
-            ntot = rows_finish(K.rtn[(jj + 1) & 1u], nm0, nlen);
+            if (!next_loaded) rows_load<32>(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
+            ntot = rows_finish<32>(K.rtn[(jj + 1) & 1u], nm0, nlen);
         }
     }
     // survivors of the coming prune, one integer atomic per warp (exact, any order)
     if (lane == 0 && kept) atomicAdd(&F.ctl->keep, kept);
 }
 
-static_assert(sizeof(ApssWarpSm) <= (size_t)kNbrWarpBytes, "APSS warp scratch exceeds the stage union");
-static_assert(sizeof(KnnWarpSm) <= (size_t)kNbrWarpBytes, "kNN warp scratch exceeds the stage union");
+constexpr uint32_t kApssStageWarps = (uint32_t)(kNbrBlockBytes / sizeof(ApssWarpSm));
+static_assert(kApssStageWarps >= 2, "APSS warp scratch exceeds the stage union");
+static_assert(kWarps * sizeof(KnnWarpSm) <= (size_t)kNbrBlockBytes, "kNN warp scratch exceeds the stage union");
 
 }  // namespace rt3d

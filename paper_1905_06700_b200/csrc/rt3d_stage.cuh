@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         const uint32_t P = global_P(F);
         if (P > 0) {
             apss_moment_warps(F, reinterpret_cast<ApssWarpSm*>(sm.u.nbr), ld_cg(&F.ctl->pbase),
-                              ld_cg(&F.ctl->pown), tc, sc);
+                              ld_cg(&F.ctl->pown), tc, sc, kApssStageWarps);
             gsync(sm, F, PH_APSS);
             apss_fit_threads(F, ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown), tc, sc);
             gsync(sm, F, PH_APSS_FIT);
