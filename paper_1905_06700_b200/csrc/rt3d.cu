@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(kFitBlock) apss_fit_kernel(const __grid_consta
                      ld_cg(&F.ctl->sc));
 }
 
+// the fit of a latency-bound launch (one or two frames): eigenvalues and the
+// Pratt solve on separate threads, side by side (apss_fit_split)
+__global__ void __launch_bounds__(128) apss_fit_split_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
+    stamp(F, PH_APSS_FIT);
+    apss_fit_split(F, ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown), ld_cg(&F.ctl->tc),
+                   ld_cg(&F.ctl->sc));
+}
+
 __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant__ FrameBatch FB) {
     const Frame& F = BATCH_FRAME(FB);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -561,8 +571,8 @@ struct rt3d_session {
     int want_per_sm = 2;              // RT3D_BLOCKS_PER_SM (lane-group configs 4, 32, 3)
     int want_per_sm_g1 = 0;           // RT3D_G1_BLOCKS_PER_SM (thread per pixel; 0: occupancy)
     int sharing = 1;                  // sessions running frames concurrently on the device
-    int occ_apss = 1, occ_knn = 1, occ_fit = 1;  // co-resident blocks per SM
-    int grid_apss = 0, grid_knn = 0, grid_fit = 0;
+    int occ_apss = 1, occ_knn = 1, occ_fit = 1, occ_fit_split = 1;  // co-resident blocks per SM
+    int grid_apss = 0, grid_knn = 0, grid_fit = 0, grid_fit_split = 0;
     int grid_fft = 0;
     // sensor
     bool have_sensor = false;
@@ -1032,7 +1042,13 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int fi
         });
     };
     make_batch(fb_apss, Fs, n, (uint32_t)s->grid_apss, first);
-    make_batch(fb_fit, Fs, n, (uint32_t)s->grid_fit, first);
+    // launches of at most ~two waves of split-fit blocks (one or two small
+    // frames: latency-bound) take the split fit; batches and large frames
+    // (throughput-bound) a thread per point
+    static const bool fit_threads = getenv("RT3D_FIT_THREADS") != nullptr;
+    const bool split_fit = !fit_threads &&
+                           (uint64_t)count * F.pcap <= 2ull * 64ull * (uint64_t)s->grid_fit_split;
+    make_batch(fb_fit, Fs, n, (uint32_t)(split_fit ? s->grid_fit_split : s->grid_fit), first);
     make_batch(fb_knn, Fs, n, (uint32_t)s->grid_knn, first);
     auto stage = [&](int st, int it) -> rt3d_status {
         return timed_launch(s, stage_cls[st], [&]() -> rt3d_status {
@@ -1063,7 +1079,10 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int fi
             });
             if (st) return st;
             st = timed_launch(s, RT3D_KC_APSS_FIT, [&]() -> rt3d_status {
-                apss_fit_kernel<<<s->grid_fit * count, kFitBlock, 0, s->stream>>>(fb_fit);
+                if (split_fit)
+                    apss_fit_split_kernel<<<s->grid_fit_split * count, 128, 0, s->stream>>>(fb_fit);
+                else
+                    apss_fit_kernel<<<s->grid_fit * count, kFitBlock, 0, s->stream>>>(fb_fit);
                 CUDA_TRY(cudaGetLastError());
                 return RT3D_OK;
             });
@@ -1266,6 +1285,7 @@ static void set_frame_grids(rt3d_session* s) {
     s->grid_apss = s->nsm * s->occ_apss;
     s->grid_knn = s->nsm * s->occ_knn;
     s->grid_fit = s->nsm * s->occ_fit;
+    s->grid_fit_split = s->nsm * s->occ_fit_split;
     s->grid_frame = 0;
     for (int c = 0; c < kNumCfg; ++c) {
         const int per = std::max(1, std::min(s->per_sm_c[c], blocks_per_sm(s, c)) / std::max(1, s->sharing));
@@ -1336,9 +1356,12 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
                                                                sizeof(KnnWarpSm) * kNbrWarps));
         int f = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&f, apss_fit_kernel, kFitBlock, 0));
+        int fs = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fs, apss_fit_split_kernel, 128, 0));
         s->occ_apss = std::max(a, 1);
         s->occ_knn = std::max(k, 1);
         s->occ_fit = std::max(f, 1);
+        s->occ_fit_split = std::max(fs, 1);
     }
     if (per_sm < 1) {
         delete s;

@@ -221,6 +221,43 @@ __device__ __forceinline__ int pd5_shift(const double m[15], double sigma) {
     return 1;
 }
 
+// pd5_shift at three shifts at once, branch-free and interleaved (the
+// latency-bound fit runs the three eliminations side by side): a shift is
+// definite iff every pivot is > 0, the elimination continuing past a failed
+// pivot only into values that no longer matter, so each result equals
+// pd5_shift's (same operations up to the first non-positive pivot).
+__device__ __forceinline__ void pd5_shift3(const double m[15], double s0, double s1, double s2,
+                                           bool& r0, bool& r1, bool& r2) {
+    double a[3][15];
+#pragma unroll
+    for (int v = 0; v < 3; ++v) {
+        const double sg = v == 0 ? s0 : (v == 1 ? s1 : s2);
+#pragma unroll
+        for (int k = 0; k < 15; ++k) a[v][k] = m[k];
+        a[v][lt(1, 1)] = m[lt(1, 1)] - sg;
+        a[v][lt(2, 2)] = m[lt(2, 2)] - sg;
+        a[v][lt(3, 3)] = m[lt(3, 3)] - sg;
+        a[v][lt(4, 0)] = m[lt(4, 0)] + 2.0 * sg;
+    }
+    bool ok[3] = {true, true, true};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+#pragma unroll
+        for (int v = 0; v < 3; ++v) {
+            const double akk = a[v][lt(k, k)];
+            ok[v] = ok[v] && (akk > 0.0);
+#pragma unroll
+            for (int i = k + 1; i < 5; ++i)
+#pragma unroll
+                for (int j = k + 1; j <= i; ++j)
+                    a[v][lt(i, j)] = akk * a[v][lt(i, j)] - a[v][lt(i, k)] * a[v][lt(j, k)];
+        }
+    }
+    r0 = ok[0];
+    r1 = ok[1];
+    r2 = ok[2];
+}
+
 // Smallest admissible eigenpair of the Pratt pencil (M, N): the eigenvector
 // that the reference's filter loop over GeneralizedEigenSolver's results keeps
 // (denoise.hpp:86-112).  For PSD M the admissible eigenvalues are the
@@ -228,7 +265,11 @@ __device__ __forceinline__ int pd5_shift(const double m[15], double sigma) {
 // bisection on a division-free definiteness test brackets it, inverse
 // iteration on an LDL' factor of the last definite shift gives the
 // eigenvector.  Same sequence of operations
-// as oracle_pratt_smallest (bit-identical on identical M).
+// as oracle_pratt_smallest (bit-identical on identical M).  kSpec: two
+// bisection steps per round, the midpoint and both possible next midpoints
+// tested together (pd5_shift3), then the same two steps taken in order: the
+// same brackets, a chain half as long for the latency-bound single-frame fit.
+template <bool kSpec = false>
 __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
     double L[15], d[5];
     const double scale =
@@ -237,15 +278,38 @@ __device__ __forceinline__ int pratt_smallest(const double m[15], double u[5]) {
     double hi = std_min(std_min(m[lt(1, 1)], m[lt(2, 2)]), m[lt(3, 3)]);
     if (pd5_shift(m, 0.0) && hi > 0.0) {
         double lo = 0.0;
+        if constexpr (!kSpec) {
 #pragma unroll 1
-        for (int it = 0; it < 200; ++it) {
-            double mid = 0.5 * (lo + hi);
-            if (!(mid > lo && mid < hi)) break;
-            if (pd5_shift(m, mid)) lo = mid;
-            else hi = mid;
-            // bracket to 1e-9 relative (as the oracle): the inverse iteration
-            // converges from there
-            if (hi - lo <= 1e-9 * hi) break;
+            for (int it = 0; it < 200; ++it) {
+                double mid = 0.5 * (lo + hi);
+                if (!(mid > lo && mid < hi)) break;
+                if (pd5_shift(m, mid)) lo = mid;
+                else hi = mid;
+                // bracket to 1e-9 relative (as the oracle): the inverse
+                // iteration converges from there
+                if (hi - lo <= 1e-9 * hi) break;
+            }
+        } else {
+            int it = 0;
+#pragma unroll 1
+            while (it < 200) {
+                const double mid = 0.5 * (lo + hi);
+                if (!(mid > lo && mid < hi)) break;
+                // the next midpoint is 0.5 (mid + hi) if mid is definite,
+                // else 0.5 (lo + mid): the same expressions as the step takes
+                const double mH = 0.5 * (mid + hi), mL = 0.5 * (lo + mid);
+                bool pA, pH, pL;
+                pd5_shift3(m, mid, mH, mL, pA, pH, pL);
+                if (pA) lo = mid;
+                else hi = mid;
+                if (++it >= 200 || hi - lo <= 1e-9 * hi) break;
+                const double mid2 = pA ? mH : mL;
+                if (!(mid2 > lo && mid2 < hi)) break;
+                if (pA ? pH : pL) lo = mid2;
+                else hi = mid2;
+                ++it;
+                if (hi - lo <= 1e-9 * hi) break;
+            }
         }
         sigma = lo;
     } else {
@@ -324,10 +388,11 @@ struct Sphere {
 // Pratt normalisation, un-centring.  The orientation flip
 // (denoise.hpp:119-123) negates (u0, ul, uq) together; project_onto_sphere
 // is bitwise invariant under it, so it is omitted.
+template <bool kSpec = false>
 __device__ __forceinline__ bool sphere_from_moments(const double m[15], double c0, double c1,
                                                     double c2, Sphere& out) {
     double v[5];
-    if (!pratt_smallest(m, v)) return false;
+    if (!pratt_smallest<kSpec>(m, v)) return false;
     double vn2 = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3] + v[4] * v[4];
     if (sqrt(vn2) < 1e-300) return false;
     double nrm = v[1] * v[1] + v[2] * v[2] + v[3] * v[3] - 4.0 * v[0] * v[4];

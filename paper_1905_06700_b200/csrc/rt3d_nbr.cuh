@@ -592,6 +592,67 @@ static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P,
     }
 }
 
+// The fit of apss_fit_threads for latency-bound launches (a single frame):
+// 64 points per 128-thread block, the first 64 threads run the covariance
+// eigenvalues and finish the point, the other 64 the Pratt pencil solve with
+// the two-step bisection, side by side; the same operations as
+// apss_fit_threads, so the same results.
+static __device__ void apss_fit_split(const Frame& F, uint32_t pb, uint32_t P, int tc, int sc) {
+    __shared__ double s_sp[64][5];
+    __shared__ int s_ok[64], s_deg[64];
+    const int t = (int)threadIdx.x, k = t & 63;
+    const bool solver = t >= 64;
+    for (uint32_t b0 = vblock(F) * 64u; b0 < P; b0 += vgrid(F) * 64u) {
+        const uint32_t nl = b0 + (uint32_t)k;
+        const bool act = nl < P;
+        const uint32_t n = pb + nl;
+        RT3D_CHECK(!act || n < F.pcap);
+        const double* mo = F.amom + (size_t)n * kMom;
+        const double wsum = act ? mo[0] : -1.0;
+        if (wsum > 0.0) {
+            double M[15];
+#pragma unroll
+            for (int e = 0; e < 15; ++e) M[e] = mo[4 + e];
+            if (solver) {
+                Sphere sp;
+                s_ok[k] = sphere_from_moments<true>(M, mo[1], mo[2], mo[3], sp) ? 1 : 0;
+                s_sp[k][0] = sp.u0;
+                s_sp[k][1] = sp.ul0;
+                s_sp[k][2] = sp.ul1;
+                s_sp[k][3] = sp.ul2;
+                s_sp[k][4] = sp.uq;
+            } else {
+                double cv[6], e0, e1, e2;
+                cov_from_moments(M, wsum, cv);
+                sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
+                s_deg[k] = (e2 <= 0.0 || e1 <= 1e-12 * e2) ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        if (!solver && act) {
+            const int fi = F.fi[sc][n], fj = F.fj[sc][n];
+            const Pos q{(fi + 0.5) * F.pitch, (fj + 0.5) * F.pitch, F.t[tc][n] * F.bres};
+            uint8_t fl = F.fl[sc][n] & (uint8_t)~(1u | 4u);
+            double z = q.z;
+            if (wsum < 0.0) {
+                fl |= 1u;  // isolated
+            } else if (wsum <= 0.0 || s_deg[k]) {
+                fl |= 4u;
+            } else {
+                const Sphere sp{s_sp[k][0], s_sp[k][1], s_sp[k][2], s_sp[k][3], s_sp[k][4]};
+                Pos o;
+                if (!s_ok[k] || !project_sphere(sp, F.cfg.eps, q.x, q.y, q.z, o.x, o.y, o.z))
+                    fl |= 4u;
+                else
+                    z = o.z;
+            }
+            F.t[tc ^ 1][n] = std_clamp(z / F.bres, 0.0, F.tlim);
+            F.fl[sc][n] = fl;
+        }
+        __syncthreads();
+    }
+}
+
 // ascending bitonic sort of one u32 per lane across the warp
 __device__ __forceinline__ uint32_t warp_sort32(uint32_t x) {
     const int lane = threadIdx.x & 31;
