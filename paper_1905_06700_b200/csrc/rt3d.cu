@@ -972,6 +972,12 @@ rt3d_status timed_launch(rt3d_session* s, int cls, Fn&& fn) {
     rt3d_session::Timed t{cls, pool_event(s), pool_event(s)};
     CUDA_TRY(cudaEventRecord(t.a, s->stream));
     rt3d_status st = fn();
+    static const bool sync_each = getenv("RT3D_SYNC_EACH") != nullptr;  // (debugging: name the failing class)
+    if (sync_each) {
+        const cudaError_t e = cudaStreamSynchronize(s->stream);
+        if (e != cudaSuccess)
+            return fail(RT3D_ERR_CUDA, "kernel class %d: %s", cls, cudaGetErrorString(e));
+    }
     CUDA_TRY(cudaEventRecord(t.b, s->stream));
     s->timed.push_back(t);
     return st;

@@ -27,7 +27,7 @@ namespace rt3d {
 
 constexpr int kNbrBlock = 128;
 constexpr int kNbrWarps = kNbrBlock / 32;
-constexpr int kKnnCap = 384;     // per-warp ball list for the kNN selection
+constexpr int kKnnCap = 192;     // per-point ball list for the kNN selection (two per warp)
 constexpr int kFitBlock = 128;
 
 // Lane groups of GW lanes scanning one point's window each: GW = 32 (kNN, a
@@ -75,13 +75,15 @@ struct ApssWarpSm {
     RowTab rt[2];
     uint2 rng[2][64];  // depth-block candidate ranges (ball_scan_blocks)
 };
-struct KnnWarpSm {
+struct KnnList {              // one lane group's ball list
     double d2[kKnnCap];
     uint32_t idx[kKnnCap];
     uint32_t sel[kKnnCap];  // the selection in rank order
     double kth;
-    RowTab rt;
-    RowTab rtn[2];  // first-window rows of this point and the next
+};
+struct KnnWarpSm {
+    KnnList l[2];
+    RowTab rt[2];
 };
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -653,134 +655,140 @@ static __device__ void apss_fit_split(const Frame& F, uint32_t pb, uint32_t P, i
     }
 }
 
-// ascending bitonic sort of one u32 per lane across the warp
-__device__ __forceinline__ uint32_t warp_sort32(uint32_t x) {
-    const int lane = threadIdx.x & 31;
+// ascending bitonic sort of one u32 per lane across each lane group
+template <int GW>
+__device__ __forceinline__ uint32_t group_sort(uint32_t x) {
+    const int gl = Grp<GW>::gl();
 #pragma unroll
-    for (int size = 2; size <= 32; size <<= 1) {
+    for (int size = 2; size <= GW; size <<= 1) {
 #pragma unroll
         for (int j = size >> 1; j > 0; j >>= 1) {
             const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
-            const bool up = (lane & size) == 0;  // this pair sorts ascending
-            const bool low = (lane & j) == 0;    // this lane keeps the smaller
+            const bool up = (gl & size) == 0 || size == GW;  // this pair sorts ascending
+            const bool low = (gl & j) == 0;                  // this lane keeps the smaller
             x = (low == up) ? min(x, y) : max(x, y);
         }
     }
     return x;
 }
 
-// k smallest (d^2, index) keys of the warp's list in rank order
-// (spatial_index.hpp:51-62) -> K.sel[0..taken); kth = the last key's d^2.
-__device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k, double& kth) {
-    const int lane = threadIdx.x & 31;
-    if (cnt <= 32u) {  // rank by counting, one key per lane
-        const int taken = (unsigned int)k < cnt ? k : (int)cnt;
-        if ((unsigned int)lane < cnt) {
-            const double my = K.d2[lane];
+// k smallest (d^2, index) keys of the group's list in rank order
+// (spatial_index.hpp:51-62) -> L.sel[0..taken), L.kth = the last key's d^2.
+// Warp-collective: both groups call it, a group with act false does nothing.
+// The list is in ascending index order, so the (d^2, index) order is
+// (d^2, slot).
+constexpr int kKnnGW = 16;       // lanes per point: two points per warp
+constexpr int kKnnKeys = 6;      // keys per lane of the threshold path (lists <= 96)
+__device__ __forceinline__ int knn_select(KnnList& L, unsigned int cnt, int k, bool act) {
+    using G = Grp<kKnnGW>;
+    const int gl = G::gl();
+    const int taken = act ? ((unsigned int)k < cnt ? k : (int)cnt) : 0;
+    constexpr unsigned int kThr = kKnnKeys * kKnnGW;
+    static_assert(2 * kThr <= kKnnCap, "kNN threshold path: list and compacted keys");
+    const int mode = !act ? -1 : (cnt <= (unsigned int)kKnnGW ? 0 : (cnt <= kThr ? 1 : 2));
+    if (__any_sync(0xffffffffu, mode == 0)) {  // rank by counting, one key per lane
+        if (mode == 0 && (unsigned int)gl < cnt) {
+            const double my = L.d2[gl];
             int rank = 0;
             for (unsigned int e = 0; e < cnt; ++e) {
-                const double d = K.d2[e];
-                rank += (d < my || (d == my && e < (unsigned int)lane)) ? 1 : 0;
+                const double d = L.d2[e];
+                rank += (d < my || (d == my && e < (unsigned int)gl)) ? 1 : 0;
             }
-            if (rank < taken) K.sel[rank] = K.idx[lane];
-            if (rank == taken - 1) K.kth = my;
+            if (rank < taken) L.sel[rank] = L.idx[gl];
+            if (rank == taken - 1) L.kth = my;
         }
-        __syncwarp();
-        kth = taken > 0 ? K.kth : 0.0;
-        __syncwarp();
-        return taken;
     }
-    if (cnt <= 128u) {
-        // The list is in ascending index order, so the (d^2, index) order is
-        // (d^2, slot).  A threshold from the lane minima (a lane holds slots
-        // lane + 32 e) on the high words of the keys' bits
-        // (d^2 >= 0, so the high word is monotone in d^2): at least k keys
-        // have a high word at or below the k-th smallest minimum's, so the
-        // keys above it rank >= k.  The keys at or below it are compacted in
-        // slot order (typically ~k of them) and ranked by counting; ranks are
-        // a permutation.
-        constexpr int E = 4;
-        const int taken = (unsigned int)k < cnt ? k : (int)cnt;
-        double a[E];
-        uint32_t h[E];
+    if (__any_sync(0xffffffffu, mode == 1)) {
+        // A threshold from the lane minima (a lane holds slots gl + 16 e) on
+        // the high words of the keys' bits (d^2 >= 0, so the high word is
+        // monotone in d^2): at least k keys have a high word at or below the
+        // k-th smallest minimum's, so the keys above it rank >= k.  The keys
+        // at or below it are compacted in slot order (typically ~k of them)
+        // and ranked by counting; ranks are a permutation.
+        const bool on = mode == 1;
+        double a[kKnnKeys];
+        uint32_t h[kKnnKeys];
         uint32_t hmin = 0xffffffffu;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const bool v = (unsigned int)lane + 32u * e < cnt;
-            a[e] = v ? K.d2[lane + 32 * e] : INFINITY;
+        for (int e = 0; e < kKnnKeys; ++e) {
+            const bool v = on && (unsigned int)(gl + kKnnGW * e) < cnt;
+            a[e] = v ? L.d2[gl + kKnnGW * e] : INFINITY;
             h[e] = v ? (uint32_t)((unsigned long long)__double_as_longlong(a[e]) >> 32) : 0xffffffffu;
             hmin = min(hmin, h[e]);
         }
-        uint32_t tau = 0xffffffffu;
-        if (k <= 32) {
-            const uint32_t srt = warp_sort32(hmin);
-            tau = __shfl_sync(0xffffffffu, srt, k - 1);
-        }
-        // the compacted keys go to slots [128, 128 + c) of the list
-        double* cd = K.d2 + 128;
-        uint32_t* ci = K.idx + 128;
+        const uint32_t srt = group_sort<kKnnGW>(hmin);
+        const uint32_t tau =
+            k <= kKnnGW ? __shfl_sync(0xffffffffu, srt, (k - 1) & (kKnnGW - 1), kKnnGW) : 0xffffffffu;
+        // the compacted keys go to slots [kThr, kThr + c) of the list
+        double* cd = L.d2 + kThr;
+        uint32_t* ci = L.idx + kThr;
         unsigned int c = 0;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-            const bool in = (unsigned int)lane + 32u * e < cnt && h[e] <= tau;
-            const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        for (int e = 0; e < kKnnKeys; ++e) {
+            const bool in = on && (unsigned int)(gl + kKnnGW * e) < cnt && h[e] <= tau;
+            const uint32_t bal = G::field(__ballot_sync(0xffffffffu, in));
             if (in) {
-                const unsigned int p = c + (unsigned int)__popc(bal & lanemask_lt());
+                const unsigned int p = c + (unsigned int)__popc(bal & G::lt());
                 cd[p] = a[e];
-                ci[p] = K.idx[lane + 32 * e];
+                ci[p] = L.idx[gl + kKnnGW * e];
             }
             c += (unsigned int)__popc(bal);
         }
         __syncwarp();
-        for (unsigned int sl = (unsigned int)lane; sl < c; sl += 32u) {
-            const double my = cd[sl];
-            int rank = 0;
-            for (unsigned int e = 0; e < c; ++e) {
-                const double d = cd[e];
-                rank += (d < my || (d == my && e < sl)) ? 1 : 0;
+        if (on) {
+            for (unsigned int sl = (unsigned int)gl; sl < c; sl += kKnnGW) {
+                const double my = cd[sl];
+                int rank = 0;
+                for (unsigned int e = 0; e < c; ++e) {
+                    const double d = cd[e];
+                    rank += (d < my || (d == my && e < sl)) ? 1 : 0;
+                }
+                if (rank < taken) L.sel[rank] = ci[sl];
+                if (rank == taken - 1) L.kth = my;
             }
-            if (rank < taken) K.sel[rank] = ci[sl];
-            if (rank == taken - 1) K.kth = my;
         }
-        __syncwarp();
-        kth = taken > 0 ? K.kth : 0.0;
-        __syncwarp();
-        return taken;
     }
-    double last_d = 0.0;
-    uint32_t last_i = 0;
-    int taken = 0;
-    for (; taken < k && (unsigned int)taken < cnt; ++taken) {
-        double bd = INFINITY;
-        uint32_t bi = 0xffffffffu;
-        for (unsigned int e = lane; e < cnt; e += 32) {
-            const double d = K.d2[e];
-            const uint32_t i = K.idx[e];
-            const bool after = taken == 0 || d > last_d || (d == last_d && i > last_i);
-            if (after && (d < bd || (d == bd && i < bi))) {
-                bd = d;
-                bi = i;
-            }
-        }
+    if (__any_sync(0xffffffffu, mode == 2)) {  // successive minima over the list
+        const bool on = mode == 2;
+        double last_d = 0.0;
+        uint32_t last_i = 0;
+        const int kr = (int)G::wmax((uint32_t)(on ? taken : 0));
+        for (int tk = 0; tk < kr; ++tk) {
+            double bd = INFINITY;
+            uint32_t bi = 0xffffffffu;
+            if (on)
+                for (unsigned int e = gl; e < cnt; e += kKnnGW) {
+                    const double d = L.d2[e];
+                    const uint32_t i = L.idx[e];
+                    const bool after = tk == 0 || d > last_d || (d == last_d && i > last_i);
+                    if (after && (d < bd || (d == bd && i < bi))) {
+                        bd = d;
+                        bi = i;
+                    }
+                }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, bd, o);
-            const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (od < bd || (od == bd && oi < bi)) {
-                bd = od;
-                bi = oi;
+            for (int o = kKnnGW / 2; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (od < bd || (od == bd && oi < bi)) {
+                    bd = od;
+                    bi = oi;
+                }
             }
+            if (on && tk < taken && gl == 0) {
+                L.sel[tk] = bi;
+                if (tk == taken - 1) L.kth = bd;
+            }
+            last_d = bd;
+            last_i = bi;
         }
-        if (lane == 0) K.sel[taken] = bi;
-        last_d = bd;
-        last_i = bi;
     }
-    kth = last_d;
     __syncwarp();
     return taken;
 }
 
-// kNN intensity filter over the current state; writes r[rc^1].
+// kNN intensity filter over the current state, two points per warp (16
+// lanes each); writes r[rc^1].
 //
 // Window pruning (exact): a member whose fine pixel lies outside the window
 // of half-width w differs by >= w+1 pixels along one axis, so its d^2 is at
@@ -790,11 +798,15 @@ __device__ __forceinline__ int knn_select(KnnWarpSm& K, unsigned int cnt, int k,
 // small window knn_w0; if the k-th key found there is below that bound for
 // the next ring, no member outside can enter the top k and the selection is
 // final; otherwise the window grows to the first ring whose bound exceeds
-// the k-th key (at most W, the full ball).
+// the k-th key (at most W, the full ball).  The two groups grow their
+// windows independently; the warp rescans until both are final.
 static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, uint32_t P, int tc,
                                  int rc, int sc) {
+    using G = Grp<kKnnGW>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = G::gl(), grp = lane >> 4;
     KnnWarpSm& K = wsm[warp];
+    KnnList& L = K.l[grp];
     const uint32_t wpb = blockDim.x >> 5;
     const uint32_t gw = vblock(F) * wpb + warp, nw = vgrid(F) * wpb;
     const double R = F.cfg.R, r2 = R * R;
@@ -802,111 +814,92 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
     const int k = F.cfg.knn_k, Wfull = F.cfg.W;
     const double pitch = F.pitch;
     const int w0 = F.cfg.knn_w0 < Wfull ? F.cfg.knn_w0 : Wfull;
-    // positions preloaded 32 points at a time (lane j holds point j's); the
-    // next point's first-window rows are loaded during this point's selection
+    // the warp's pairs gw + j nw, points 2 pair + group: positions preloaded
+    // 16 pairs at a time (lane 2 i + g holds pair jbase + i's point g)
     int pfi = 0, pfj = 0;
     double pt = 0.0;
     uint32_t jbase = 0xffffffffu;
-    auto point = [&](uint32_t j, int& fi, int& fj, double& t) {
-        if ((j & ~31u) != jbase) {
-            jbase = j & ~31u;
-            const uint32_t nl = gw + (jbase + (uint32_t)lane) * nw;
+    auto point = [&](uint32_t j, int& fi, int& fj, double& t) {  // (warp-collective)
+        if ((j & ~15u) != jbase) {
+            jbase = j & ~15u;
+            const uint32_t nl = 2u * (gw + (jbase + (uint32_t)(lane >> 1)) * nw) + (uint32_t)(lane & 1);
             if (nl < P) {
                 pfi = F.fi[sc][pb + nl];
                 pfj = F.fj[sc][pb + nl];
                 pt = F.t[tc][pb + nl];
             }
         }
-        fi = __shfl_sync(0xffffffffu, pfi, (int)(j & 31u));
-        fj = __shfl_sync(0xffffffffu, pfj, (int)(j & 31u));
-        t = __shfl_sync(0xffffffffu, pt, (int)(j & 31u));
+        const int src = (int)((j & 15u) << 1) | grp;
+        fi = __shfl_sync(0xffffffffu, pfi, src);
+        fj = __shfl_sync(0xffffffffu, pfj, src);
+        t = __shfl_sync(0xffffffffu, pt, src);
     };
-    bool single_cur = false;
-    uint32_t ntot = 0;
-    if (gw < P) {
-        int fi, fj;
-        double t;
-        point(0, fi, fj, t);
-        int ci0, ci1;
-        window_rows(F, fi, w0, ci0, ci1);
-        single_cur = ci1 - ci0 < 32;
-        if (single_cur) {
-            uint32_t m0r, lenr;
-            rows_load<32>(F, sc, fi, fj, w0, ci0, ci1, m0r, lenr);
-            ntot = rows_finish<32>(K.rtn[0], m0r, lenr);
-        }
-    }
-    uint32_t jj = 0;
     unsigned int kept = 0;
-    for (uint32_t nl = gw; nl < P; nl += nw, ++jj) {
-        const uint32_t n = pb + nl;
-        RT3D_CHECK(n < F.pcap);
+    for (uint32_t j = 0;; ++j) {
+        const uint32_t pair = gw + j * nw;
+        if (2u * pair >= P) break;  // (warp-uniform)
         int fi, fj;
         double tq;
-        point(jj, fi, fj, tq);
+        point(j, fi, fj, tq);
+        const uint32_t nl = 2u * pair + (uint32_t)grp;
+        const bool act = nl < P;
+        const uint32_t n = pb + nl;
+        RT3D_CHECK(!act || n < F.pcap);
         const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, tq * F.bres};
-        const bool first_single = single_cur;
-        const uint32_t first_total = ntot;
-        const bool has_next = nl + nw < P;
-        int nfi = 0, nfj = 0, nci0 = 0, nci1 = -1;
-        double ntq = 0.0;
-        bool single_next = false;
-        uint32_t nm0 = 0, nlen = 0;
-        if (has_next) {
-            point(jj + 1, nfi, nfj, ntq);
-            window_rows(F, nfi, w0, nci0, nci1);
-            single_next = nci1 - nci0 < 32;
-        }
-        bool next_loaded = false;
         int w = w0;
-        double kth = 0.0;
         int taken = 0;
-        unsigned int cnt;
-        for (;;) {
-            cnt = 0;
+        unsigned int cnt = 0;
+        bool done = !act, over = false;
+        while (!__all_sync(0xffffffffu, done)) {
+            unsigned int c = 0;
             auto visitK = [&](int rank, uint32_t mm, const Pos&, double d2, int, int) {
-                const unsigned int slot = cnt + (unsigned int)rank;
+                const unsigned int slot = c + (unsigned int)rank;
                 if (slot < (unsigned int)kKnnCap) {
-                    K.d2[slot] = d2;
-                    K.idx[slot] = mm;
+                    L.d2[slot] = d2;
+                    L.idx[slot] = mm;
                 }
             };
-            auto flushK = [&](int nm) { cnt += (unsigned int)nm; };
-            if (w == w0 && first_single)
-                rows_scan<32, false>(F, tc, sc, K.rtn[jj & 1u], first_total, q, r2, visitK, flushK);
-            else ball_scan<32, false>(F, tc, sc, K.rt, fi, fj, q, r2, visitK, flushK, w);
-            __syncwarp();
-            if (!next_loaded && has_next && single_next) {
-                rows_load<32>(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
-                next_loaded = true;
+            auto flushK = [&](int nm) { c += (unsigned int)nm; };
+            ball_scan<kKnnGW, false>(F, tc, sc, K.rt[grp], fi, fj, q, r2, visitK, flushK, w, !done);
+            const bool sel = !done && c <= (unsigned int)kKnnCap;
+            if (!done) cnt = c;
+            if (!done && !sel) {  // overflow: exact rescans below
+                over = true;
+                done = true;
             }
-            if (cnt > (unsigned int)kKnnCap) break;  // overflow: exact rescan below
-            taken = knn_select(K, cnt, k, kth);
-            if (w >= Wfull) break;
-            if (taken < k) {  // too few in the small window: take the full ball
-                w = Wfull;
-                continue;
+            const int tk = knn_select(L, cnt, k, sel);
+            if (sel) {
+                taken = tk;
+                if (w >= Wfull) {
+                    done = true;
+                } else if (taken < k) {  // too few in the small window: take the full ball
+                    w = Wfull;
+                } else {
+                    const double kth = L.kth;
+                    int wn = w;
+                    while (wn < Wfull) {
+                        const double b = (double)(wn + 1) * pitch;
+                        if (b * b * (1.0 - 1e-9) > kth) break;
+                        ++wn;
+                    }
+                    if (wn == w) done = true;  // nothing outside the window can enter the top k
+                    else w = wn;
+                }
             }
-            int wn = w;
-            while (wn < Wfull) {
-                const double b = (double)(wn + 1) * pitch;
-                if (b * b * (1.0 - 1e-9) > kth) break;
-                ++wn;
-            }
-            if (wn == w) break;  // nothing outside the window can enter the top k
-            w = wn;
         }
-        double result;
-        if (cnt > (unsigned int)kKnnCap) {
+        double result = 0.0;
+        if (__any_sync(0xffffffffu, over)) {
             // list overflow (full window): successive minima over rescans
             double last_d = 0.0, acc = 0.0;
             uint32_t last_i = 0;
-            int tk = 0;
-            for (; tk < k && (unsigned int)tk < cnt; ++tk) {
+            const int kr = (int)G::wmax((uint32_t)(over ? (k < (int)cnt ? k : (int)cnt) : 0));
+            int tkn = 0;
+            for (int tk = 0; tk < kr; ++tk) {
+                const bool on = over && tk < k && (unsigned int)tk < cnt;
                 double bd = INFINITY;
                 uint32_t bi = 0xffffffffu;
-                ball_scan<32, true>(
-                    F, tc, sc, K.rt, fi, fj, q, r2,
+                ball_scan<kKnnGW, true>(
+                    F, tc, sc, K.rt[grp], fi, fj, q, r2,
                     [&](int, uint32_t mm, const Pos&, double d, int, int) {
                         const bool after = tk == 0 || d > last_d || (d == last_d && mm > last_i);
                         if (after && (d < bd || (d == bd && mm < bi))) {
@@ -914,9 +907,9 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
                             bi = mm;
                         }
                     },
-                    [&](int) {}, w);
+                    [&](int) {}, w, on);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
+                for (int o = kKnnGW / 2; o > 0; o >>= 1) {
                     const double od = __shfl_xor_sync(0xffffffffu, bd, o);
                     const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
                     if (od < bd || (od == bd && oi < bi)) {
@@ -924,35 +917,38 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
                         bi = oi;
                     }
                 }
-                acc += rr[bi];
+                if (on) {
+                    acc += rr[bi];
+                    ++tkn;
+                }
                 last_d = bd;
                 last_i = bi;
             }
-            result = cnt == 0 ? rr[n] : acc / (double)tk;
-        } else {
-            // mean over the selection in rank order (denoise.hpp:233-234):
-            // the loads in parallel, the sum in rank order
-            double acc = 0.0;
-            for (int t0 = 0; t0 < taken; t0 += 32) {
-                const double v = t0 + lane < taken ? rr[K.sel[t0 + lane]] : 0.0;
-                const int nb = taken - t0 < 32 ? taken - t0 : 32;
-                for (int t = 0; t < nb; ++t) acc += __shfl_sync(0xffffffffu, v, t);
-            }
-            result = taken == 0 ? rr[n] : acc / (double)taken;
+            if (over) result = cnt == 0 ? rr[n] : acc / (double)tkn;
         }
-        if (lane == 0) {
+        // mean over the selection in rank order (denoise.hpp:233-234): the
+        // loads in parallel, the sum in rank order
+        {
+            double acc = 0.0;
+            const int tm = (int)G::wmax((uint32_t)(over ? 0 : taken));
+            for (int t0 = 0; t0 < tm; t0 += kKnnGW) {
+                const double v = !over && t0 + gl < taken ? rr[L.sel[t0 + gl]] : 0.0;
+#pragma unroll 4
+                for (int t = 0; t < kKnnGW; ++t) {
+                    const double x = __shfl_sync(0xffffffffu, v, t, kKnnGW);
+                    if (t0 + t < taken) acc += x;
+                }
+            }
+            if (act && !over) result = taken == 0 ? rr[n] : acc / (double)taken;
+        }
+        if (act && gl == 0) {
             F.r[rc ^ 1][n] = result;
             kept += (result >= F.cfg.r_min) ? 1u : 0u;  // prune's test (denoise.hpp:246)
         }
         __syncwarp();
-        single_cur = single_next;
-        if (has_next && single_next) {
-            if (!next_loaded) rows_load<32>(F, sc, nfi, nfj, w0, nci0, nci1, nm0, nlen);
-            ntot = rows_finish<32>(K.rtn[(jj + 1) & 1u], nm0, nlen);
-        }
     }
-    // survivors of the coming prune, one integer atomic per warp (exact, any order)
-    if (lane == 0 && kept) atomicAdd(&F.ctl->keep, kept);
+    // survivors of the coming prune, one integer atomic per group (exact, any order)
+    if (gl == 0 && kept) atomicAdd(&F.ctl->keep, kept);
 }
 
 constexpr uint32_t kApssStageWarps = (uint32_t)(kNbrBlockBytes / sizeof(ApssWarpSm));
