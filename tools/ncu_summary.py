@@ -16,7 +16,8 @@ ROOT = Path(__file__).resolve().parents[1]
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 CLASS = {"stage_kernel<0,": "stage_first", "stage_kernel<1,": "stage_depth",
          "stage_kernel<2,": "stage_intensity", "stage_kernel<3,": "stage_tail",
-         "apss_kernel": "apss", "apss_fit_kernel": "apss_fit", "knn_kernel": "knn"}
+         "apss_kernel": "apss", "apss_fit_kernel": "apss_fit", "apss_fit_split_kernel": "apss_fit",
+         "zblock_kernel": "apss_fit", "knn_kernel": "knn"}
 
 
 def kclass(name):
@@ -81,7 +82,7 @@ def full(path):
                    for c, v in traffic.items()}
 
 
-CMD = "python tools/profile_batch.py (one batch of 8 config-B frames, the bench step)"
+CMD = "python tools/profile_batch.py B 16 (one batch of 16 config-B frames, the bench step)"
 FULL_ARGS = "--profile-from-start off -c 6"
 
 
