@@ -2063,8 +2063,9 @@ __device__ __forceinline__ void cov_from_moments(const double* M, double wsum, d
     cv[5] = M[lt(3, 3)] / wsum;
 }
 
-// the halving tree over 32 lane partials (column `col` of p[32][stride]):
-// p[l] = p[l] + p[l+o], o = 16..1 (oracle: lane_tree)
+// the halving tree over kApssLanes lane partials (column `col` of
+// p[kApssLanes][stride]): p[l] = p[l] + p[l+o], o = kApssLanes/2..1 (oracle:
+// lane_tree)
 __device__ __forceinline__ double halving_sum_lanes(double* p, int stride, int col) {
     for (int o = kApssLanes / 2; o > 0; o >>= 1)
         for (int l = 0; l < o; ++l) p[l * stride + col] = p[l * stride + col] + p[(l + o) * stride + col];
