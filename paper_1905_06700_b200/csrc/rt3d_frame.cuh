@@ -2079,12 +2079,12 @@ __device__ __forceinline__ double halving_sum_lanes(double* p, int stride, int c
 template <typename Enum>
 __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, int min_nbrs,
                                            double eps, uint8_t& flags, Pos& out) {
-    const double r2 = R * R;
+    const double r2 = R * R, Rinv = 1.0 / R;
     unsigned int cnt = 0;
     double pa[kApssLanes][4];
     for (int l = 0; l < kApssLanes; ++l) pa[l][0] = pa[l][1] = pa[l][2] = pa[l][3] = 0.0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        const double w = apss_weight_d2(R, d2);
+        const double w = apss_weight_d2(R, Rinv, d2);
         double* a = pa[cnt % (unsigned int)kApssLanes];
         ++cnt;
         a[0] += w;
@@ -2111,7 +2111,7 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
         for (int e = 0; e < kRedStride; ++e) pb[l][e] = 0.0;
     unsigned int c2 = 0;
     each(r2, [&](uint32_t, const Pos& o, double d2) {
-        apss_pass_b(pb[c2 % (unsigned int)kApssLanes], apss_weight_d2(R, d2), o.x, o.y, o.z, m0, m1, m2);
+        apss_pass_b(pb[c2 % (unsigned int)kApssLanes], apss_weight_d2(R, Rinv, d2), o.x, o.y, o.z, m0, m1, m2);
         ++c2;
     });
     double cv[6], M[15];

@@ -402,7 +402,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
     ApssWarpSm& A = wsm[warp];
     ApssList& L = A.u.list[grp];
     const uint32_t gw = vblock(F) * wpb + warp, nw = vgrid(F) * wpb;
-    const double R = F.cfg.R, r2 = R * R;
+    const double R = F.cfg.R, r2 = R * R, Rinv = 1.0 / R;
     const double pitch = F.pitch;
     // the warp's pairs gw + j nw, points 2 pair + group: positions preloaded
     // 16 pairs at a time (lane 2 i + g holds pair jbase + i's point g)
@@ -455,7 +455,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             // (the scans end with a warp barrier; pass B reads back only the
             // entries this lane rewrote)
             for (unsigned int g = gl; g < cnt; g += kApssGW) {
-                const double w = apss_weight_d2(R, L.w[g]);
+                const double w = apss_weight_d2(R, Rinv, L.w[g]);
                 const uint32_t c = L.fij[g];
                 L.w[g] = w;
                 a0 += w;
@@ -469,7 +469,7 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         const bool anyover = __any_sync(0xffffffffu, over);
         auto chunk_visit = [&](int rank, uint32_t, const Pos& o, double d2, int, int) {
             double* c = A.chunk[G::base() + rank];
-            c[0] = apss_weight_d2(R, d2);
+            c[0] = apss_weight_d2(R, Rinv, d2);
             c[1] = o.x;
             c[2] = o.y;
             c[3] = o.z;
