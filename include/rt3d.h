@@ -249,14 +249,14 @@ rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_by
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg);
 rt3d_status rt3d_report_info(rt3d_session* s, rt3d_report* out);
 /* A batch of frames: reconstruct (reconstruct.hpp:457-489) on each of the n
- * (<= 16) sessions' resident cubes, all in one launch sequence on sessions[0]'s
+ * (<= 32) sessions' resident cubes, all in one launch sequence on sessions[0]'s
  * stream (a frame axis in every kernel's grid; video streams).
  * Sessions share the device and the configuration; each session's report and
  * state then read exactly as after rt3d_reconstruct on that session.
  * RT3D_ERR_UNSUPPORTED when the cubes need different sweep layouts. */
 rt3d_status rt3d_reconstruct_batch(rt3d_session* const* sessions, int32_t n,
                                    const rt3d_recon_config* cfg);
-/* Row bands of ONE large frame: n in {1,2,4,8,16}
+/* Row bands of ONE large frame: n in {1,2,4,8,16,32}
  * sessions holding the same sensor and cube; session k reconstructs the
  * pixels of node k at depth log2(n) of parallel::pairwise_sum's tree
  * (parallel.hpp:52-61; whole rows), reading its neighbours' halo rows before

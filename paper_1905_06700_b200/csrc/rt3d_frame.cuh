@@ -229,7 +229,7 @@ struct Frame {
 // frames of one launch (a batch shares each stage / neighbour kernel): block
 // b serves frame b / bpf; kernels take the batch as a __grid_constant__
 // parameter and keep a reference to their frame
-constexpr int kMaxBatch = 16;
+constexpr int kMaxBatch = 32;
 struct FrameBatch {
     uint32_t n, bpf;
     uint32_t first, pad_;  // this launch runs frames first .. first + gridDim.x / bpf - 1

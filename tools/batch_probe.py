@@ -20,8 +20,8 @@ keys = sys.argv[1:] or ["B", "C"]
 flush = torch.empty(64 * 2 ** 20, dtype=torch.float32, device="cuda:0")
 for key in keys:
     name, spec, seed, cfg = W.CONFIGS[key]()
-    cubes = [simulate(W.config_c(f)[1], 1000 + f) for f in range(16)] if key == "C" else \
-        [simulate(spec, seed)] * 16
+    cubes = [simulate(W.config_c(f)[1], 1000 + f) for f in range(32)] if key == "C" else \
+        [simulate(spec, seed)] * 32
     for n in [int(x) for x in os.environ.get("BATCHES", "1,2,4,8").split(",")]:
         ss = [Session(0) for _ in range(n)]
         for s, c in zip(ss, cubes):
