@@ -77,8 +77,11 @@ __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant
     extern __shared__ __align__(16) unsigned char smem_raw[];
     if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
     stamp(F, PH_LAUNCH);
-    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), ld_cg(&F.ctl->pown),
-              ld_cg(&F.ctl->tc), ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
+    // pairs by ticket on large clouds only: on small ones the one counter
+    // per frame is contended (B, C: kNN +25-50 %)
+    const uint32_t P = ld_cg(&F.ctl->pown);
+    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), P, ld_cg(&F.ctl->tc),
+              ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc), P >= (1u << 20));
 }
 
 // Depth intervals of the blocks of F.zbs consecutive points of each pixel

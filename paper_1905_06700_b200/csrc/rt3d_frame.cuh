@@ -102,6 +102,7 @@ struct Ctl {
     // blocktree sweeps: block nodes handed out by ticket (by sweep parity);
     // the last block to leave a sweep resets them
     unsigned int wq_ticket[2], wq_done[2];
+    unsigned int knn_next, pad2_;  // kNN: the next pair of points by ticket (reset by every stage kernel)
 };
 constexpr unsigned long long kBarrierTimeoutNs = 2000000000ull;
 #ifndef RT3D_BARRIER_SLEEP_NS

@@ -801,7 +801,7 @@ __device__ __forceinline__ int knn_select(KnnList& L, unsigned int cnt, int k, b
 // the k-th key (at most W, the full ball).  The two groups grow their
 // windows independently; the warp rescans until both are final.
 static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, uint32_t P, int tc,
-                                 int rc, int sc) {
+                                 int rc, int sc, bool dyn = false) {
     using G = Grp<kKnnGW>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gl = G::gl(), grp = lane >> 4;
@@ -834,13 +834,43 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
         fj = __shfl_sync(0xffffffffu, pfj, src);
         t = __shfl_sync(0xffffffffu, pt, src);
     };
+    // dyn (the stand-alone kernel): pairs by ticket (F.ctl->knn_next), so a
+    // warp that drew points needing wider windows does not hold up the
+    // launch; the next ticket and its positions are fetched while the current
+    // pair is filtered.  Otherwise the warp's pairs gw + j nw.
+    unsigned int* const tkt = &F.ctl->knn_next;
+    uint32_t pair = gw;
+    int dfi = 0, dfj = 0;
+    double dtq = 0.0;
+    auto load_pos = [&](uint32_t pr) {
+        const uint32_t nl = 2u * pr + (uint32_t)grp;
+        if (nl < P) {
+            dfi = F.fi[sc][pb + nl];
+            dfj = F.fj[sc][pb + nl];
+            dtq = F.t[tc][pb + nl];
+        }
+    };
+    if (dyn) {
+        unsigned int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(tkt, 1u);
+        pair = __shfl_sync(0xffffffffu, t0, 0);
+        load_pos(pair);
+    }
     unsigned int kept = 0;
     for (uint32_t j = 0;; ++j) {
-        const uint32_t pair = gw + j * nw;
+        if (!dyn) pair = gw + j * nw;
         if (2u * pair >= P) break;  // (warp-uniform)
+        unsigned int nxt = 0;
+        if (dyn && lane == 0) nxt = atomicAdd(tkt, 1u);
         int fi, fj;
         double tq;
-        point(j, fi, fj, tq);
+        if (dyn) {
+            fi = dfi;
+            fj = dfj;
+            tq = dtq;
+        } else {
+            point(j, fi, fj, tq);
+        }
         const uint32_t nl = 2u * pair + (uint32_t)grp;
         const bool act = nl < P;
         const uint32_t n = pb + nl;
@@ -886,6 +916,10 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
                     else w = wn;
                 }
             }
+        }
+        if (dyn) {  // the next pair's positions load during the selection's tail
+            const uint32_t np = __shfl_sync(0xffffffffu, nxt, 0);
+            load_pos(np);
         }
         double result = 0.0;
         if (__any_sync(0xffffffffu, over)) {
@@ -946,6 +980,7 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             kept += (result >= F.cfg.r_min) ? 1u : 0u;  // prune's test (denoise.hpp:246)
         }
         __syncwarp();
+        if (dyn) pair = __shfl_sync(0xffffffffu, nxt, 0);
     }
     // survivors of the coming prune, one integer atomic per group (exact, any order)
     if (gl == 0 && kept) atomicAdd(&F.ctl->keep, kept);
