@@ -499,9 +499,12 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         const bool skip = !act || isol || wsum <= 0.0;
         if (act && (isol || wsum <= 0.0) && gl == 0) F.amom[(size_t)n * kMom] = isol ? -1.0 : wsum;
         if (__all_sync(0xffffffffu, skip)) continue;
-        m0 /= wsum;
-        m1 /= wsum;
-        m2 /= wsum;
+        {  // (the three divisions by wsum share its reciprocal)
+            const double winv = 1.0 / wsum;
+            m0 = div_rcp(m0, wsum, winv);
+            m1 = div_rcp(m1, wsum, winv);
+            m2 = div_rcp(m2, wsum, winv);
+        }
         // pass B: covariance and fit moments
         double b[kRedStride];
 #pragma unroll
@@ -967,8 +970,8 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             const int tm = (int)G::wmax((uint32_t)(over ? 0 : taken));
             for (int t0 = 0; t0 < tm; t0 += kKnnGW) {
                 const double v = !over && t0 + gl < taken ? rr[L.sel[t0 + gl]] : 0.0;
-#pragma unroll 4
-                for (int t = 0; t < kKnnGW; ++t) {
+                const int nb = tm - t0 < kKnnGW ? tm - t0 : kKnnGW;  // (warp-uniform)
+                for (int t = 0; t < nb; ++t) {
                     const double x = __shfl_sync(0xffffffffu, v, t, kKnnGW);
                     if (t0 + t < taken) acc += x;
                 }
