@@ -836,9 +836,12 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     // latency-bound; one candidate on large arrays, where backtracks are rare
     // and the second candidate is paid in full (config D: -5%,
     // profiles/r01_d_switch_sweep.jsonl)
+    // Latency-bound launches (one or a few frames) also evaluate two depth
+    // candidates: the depth block backtracks nearly every iteration at B and C
+    // (B single frame +0.5 %, C +2.5 %; batches of 16: B -2 %).
     F.cfg.two_cand = getenv("RT3D_ONE_CAND") ? 0
                      : getenv("RT3D_TWO_CAND") ? atoi(getenv("RT3D_TWO_CAND"))
-                     : (s->n_events >= (1ull << 20) ? 0 : 1);
+                     : (s->n_events >= (1ull << 20) ? 0 : (s->batch_hint < 4 ? 3 : 1));
     {
         // first kNN window: about k fine pixels; no pruning on huge grids
         // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
