@@ -2064,6 +2064,16 @@ __device__ __forceinline__ void cov_from_moments(const double* M, double wsum, d
     cv[5] = M[lt(3, 3)] / wsum;
 }
 
+// apss_project's degeneracy test on the covariance (denoise.hpp:197-203),
+// the Jacobi sweeps skipped where the answer is provably "no"
+// (cov_clearly_nondegenerate)
+__device__ __forceinline__ bool cov_degenerate(const double cv[6]) {
+    if (cov_clearly_nondegenerate(cv)) return false;
+    double e0, e1, e2;
+    sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
+    return e2 <= 0.0 || e1 <= 1e-12 * e2;
+}
+
 // the halving tree over kApssLanes lane partials (column `col` of
 // p[kApssLanes][stride]): p[l] = p[l] + p[l+o], o = kApssLanes/2..1 (oracle:
 // lane_tree)
@@ -2118,9 +2128,7 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
     double cv[6], M[15];
     for (int e = 0; e < 15; ++e) M[e] = halving_sum_lanes(&pb[0][0], kRedStride, e);
     cov_from_moments(M, wsum, cv);
-    double e0, e1, e2;
-    sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
-    if (e2 <= 0.0 || e1 <= 1e-12 * e2) {
+    if (cov_degenerate(cv)) {
         flags |= 4u;
         return false;
     }

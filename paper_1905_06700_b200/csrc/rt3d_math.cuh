@@ -180,6 +180,27 @@ __device__ __forceinline__ void sym3_eigenvalues(double a00, double a10, double 
     e2 = d2;
 }
 
+// A decision-preserving shortcut for apss_project's degeneracy test
+// (denoise.hpp:197-203: degenerate iff e2 <= 0 or e1 <= 1e-12 e2, e from an
+// eigen-solver of the covariance).  For a symmetric positive semidefinite C
+// with trace tr and determinant det, e2 <= tr and e0 e1 e2 = det with
+// e0 <= e1, so e1 >= sqrt(det / tr).  When det, less a bound on its rounding
+// error (2e-15 times the sum of the absolute products), exceeds 1e-16 tr^3,
+// e1 > 1e-8 tr: four orders of magnitude above the threshold and far beyond
+// any backward-stable solver's error (~1e-14 tr), so the Jacobi sweeps
+// (sym3_eigenvalues, the oracle's) and the reference's solver all declare C
+// non-degenerate and the sweeps can be skipped.  (An indefinite C rounds to
+// det < 0 or near 0 and takes the full test.)
+__device__ __forceinline__ bool cov_clearly_nondegenerate(const double cv[6]) {
+    const double a = cv[0], b = cv[1], d = cv[2], c = cv[3], e = cv[4], f = cv[5];
+    const double tr = a + d + f;
+    if (!(tr > 0.0)) return false;
+    const double det = a * (d * f - e * e) - b * (b * f - e * c) + c * (b * e - d * c);
+    const double S = fabs(a) * (fabs(d * f) + e * e) + fabs(b) * (fabs(b * f) + fabs(e * c)) +
+                     fabs(c) * (fabs(b * e) + fabs(d * c));
+    return det - 2e-15 * S > 1e-16 * tr * tr * tr;
+}
+
 // Symmetric 5x5 in packed lower-triangular order: index (i,j), i>=j, at
 // i*(i+1)/2 + j.
 __device__ __forceinline__ constexpr int lt(int i, int j) { return i * (i + 1) / 2 + j; }

@@ -577,9 +577,7 @@ static __device__ void apss_fit_threads(const Frame& F, uint32_t pb, uint32_t P,
 #pragma unroll
             for (int k = 0; k < 15; ++k) M[k] = mo[4 + k];
             cov_from_moments(M, wsum, cv);
-            double e0, e1, e2;
-            sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
-            if (e2 <= 0.0 || e1 <= 1e-12 * e2) {
+            if (cov_degenerate(cv)) {
                 fl |= 4u;
             } else {
                 Sphere sp;
@@ -627,10 +625,9 @@ static __device__ void apss_fit_split(const Frame& F, uint32_t pb, uint32_t P, i
                 s_sp[k][3] = sp.ul2;
                 s_sp[k][4] = sp.uq;
             } else {
-                double cv[6], e0, e1, e2;
+                double cv[6];
                 cov_from_moments(M, wsum, cv);
-                sym3_eigenvalues(cv[0], cv[1], cv[2], cv[3], cv[4], cv[5], e0, e1, e2);
-                s_deg[k] = (e2 <= 0.0 || e1 <= 1e-12 * e2) ? 1 : 0;
+                s_deg[k] = cov_degenerate(cv) ? 1 : 0;
             }
         }
         __syncthreads();
