@@ -1114,7 +1114,7 @@ int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_par
             q[3 * m + 2] = o->z;
             w[m] = apss_weight(R, sqrt(sqdist(o->x, o->y, o->z, pt->x, pt->y, pt->z)));
             a[0] += w[m];
-            for (int c = 0; c < 3; ++c) a[1 + c] += w[m] * q[3 * m + c];
+            for (int c = 0; c < 3; ++c) a[1 + c] = fma(w[m], q[3 * m + c], a[1 + c]);
         }
         double wsum = lane_tree(&pa[0][0], 4, 0), mean[3];
         for (int c = 0; c < 3; ++c) mean[c] = lane_tree(&pa[0][0], 4, 1 + c);
@@ -1130,16 +1130,24 @@ int oracle_apss_project(const rt3d_point* cloud, uint64_t n, const rt3d_apss_par
         for (uint64_t m = 0; m < cnt; ++m) {
             double* b = pb[m % APSS_LANES];
             double d[3] = {q[3 * m] - mean[0], q[3 * m + 1] - mean[1], q[3 * m + 2] - mean[2]};
+            /* the moment sums by fused multiply-add, as the device
+             * (apss_pass_b): one rounding per accumulation instead of two */
             int e = 0;
             for (int r = 0; r < 3; ++r) {
                 double wr = w[m] * d[r];
-                for (int c = 0; c <= r; ++c) b[e++] += wr * d[c];
+                for (int c = 0; c <= r; ++c) {
+                    b[e] = fma(wr, d[c], b[e]);
+                    ++e;
+                }
             }
             if (w[m] > 0.0) {
                 double dv[5] = {1.0, d[0], d[1], d[2], d[0] * d[0] + d[1] * d[1] + d[2] * d[2]};
                 for (int r = 0; r < 5; ++r) {
                     double wr = w[m] * dv[r];
-                    for (int c = 0; c <= r; ++c) b[e++] += wr * dv[c];
+                    for (int c = 0; c <= r; ++c) {
+                        b[e] = fma(wr, dv[c], b[e]);
+                        ++e;
+                    }
                 }
             }
         }

@@ -2050,7 +2050,10 @@ __device__ __forceinline__ void apss_pass_b(double (&b)[kRedStride], double w, d
     for (int r = 0; r < 5; ++r) {
         const double wa = w * dv[r];
 #pragma unroll
-        for (int c = 0; c <= r; ++c) b[e++] += wa * dv[c];
+        for (int c = 0; c <= r; ++c) {  // fused multiply-add (the oracle's fma)
+            b[e] = __fma_rn(wa, dv[c], b[e]);
+            ++e;
+        }
     }
 }
 
@@ -2099,9 +2102,9 @@ __device__ __forceinline__ bool apss_point(Enum&& each, const Pos& q, double R, 
         double* a = pa[cnt % (unsigned int)kApssLanes];
         ++cnt;
         a[0] += w;
-        a[1] += w * o.x;
-        a[2] += w * o.y;
-        a[3] += w * o.z;
+        a[1] = __fma_rn(w, o.x, a[1]);
+        a[2] = __fma_rn(w, o.y, a[2]);
+        a[3] = __fma_rn(w, o.z, a[3]);
     });
     if (cnt < (unsigned int)min_nbrs) {
         flags |= 1u;

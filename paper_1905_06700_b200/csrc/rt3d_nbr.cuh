@@ -459,9 +459,9 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                 const uint32_t c = L.fij[g];
                 L.w[g] = w;
                 a0 += w;
-                a1 += w * (((double)(int)(c >> 16) + 0.5) * pitch);
-                a2 += w * (((double)(int)(c & 0xFFFFu) + 0.5) * pitch);
-                a3 += w * L.z[g];
+                a1 = __fma_rn(w, ((double)(int)(c >> 16) + 0.5) * pitch, a1);
+                a2 = __fma_rn(w, ((double)(int)(c & 0xFFFFu) + 0.5) * pitch, a2);
+                a3 = __fma_rn(w, L.z[g], a3);
             }
         }
         // ball larger than the list (either group): accumulate chunk by chunk
@@ -484,9 +484,9 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
                         const double* c = A.chunk[G::base() + r];
                         const double w = c[0];
                         a0 += w;
-                        a1 += w * c[1];
-                        a2 += w * c[2];
-                        a3 += w * c[3];
+                        a1 = __fma_rn(w, c[1], a1);
+                        a2 = __fma_rn(w, c[2], a2);
+                        a3 = __fma_rn(w, c[3], a3);
                     }
                     c1 += (unsigned int)nm;
                 },
