@@ -375,6 +375,92 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
     }
 }
 
+// Both groups' points in one fine cell (consecutive points of one pixel)
+// share their window: one 32-lane scan of it with two memberships per
+// candidate, d^2 = (dx^2 + dy^2) + dz^2 left to right as ball_scan forms it,
+// so the lateral part is shared exactly; each member goes to its point's list
+// in ascending index order (group g's list is Ls[g]).
+__device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt, int fi,
+                                               int fj, double qx, double qy, double qz0,
+                                               double qz1, double r2, ApssList* Ls,
+                                               unsigned int& c0, unsigned int& c1) {
+    using G = Grp<32>;
+    const int lane = threadIdx.x & 31;
+    const int W = F.cfg.W;
+    const double* tt = F.t[tc];
+    const int32_t* FI = F.fi[sc];
+    const int32_t* FJ = F.fj[sc];
+    const uint32_t lt = G::lt(), le = G::le();
+    int ci0, ci1;
+    window_rows(F, fi, W, ci0, ci1);
+    for (int rb = ci0; rb <= ci1; rb += 32) {
+        uint32_t m0r, lenr;
+        rows_load<32>(F, sc, fi, fj, W, rb, ci1, m0r, lenr);
+        const uint32_t total = rows_finish<32>(rt, m0r, lenr);
+        const bool hr = (uint32_t)lane < rt.n;
+        const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
+        const uint32_t dk = hr ? rt.m0[lane] - pk : 0u;
+        auto locate = [&](uint32_t fb) -> uint32_t {  // (rows_scan's)
+            const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= fb)) - 1;
+            const uint32_t bit = (pk > fb && pk - fb < 32u) ? 1u << (pk - fb) : 0u;
+            const int j = j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & le);
+            return fb + (uint32_t)lane + __shfl_sync(0xffffffffu, dk, j & 31);
+        };
+        bool v = (uint32_t)lane < total;
+        uint32_t mm = locate(0u);
+        RT3D_CHECK(!v || mm < F.pcap);
+        int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
+        double ctt = v ? tt[mm] : 0.0;
+        for (uint32_t fb = 0; fb < total; fb += 32) {
+            const uint32_t f2 = fb + 32 + (uint32_t)lane;
+            const bool v2 = f2 < total;
+            const uint32_t mm2 = locate(fb + 32);
+            RT3D_CHECK(!v2 || mm2 < F.pcap);
+            const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
+            const double ntt = v2 ? tt[mm2] : 0.0;
+            bool ok0 = false, ok1 = false;
+            double oz = 0.0, d20 = 0.0, d21 = 0.0;
+            if (v) {
+                const double ox = (cfi + 0.5) * F.pitch, oy = (cfj + 0.5) * F.pitch;
+                oz = ctt * F.bres;
+                const double dx = ox - qx, dy = oy - qy;
+                const double dxy = dx * dx + dy * dy;
+                const double dz0 = oz - qz0, dz1 = oz - qz1;
+                d20 = dxy + dz0 * dz0;
+                d21 = dxy + dz1 * dz1;
+                ok0 = d20 <= r2;
+                ok1 = d21 <= r2;
+            }
+            const uint32_t b0 = __ballot_sync(0xffffffffu, ok0), b1 = __ballot_sync(0xffffffffu, ok1);
+            const uint32_t cf = ((uint32_t)cfi << 16) | (uint32_t)cfj;
+            if (ok0) {
+                const unsigned int g = c0 + (unsigned int)__popc(b0 & lt);
+                if (g < (unsigned int)kApssCap) {
+                    Ls[0].z[g] = oz;
+                    Ls[0].w[g] = d20;
+                    Ls[0].fij[g] = cf;
+                }
+            }
+            if (ok1) {
+                const unsigned int g = c1 + (unsigned int)__popc(b1 & lt);
+                if (g < (unsigned int)kApssCap) {
+                    Ls[1].z[g] = oz;
+                    Ls[1].w[g] = d21;
+                    Ls[1].fij[g] = cf;
+                }
+            }
+            c0 += (unsigned int)__popc(b0);
+            c1 += (unsigned int)__popc(b1);
+            v = v2;
+            mm = mm2;
+            cfi = nfi;
+            cfj = nfj;
+            ctt = ntt;
+        }
+        __syncwarp();
+    }
+}
+
 // p[l] = p[l] + p[l+o], o = GW/2..1, over the group's lanes; the sum lands
 // in the group's lane 0 and is broadcast (oracle: lane_tree)
 template <int GW>
@@ -444,11 +530,21 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             }
         };
         auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
-        if (F.zb)
+        // the two points in one fine cell (consecutive points of a pixel):
+        // one shared 32-lane scan of their common window
+        const int ofi = __shfl_xor_sync(0xffffffffu, fi, 16), ofj = __shfl_xor_sync(0xffffffffu, fj, 16);
+        const bool share = !F.zb && __all_sync(0xffffffffu, act && fi == ofi && fj == ofj);
+        if (share) {
+            const double qz0 = __shfl_sync(0xffffffffu, q.z, 0), qz1 = __shfl_sync(0xffffffffu, q.z, 16);
+            unsigned int c0 = 0, c1 = 0;
+            ball_scan_pair(F, tc, sc, A.rt[0], fi, fj, q.x, q.y, qz0, qz1, r2, A.u.list, c0, c1);
+            cnt = grp ? c1 : c0;
+        } else if (F.zb) {
             ball_scan_blocks<kApssGW, false>(F, tc, sc, A.rt[grp], A.rng[grp], fi, fj, q, r2, visitA,
                                              flushA, -1, act);
-        else
+        } else {
             ball_scan<kApssGW, false>(F, tc, sc, A.rt[grp], fi, fj, q, r2, visitA, flushA, -1, act);
+        }
         const bool over = cnt > (unsigned int)kApssCap;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         if (!over) {
