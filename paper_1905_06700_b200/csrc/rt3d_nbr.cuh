@@ -379,14 +379,14 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
 // share their window: one 32-lane scan of it with two memberships per
 // candidate, d^2 = (dx^2 + dy^2) + dz^2 left to right as ball_scan forms it,
 // so the lateral part is shared exactly; each member goes to its point's list
-// in ascending index order (group g's list is Ls[g]).
+// in ascending index order: put(g, slot, index, z, d^2, fine cell).
+template <typename Put>
 __device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt, int fi,
                                                int fj, double qx, double qy, double qz0,
-                                               double qz1, double r2, ApssList* Ls,
+                                               double qz1, double r2, int W, Put put,
                                                unsigned int& c0, unsigned int& c1) {
     using G = Grp<32>;
     const int lane = threadIdx.x & 31;
-    const int W = F.cfg.W;
     const double* tt = F.t[tc];
     const int32_t* FI = F.fi[sc];
     const int32_t* FJ = F.fj[sc];
@@ -433,22 +433,8 @@ __device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, R
             }
             const uint32_t b0 = __ballot_sync(0xffffffffu, ok0), b1 = __ballot_sync(0xffffffffu, ok1);
             const uint32_t cf = ((uint32_t)cfi << 16) | (uint32_t)cfj;
-            if (ok0) {
-                const unsigned int g = c0 + (unsigned int)__popc(b0 & lt);
-                if (g < (unsigned int)kApssCap) {
-                    Ls[0].z[g] = oz;
-                    Ls[0].w[g] = d20;
-                    Ls[0].fij[g] = cf;
-                }
-            }
-            if (ok1) {
-                const unsigned int g = c1 + (unsigned int)__popc(b1 & lt);
-                if (g < (unsigned int)kApssCap) {
-                    Ls[1].z[g] = oz;
-                    Ls[1].w[g] = d21;
-                    Ls[1].fij[g] = cf;
-                }
-            }
+            if (ok0) put(0, c0 + (unsigned int)__popc(b0 & lt), mm, oz, d20, cf);
+            if (ok1) put(1, c1 + (unsigned int)__popc(b1 & lt), mm, oz, d21, cf);
             c0 += (unsigned int)__popc(b0);
             c1 += (unsigned int)__popc(b1);
             v = v2;
@@ -537,7 +523,15 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         if (share) {
             const double qz0 = __shfl_sync(0xffffffffu, q.z, 0), qz1 = __shfl_sync(0xffffffffu, q.z, 16);
             unsigned int c0 = 0, c1 = 0;
-            ball_scan_pair(F, tc, sc, A.rt[0], fi, fj, q.x, q.y, qz0, qz1, r2, A.u.list, c0, c1);
+            ball_scan_pair(F, tc, sc, A.rt[0], fi, fj, q.x, q.y, qz0, qz1, r2, F.cfg.W,
+                           [&](int g, unsigned int slot, uint32_t, double oz, double d2, uint32_t cf) {
+                               if (slot < (unsigned int)kApssCap) {
+                                   A.u.list[g].z[slot] = oz;
+                                   A.u.list[g].w[slot] = d2;
+                                   A.u.list[g].fij[slot] = cf;
+                               }
+                           },
+                           c0, c1);
             cnt = grp ? c1 : c0;
         } else if (F.zb) {
             ball_scan_blocks<kApssGW, false>(F, tc, sc, A.rt[grp], A.rng[grp], fi, fj, q, r2, visitA,
