@@ -231,6 +231,10 @@ rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable);
  * per-block progress records and fault records; NULL otherwise. */
 void* rt3d_debug_buffer(rt3d_session* s);
 rt3d_status rt3d_kernel_times(rt3d_session* s, double* ms, uint64_t* launches);
+/* Frames replay cached CUDA graphs (keyed by the launch's frame parameters:
+ * buffers, configuration and sweep layout, not the cube's contents): the
+ * graphs captured and the graph launches made by this session so far. */
+rt3d_status rt3d_graph_counts(rt3d_session* s, uint64_t* captures, uint64_t* launches);
 
 /* Upload the sensor (IRF tables, gain, dead mask) and the photon cube.  They
  * stay resident until replaced.  Validation follows SensorModel's ctor

@@ -543,10 +543,16 @@ struct DevBuf {
     ~DevBuf() { release(); }  // every member buffer goes with its session
     cudaError_t ensure(size_t bytes) {
         if (bytes <= cap && p) return cudaSuccess;
+        const size_t old = p ? cap : 0;
         if (p) cudaFree(p);
         p = nullptr;
         cap = 0;
+        // geometric growth: a stream of cubes of varying size reallocates a
+        // few times, not at every larger one, so buffer addresses (and the
+        // frame graphs cached by them) stay put
         size_t want = std::max<size_t>(bytes, 256);
+        if (old) want = std::max(want, old + old / 2);
+        want = (want + 65535) & ~(size_t)65535;
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
         return e;
@@ -655,6 +661,7 @@ struct rt3d_session {
         uint64_t used = 0;
     } gc[4];  // pipelined frames alternate two cube slots: two live graphs
     uint64_t gc_clock = 0;
+    uint64_t graph_captures = 0, graph_launches = 0;  // (rt3d_graph_counts)
 };
 
 namespace {
@@ -1167,8 +1174,10 @@ rt3d_status launch_frames(rt3d_session* s, Frame* Fs, int n, int first = 0, int 
         g.bpf = bpf;
         g.zero_ctl = zero_ctl;
         g.valid = true;
+        ++s->graph_captures;
     }
     s->gc[hit].used = ++s->gc_clock;
+    ++s->graph_launches;
     CUDA_TRY(cudaGraphLaunch(s->gc[hit].exec, s->stream));
     return RT3D_OK;
 }
@@ -1486,6 +1495,13 @@ rt3d_status rt3d_session_time_kernels(rt3d_session* s, int enable) {
         s->kt_ms[k] = 0.0;
         s->kt_n[k] = 0;
     }
+    return RT3D_OK;
+}
+
+rt3d_status rt3d_graph_counts(rt3d_session* s, uint64_t* captures, uint64_t* launches) {
+    if (!s || !captures || !launches) return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d_graph_counts: null argument");
+    *captures = s->graph_captures;
+    *launches = s->graph_launches;
     return RT3D_OK;
 }
 

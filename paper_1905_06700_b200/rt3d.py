@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
     _bind(L, "rt3d_session_time_kernels", _st, [SS, C.c_int])
     _bind(L, "rt3d_kernel_times", _st, [SS, P(_dbl), P(_u64)])
+    _bind(L, "rt3d_graph_counts", _st, [SS, P(_u64), P(_u64)])
     _bind(L, "rt3d_debug_buffer", C.c_void_p, [SS])
     _bind(L, "rt3d_set_sensor", _st, [SS, P(Sensor)])
     _bind(L, "rt3d_set_cube", _st, [SS, P(Cube)])
@@ -112,7 +113,7 @@ def _check(status: int):
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
     "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
-    "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_debug_buffer",
+    "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_graph_counts", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
     "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_reconstruct_bands", "rt3d_band_pixels",
     "rt3d_band_plan", "rt3d_measure_fp64_peak",
@@ -296,6 +297,12 @@ class Session:
     def time_kernels(self, enable: bool = True):
         """CUDA events around every launch on the session stream (resets totals)."""
         _check(lib().rt3d_session_time_kernels(self.h, int(enable)))
+
+    def graph_counts(self):
+        """(graphs captured, graph launches) of this session so far."""
+        c, n = _u64(), _u64()
+        _check(lib().rt3d_graph_counts(self.h, C.byref(c), C.byref(n)))
+        return c.value, n.value
 
     def kernel_times(self) -> dict:
         """{class: (total_ms, launches)} since time_kernels(); synchronizes."""

@@ -42,6 +42,32 @@ def test_stream_of_different_cubes_matches_reconstruct(gpu):
         assert rep["final_nll"] == ref["trace"][-1], k
 
 
+def test_stream_of_different_cubes_replays_one_graph(gpu):
+    """Frames of a stream differ in their cubes, not in their launch
+    parameters: one captured graph serves them all (a key holding
+    per-cube sizes would re-capture every frame)."""
+    cubes = [simulate(SPEC, seed) for seed in (31, 32, 33, 34, 35, 36)]
+    assert len({len(c.events) for c in cubes}) > 1
+
+    def stream(s):
+        pend = [s.frame_submit(c, CFG) for c in cubes[:2]]
+        for c in cubes[2:]:
+            s.frame_collect(pend.pop(0))
+            pend.append(s.frame_submit(c, CFG))
+        for t in pend:
+            s.frame_collect(t)
+
+    with Session(0) as s:
+        s.set_scene(cubes[0])
+        stream(s)                       # buffers grow to the stream's sizes
+        c0, n0 = s.graph_counts()
+        assert c0 <= 4                  # (a graph per in-flight slot, and growth)
+        stream(s)
+        c1, n1 = s.graph_counts()
+    assert n1 - n0 == len(cubes)
+    assert c1 == c0                     # every frame of the second pass replays
+
+
 def test_collect_with_too_small_buffer_keeps_the_frame(gpu):
     c = simulate(SPEC, 21)
     gpu.set_scene(c)
