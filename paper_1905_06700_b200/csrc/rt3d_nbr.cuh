@@ -375,15 +375,57 @@ __device__ __forceinline__ void ball_scan_blocks(const Frame& F, int tc, int sc,
     }
 }
 
-// Both groups' points in one fine cell (consecutive points of one pixel)
-// share their window: one 32-lane scan of it with two memberships per
-// candidate, d^2 = (dx^2 + dy^2) + dz^2 left to right as ball_scan forms it,
-// so the lateral part is shared exactly; each member goes to its point's list
-// in ascending index order: put(g, slot, index, z, d^2, fine cell).
+// Candidate range of window row ci = rb + lane for two points in the same
+// or adjacent fine cells: the union of their disc-culled column ranges
+// (contiguous: each holds its own point's column, and those differ by at most
+// one); a row outside one point's disc takes the other's range.
+__device__ __forceinline__ void rows_load_union(const Frame& F, int sc, int fiA, int fjA, int fiB,
+                                                int fjB, int W, int rb, int ci1, uint32_t& m0,
+                                                uint32_t& len) {
+    const int s = F.s;
+    const double rw = F.cfg.R / F.pitch;
+    const double lim2 = rw * rw * (1.0 + 1e-9);
+    const int ci = rb + (int)(threadIdx.x & 31);
+    m0 = 0;
+    len = 0;
+    if (ci > ci1) return;
+    int c0 = 0x7fffffff, c1 = -1;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int fi = p ? fiB : fiA, fj = p ? fjB : fjA;
+        const int r_lo = ci * s, r_hi = r_lo + s - 1;
+        const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
+        const double rem = lim2 - (double)dmin * (double)dmin;
+        if (rem >= 0.0) {  // (rows_load's bound for this point)
+            int wj = (int)floor(sqrt(rem));
+            wj = wj > W ? W : wj;
+            int b0 = fj - wj, b1 = fj + wj;
+            b0 = b0 < 0 ? 0 : b0;
+            b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
+            const int a = coarse_of(F, b0), e = coarse_of(F, b1);
+            c0 = a < c0 ? a : c0;
+            c1 = e > c1 ? e : c1;
+        }
+    }
+    if (c1 >= 0) {
+        const uint32_t prow = (uint32_t)ci * F.cols;
+        const uint32_t* bo = F.bo[sc];
+        m0 = bo[prow + c0];
+        len = bo[prow + c1 + 1] - m0;
+    }
+}
+
+// The warp's two points in the same or adjacent fine cells (consecutive
+// points of a pixel, or of neighbouring pixels): one 32-lane scan of the
+// union of their windows with two memberships per candidate, each formed
+// with its own point exactly as ball_scan forms it (a candidate outside a
+// point's own window lies outside its ball and fails the test), each member
+// going to its point's list in ascending index order:
+// put(g, slot, index, z, d^2, fine cell).
 template <typename Put>
-__device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt, int fi,
-                                               int fj, double qx, double qy, double qz0,
-                                               double qz1, double r2, int W, Put put,
+__device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt,
+                                               int fiA, int fjA, int fiB, int fjB, const Pos& qA,
+                                               const Pos& qB, double r2, int W, Put put,
                                                unsigned int& c0, unsigned int& c1) {
     using G = Grp<32>;
     const int lane = threadIdx.x & 31;
@@ -391,11 +433,14 @@ __device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, R
     const int32_t* FI = F.fi[sc];
     const int32_t* FJ = F.fj[sc];
     const uint32_t lt = G::lt(), le = G::le();
-    int ci0, ci1;
-    window_rows(F, fi, W, ci0, ci1);
+    int ci0, ci1, di0, di1;
+    window_rows(F, fiA, W, ci0, ci1);
+    window_rows(F, fiB, W, di0, di1);
+    ci0 = di0 < ci0 ? di0 : ci0;
+    ci1 = di1 > ci1 ? di1 : ci1;
     for (int rb = ci0; rb <= ci1; rb += 32) {
         uint32_t m0r, lenr;
-        rows_load<32>(F, sc, fi, fj, W, rb, ci1, m0r, lenr);
+        rows_load_union(F, sc, fiA, fjA, fiB, fjB, W, rb, ci1, m0r, lenr);
         const uint32_t total = rows_finish<32>(rt, m0r, lenr);
         const bool hr = (uint32_t)lane < rt.n;
         const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
@@ -423,11 +468,10 @@ __device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, R
             if (v) {
                 const double ox = (cfi + 0.5) * F.pitch, oy = (cfj + 0.5) * F.pitch;
                 oz = ctt * F.bres;
-                const double dx = ox - qx, dy = oy - qy;
-                const double dxy = dx * dx + dy * dy;
-                const double dz0 = oz - qz0, dz1 = oz - qz1;
-                d20 = dxy + dz0 * dz0;
-                d21 = dxy + dz1 * dz1;
+                const double dxA = ox - qA.x, dyA = oy - qA.y, dzA = oz - qA.z;
+                const double dxB = ox - qB.x, dyB = oy - qB.y, dzB = oz - qB.z;
+                d20 = dxA * dxA + dyA * dyA + dzA * dzA;
+                d21 = dxB * dxB + dyB * dyB + dzB * dzB;
                 ok0 = d20 <= r2;
                 ok1 = d21 <= r2;
             }
@@ -516,14 +560,18 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
             }
         };
         auto flushA = [&](int nm) { cnt += (unsigned int)nm; };
-        // the two points in one fine cell (consecutive points of a pixel):
-        // one shared 32-lane scan of their common window
+        // the two points in the same or adjacent fine cells (consecutive
+        // points of a pixel or of neighbouring pixels): one shared 32-lane
+        // scan of the union of their windows
         const int ofi = __shfl_xor_sync(0xffffffffu, fi, 16), ofj = __shfl_xor_sync(0xffffffffu, fj, 16);
-        const bool share = !F.zb && __all_sync(0xffffffffu, act && fi == ofi && fj == ofj);
+        const bool share = !F.zb && __all_sync(0xffffffffu, act && abs(fi - ofi) <= 1 && abs(fj - ofj) <= 1);
         if (share) {
-            const double qz0 = __shfl_sync(0xffffffffu, q.z, 0), qz1 = __shfl_sync(0xffffffffu, q.z, 16);
+            const int fiA = __shfl_sync(0xffffffffu, fi, 0), fjA = __shfl_sync(0xffffffffu, fj, 0);
+            const int fiB = __shfl_sync(0xffffffffu, fi, 16), fjB = __shfl_sync(0xffffffffu, fj, 16);
+            const Pos qA{(fiA + 0.5) * pitch, (fjA + 0.5) * pitch, __shfl_sync(0xffffffffu, q.z, 0)};
+            const Pos qB{(fiB + 0.5) * pitch, (fjB + 0.5) * pitch, __shfl_sync(0xffffffffu, q.z, 16)};
             unsigned int c0 = 0, c1 = 0;
-            ball_scan_pair(F, tc, sc, A.rt[0], fi, fj, q.x, q.y, qz0, qz1, r2, F.cfg.W,
+            ball_scan_pair(F, tc, sc, A.rt[0], fiA, fjA, fiB, fjB, qA, qB, r2, F.cfg.W,
                            [&](int g, unsigned int slot, uint32_t, double oz, double d2, uint32_t cf) {
                                if (slot < (unsigned int)kApssCap) {
                                    A.u.list[g].z[slot] = oz;
