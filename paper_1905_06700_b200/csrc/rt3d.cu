@@ -852,7 +852,11 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
     {
         // first kNN window: about k fine pixels; no pruning on huge grids
         // (the pruning margin assumes < 2^20 fine pixels, see knn_warps)
-        int w0 = (int)std::ceil(std::sqrt((double)std::max(cfg.knn_k, 1)) / 2.0);
+        // a window holding ~k cells; superres frames replicate each coarse
+        // pixel's K peaks to all s^2 fine cells, so their cells hold K points
+        // each (C: w0 = 1; kNN -13 % against w0 = 2)
+        const double per_cell = s->s > 1 ? (double)std::max(cfg.K, 1) : 1.0;
+        int w0 = (int)std::ceil(std::sqrt((double)std::max(cfg.knn_k, 1) / per_cell) / 2.0);
         w0 = std::max(w0, 1);
         if (F.frows >= (1 << 20) || F.fcols >= (1 << 20) || getenv("RT3D_KNN_NO_PRUNE")) w0 = cfg.W;
         if (const char* e = getenv("RT3D_KNN_W0")) w0 = std::max(1, atoi(e));
