@@ -422,17 +422,74 @@ __device__ __forceinline__ void rows_load_union(const Frame& F, int sc, int fiA,
 // point's own window lies outside its ball and fails the test), each member
 // going to its point's list in ascending index order:
 // put(g, slot, index, z, d^2, fine cell).
+// The candidates of a 32-lane row batch (rt, total) against two points,
+// each membership formed with its own point exactly as rows_scan forms it;
+// members go to put(g, slot, index, z, d^2, fine cell) in ascending index
+// order (slot = the point's member count before it).
 template <typename Put>
-__device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt,
-                                               int fiA, int fjA, int fiB, int fjB, const Pos& qA,
-                                               const Pos& qB, double r2, int W, Put put,
-                                               unsigned int& c0, unsigned int& c1) {
+__device__ __forceinline__ void rows_scan_pair(const Frame& F, int tc, int sc, const RowTab& rt,
+                                               uint32_t total, const Pos& qA, const Pos& qB,
+                                               double r2, Put put, unsigned int& c0,
+                                               unsigned int& c1) {
     using G = Grp<32>;
     const int lane = threadIdx.x & 31;
     const double* tt = F.t[tc];
     const int32_t* FI = F.fi[sc];
     const int32_t* FJ = F.fj[sc];
     const uint32_t lt = G::lt(), le = G::le();
+    const bool hr = (uint32_t)lane < rt.n;
+    const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
+    const uint32_t dk = hr ? rt.m0[lane] - pk : 0u;
+    auto locate = [&](uint32_t fb) -> uint32_t {  // (rows_scan's)
+        const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= fb)) - 1;
+        const uint32_t bit = (pk > fb && pk - fb < 32u) ? 1u << (pk - fb) : 0u;
+        const int j = j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & le);
+        return fb + (uint32_t)lane + __shfl_sync(0xffffffffu, dk, j & 31);
+    };
+    bool v = (uint32_t)lane < total;
+    uint32_t mm = locate(0u);
+    RT3D_CHECK(!v || mm < F.pcap);
+    int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
+    double ctt = v ? tt[mm] : 0.0;
+    for (uint32_t fb = 0; fb < total; fb += 32) {
+        const uint32_t f2 = fb + 32 + (uint32_t)lane;
+        const bool v2 = f2 < total;
+        const uint32_t mm2 = locate(fb + 32);
+        RT3D_CHECK(!v2 || mm2 < F.pcap);
+        const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
+        const double ntt = v2 ? tt[mm2] : 0.0;
+        bool ok0 = false, ok1 = false;
+        double oz = 0.0, d20 = 0.0, d21 = 0.0;
+        if (v) {
+            const double ox = (cfi + 0.5) * F.pitch, oy = (cfj + 0.5) * F.pitch;
+            oz = ctt * F.bres;
+            const double dxA = ox - qA.x, dyA = oy - qA.y, dzA = oz - qA.z;
+            const double dxB = ox - qB.x, dyB = oy - qB.y, dzB = oz - qB.z;
+            d20 = dxA * dxA + dyA * dyA + dzA * dzA;
+            d21 = dxB * dxB + dyB * dyB + dzB * dzB;
+            ok0 = d20 <= r2;
+            ok1 = d21 <= r2;
+        }
+        const uint32_t b0 = __ballot_sync(0xffffffffu, ok0), b1 = __ballot_sync(0xffffffffu, ok1);
+        const uint32_t cf = ((uint32_t)cfi << 16) | (uint32_t)cfj;
+        if (ok0) put(0, c0 + (unsigned int)__popc(b0 & lt), mm, oz, d20, cf);
+        if (ok1) put(1, c1 + (unsigned int)__popc(b1 & lt), mm, oz, d21, cf);
+        c0 += (unsigned int)__popc(b0);
+        c1 += (unsigned int)__popc(b1);
+        v = v2;
+        mm = mm2;
+        cfi = nfi;
+        cfj = nfj;
+        ctt = ntt;
+    }
+    __syncwarp();
+}
+
+template <typename Put>
+__device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, RowTab& rt,
+                                               int fiA, int fjA, int fiB, int fjB, const Pos& qA,
+                                               const Pos& qB, double r2, int W, Put put,
+                                               unsigned int& c0, unsigned int& c1) {
     int ci0, ci1, di0, di1;
     window_rows(F, fiA, W, ci0, ci1);
     window_rows(F, fiB, W, di0, di1);
@@ -442,52 +499,124 @@ __device__ __forceinline__ void ball_scan_pair(const Frame& F, int tc, int sc, R
         uint32_t m0r, lenr;
         rows_load_union(F, sc, fiA, fjA, fiB, fjB, W, rb, ci1, m0r, lenr);
         const uint32_t total = rows_finish<32>(rt, m0r, lenr);
-        const bool hr = (uint32_t)lane < rt.n;
-        const uint32_t pk = hr ? rt.pre[lane] : 0xffffffffu;
-        const uint32_t dk = hr ? rt.m0[lane] - pk : 0u;
-        auto locate = [&](uint32_t fb) -> uint32_t {  // (rows_scan's)
-            const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= fb)) - 1;
-            const uint32_t bit = (pk > fb && pk - fb < 32u) ? 1u << (pk - fb) : 0u;
-            const int j = j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & le);
-            return fb + (uint32_t)lane + __shfl_sync(0xffffffffu, dk, j & 31);
-        };
-        bool v = (uint32_t)lane < total;
-        uint32_t mm = locate(0u);
-        RT3D_CHECK(!v || mm < F.pcap);
-        int cfi = v ? FI[mm] : 0, cfj = v ? FJ[mm] : 0;
-        double ctt = v ? tt[mm] : 0.0;
-        for (uint32_t fb = 0; fb < total; fb += 32) {
-            const uint32_t f2 = fb + 32 + (uint32_t)lane;
-            const bool v2 = f2 < total;
-            const uint32_t mm2 = locate(fb + 32);
-            RT3D_CHECK(!v2 || mm2 < F.pcap);
-            const int nfi = v2 ? FI[mm2] : 0, nfj = v2 ? FJ[mm2] : 0;
-            const double ntt = v2 ? tt[mm2] : 0.0;
-            bool ok0 = false, ok1 = false;
-            double oz = 0.0, d20 = 0.0, d21 = 0.0;
-            if (v) {
-                const double ox = (cfi + 0.5) * F.pitch, oy = (cfj + 0.5) * F.pitch;
-                oz = ctt * F.bres;
-                const double dxA = ox - qA.x, dyA = oy - qA.y, dzA = oz - qA.z;
-                const double dxB = ox - qB.x, dyB = oy - qB.y, dzB = oz - qB.z;
-                d20 = dxA * dxA + dyA * dyA + dzA * dzA;
-                d21 = dxB * dxB + dyB * dyB + dzB * dzB;
-                ok0 = d20 <= r2;
-                ok1 = d21 <= r2;
+        rows_scan_pair(F, tc, sc, rt, total, qA, qB, r2, put, c0, c1);
+    }
+}
+
+// ball_scan_pair through the depth blocks (superres frames, F.zb): the union
+// window's (coarse row, coarse pixel) pairs one per lane, a block kept when
+// its depth interval reaches either point's [z - R, z + R] (the culling test
+// of ball_scan_blocks, per point), kept runs merged into ranges.
+template <typename Put>
+__device__ __forceinline__ void ball_scan_blocks_pair(const Frame& F, int tc, int sc, RowTab& rt,
+                                                      uint2* rng, int fiA, int fjA, int fiB,
+                                                      int fjB, const Pos& qA, const Pos& qB,
+                                                      double r2, Put put, unsigned int& c0,
+                                                      unsigned int& c1) {
+    using G = Grp<32>;
+    const int lane = threadIdx.x & 31;
+    const int W = F.cfg.W;
+    const double rw = F.cfg.R / F.pitch;
+    const double lim2 = rw * rw * (1.0 + 1e-9);
+    const double zc = F.cfg.R * (1.0 + 1e-9);
+    const uint32_t* bo = F.bo[sc];
+    const uint32_t KB = F.zkb, BS = F.zbs;
+    const int s = F.s;
+    const uint32_t le = G::le();
+    int ci0, ci1, di0, di1;
+    window_rows(F, fiA, W, ci0, ci1);
+    window_rows(F, fiB, W, di0, di1);
+    ci0 = di0 < ci0 ? di0 : ci0;
+    ci1 = di1 > ci1 ? di1 : ci1;
+    for (int rb = ci0; rb <= ci1; rb += 32) {
+        // lane r: coarse row rb + r, the union of both points' disc-culled
+        // coarse columns (rows_load_union's)
+        const int ci = rb + lane;
+        int c0c = 0;
+        uint32_t npx = 0;
+        if (ci <= ci1) {
+            int a0 = 0x7fffffff, a1 = -1;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const int fi = p ? fiB : fiA, fj = p ? fjB : fjA;
+                const int r_lo = ci * s, r_hi = r_lo + s - 1;
+                const int dmin = fi < r_lo ? r_lo - fi : (fi > r_hi ? fi - r_hi : 0);
+                const double rem = lim2 - (double)dmin * (double)dmin;
+                if (rem >= 0.0) {
+                    int wj = (int)floor(sqrt(rem));
+                    wj = wj > W ? W : wj;
+                    int b0 = fj - wj, b1 = fj + wj;
+                    b0 = b0 < 0 ? 0 : b0;
+                    b1 = b1 > F.fcols - 1 ? F.fcols - 1 : b1;
+                    const int x0 = coarse_of(F, b0), x1 = coarse_of(F, b1);
+                    a0 = x0 < a0 ? x0 : a0;
+                    a1 = x1 > a1 ? x1 : a1;
+                }
             }
-            const uint32_t b0 = __ballot_sync(0xffffffffu, ok0), b1 = __ballot_sync(0xffffffffu, ok1);
-            const uint32_t cf = ((uint32_t)cfi << 16) | (uint32_t)cfj;
-            if (ok0) put(0, c0 + (unsigned int)__popc(b0 & lt), mm, oz, d20, cf);
-            if (ok1) put(1, c1 + (unsigned int)__popc(b1 & lt), mm, oz, d21, cf);
-            c0 += (unsigned int)__popc(b0);
-            c1 += (unsigned int)__popc(b1);
-            v = v2;
-            mm = mm2;
-            cfi = nfi;
-            cfj = nfj;
-            ctt = ntt;
+            if (a1 >= 0) {
+                c0c = a0;
+                npx = (uint32_t)(a1 - a0 + 1);
+            }
         }
-        __syncwarp();
+        uint32_t inc = npx;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t ppre = inc - npx, P = __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t pk = npx ? ppre : 0xffffffffu;
+        const uint32_t nem = __ballot_sync(0xffffffffu, npx != 0u);
+        const int fne = nem ? __ffs((int)nem) - 1 : 0;
+        for (uint32_t ub = 0; ub < P; ub += 32) {
+            const int j0 = __popc(__ballot_sync(0xffffffffu, pk <= ub)) - 1;
+            const uint32_t bit = (pk > ub && pk - ub < 32u) ? 1u << (pk - ub) : 0u;
+            const int L = fne + j0 + __popc(__reduce_or_sync(0xffffffffu, bit) & le);
+            const uint32_t Lpre = __shfl_sync(0xffffffffu, ppre, L & 31);
+            const int Lc0 = __shfl_sync(0xffffffffu, c0c, L & 31);
+            const uint32_t u = ub + (uint32_t)lane;
+            uint32_t n0 = 0, n1 = 0, keep = 0;
+            if (u < P) {
+                const uint32_t p = (uint32_t)(rb + L) * (uint32_t)F.cols + (uint32_t)Lc0 + (u - Lpre);
+                const double2* zp = F.zb + (size_t)p * KB;
+#pragma unroll
+                for (uint32_t k = 0; k < 4u; ++k) {
+                    if (k < KB) {
+                        const double2 zz = zp[k];
+                        const bool kA = !(zz.x - qA.z > zc || qA.z - zz.y > zc);
+                        const bool kB = !(zz.x - qB.z > zc || qB.z - zz.y > zc);
+                        if (kA || kB) keep |= 1u << k;
+                    }
+                }
+                n0 = bo[p];
+                n1 = bo[p + 1];
+            }
+            const uint32_t starts = keep & ~(keep << 1);
+            const uint32_t kc = (uint32_t)__popc(starts);
+            uint32_t kinc = kc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, kinc, o);
+                if (lane >= o) kinc += y;
+            }
+            const uint32_t KT = __shfl_sync(0xffffffffu, kinc, 31);
+            uint32_t wpos = kinc - kc;
+            for (uint32_t st = starts; st; st &= st - 1u) {
+                const int a = __ffs((int)st) - 1;
+                const int e = __ffs((int)(~keep & ~((1u << a) - 1u))) - 1;
+                const uint32_t lo = n0 + (uint32_t)a * BS;
+                const uint32_t hi = min(n0 + (uint32_t)e * BS, n1);
+                rng[wpos++] = make_uint2(lo, hi - lo);
+            }
+            __syncwarp();
+            for (uint32_t gb = 0; gb < KT; gb += 32) {
+                const uint32_t g = gb + (uint32_t)lane;
+                const uint2 rg = g < KT ? rng[g] : make_uint2(0u, 0u);
+                const uint32_t total = rows_finish<32>(rt, rg.x, rg.y);
+                rows_scan_pair(F, tc, sc, rt, total, qA, qB, r2, put, c0, c1);
+            }
+            __syncwarp();
+        }
     }
 }
 
@@ -564,22 +693,25 @@ static __device__ void apss_moment_warps(const Frame& F, ApssWarpSm* wsm, uint32
         // points of a pixel or of neighbouring pixels): one shared 32-lane
         // scan of the union of their windows
         const int ofi = __shfl_xor_sync(0xffffffffu, fi, 16), ofj = __shfl_xor_sync(0xffffffffu, fj, 16);
-        const bool share = !F.zb && __all_sync(0xffffffffu, act && abs(fi - ofi) <= 1 && abs(fj - ofj) <= 1);
+        const bool share = __all_sync(0xffffffffu, act && abs(fi - ofi) <= 1 && abs(fj - ofj) <= 1);
         if (share) {
             const int fiA = __shfl_sync(0xffffffffu, fi, 0), fjA = __shfl_sync(0xffffffffu, fj, 0);
             const int fiB = __shfl_sync(0xffffffffu, fi, 16), fjB = __shfl_sync(0xffffffffu, fj, 16);
             const Pos qA{(fiA + 0.5) * pitch, (fjA + 0.5) * pitch, __shfl_sync(0xffffffffu, q.z, 0)};
             const Pos qB{(fiB + 0.5) * pitch, (fjB + 0.5) * pitch, __shfl_sync(0xffffffffu, q.z, 16)};
             unsigned int c0 = 0, c1 = 0;
-            ball_scan_pair(F, tc, sc, A.rt[0], fiA, fjA, fiB, fjB, qA, qB, r2, F.cfg.W,
-                           [&](int g, unsigned int slot, uint32_t, double oz, double d2, uint32_t cf) {
-                               if (slot < (unsigned int)kApssCap) {
-                                   A.u.list[g].z[slot] = oz;
-                                   A.u.list[g].w[slot] = d2;
-                                   A.u.list[g].fij[slot] = cf;
-                               }
-                           },
-                           c0, c1);
+            auto put = [&](int g, unsigned int slot, uint32_t, double oz, double d2, uint32_t cf) {
+                if (slot < (unsigned int)kApssCap) {
+                    A.u.list[g].z[slot] = oz;
+                    A.u.list[g].w[slot] = d2;
+                    A.u.list[g].fij[slot] = cf;
+                }
+            };
+            if (F.zb)  // (rng[0..1] as one 128-range scratch)
+                ball_scan_blocks_pair(F, tc, sc, A.rt[0], &A.rng[0][0], fiA, fjA, fiB, fjB, qA, qB, r2,
+                                      put, c0, c1);
+            else
+                ball_scan_pair(F, tc, sc, A.rt[0], fiA, fjA, fiB, fjB, qA, qB, r2, F.cfg.W, put, c0, c1);
             cnt = grp ? c1 : c0;
         } else if (F.zb) {
             ball_scan_blocks<kApssGW, false>(F, tc, sc, A.rt[grp], A.rng[grp], fi, fj, q, r2, visitA,
