@@ -1,7 +1,9 @@
 """GPU: batched frames (rt3d_reconstruct_batch, a frame axis in every
 kernel's grid) give, session by session, exactly what rt3d_reconstruct gives
 on that session's cube: clouds, backgrounds, nll traces and step
-diagnostics bit for bit, for batches of 1..16 frames of different cubes."""
+diagnostics bit for bit, for batches of 1..32 frames of different cubes (single
+frames and small batches take other kernel variants than large batches: the
+split fit, two depth candidates per sweep, lane-group sweeps)."""
 import numpy as np
 import pytest
 
@@ -45,7 +47,7 @@ def _batch(cubes, cfg):
             s.close()
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 8, 16])
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 16, 32])
 def test_batch_matches_single_frames(gpu, n):
     cubes = [simulate(SPEC, 40 + k) for k in range(n)]
     singles = []
