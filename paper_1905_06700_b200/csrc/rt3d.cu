@@ -1591,7 +1591,7 @@ rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* v) {
         int ex = 0;
         const double mant = std::frexp(f.dtau, &ex);
         d.pow2 = (mant == 0.5) ? 1u : 0u;
-        d.inv_dtau = d.pow2 ? std::ldexp(1.0, 1 - ex) : 0.0;
+        d.inv_dtau = d.pow2 ? std::ldexp(1.0, 1 - ex) : 1.0 / f.dtau;  // (irf_x)
         d.lim = (double)(f.n_samples - 2);
         o += 2 * f.n_samples;
     }

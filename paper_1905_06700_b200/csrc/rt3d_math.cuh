@@ -39,11 +39,16 @@ struct IrfDev {
 };
 
 // (tau - tau_min) / dtau, sensor.hpp:71.  Division by a power of two and
-// multiplication by its (exact) reciprocal round identically, so the fast
-// path is bit-identical; any other dtau takes the IEEE division.
+// multiplication by its (exact) reciprocal round identically; any other dtau
+// takes the correctly rounded reciprocal inv_dtau with one fused correction
+// (Markstein, as apss_weight_d2: the IEEE quotient for normal operands; a
+// difference tau - tau_min of O(1) doubles is zero or normal, and a zero
+// gives +0 where the division could give -0, which the interpolation that
+// follows absorbs: s0 + (+-0) (s1 - s0) is s0 either way).
 __device__ __forceinline__ double irf_x(const IrfDev& f, double tau) {
     const double a = tau - f.tau_min;
-    return f.pow2 ? a * f.inv_dtau : a / f.dtau;
+    const double q0 = a * f.inv_dtau;
+    return f.pow2 ? q0 : __fma_rn(__fma_rn(-q0, f.dtau, a), f.inv_dtau, q0);
 }
 
 // sensor.hpp:69-75
