@@ -3,8 +3,9 @@
 // as stand-alone high-occupancy kernels, launched between the cooperative
 // stage kernels of a frame.
 //
-// Work mapping: a lane group per point (kNN: a warp; APSS: 16 lanes, two
-// points per warp).  Inside PALM every point sits at its fine-pixel centre, so
+// Work mapping: 16 lanes per point, two points per warp (APSS and kNN); two
+// points in the same or adjacent fine cells share one 32-lane scan of their
+// windows' union (APSS).  Inside PALM every point sits at its fine-pixel centre, so
 // SpatialIndex::query's ball (spatial_index.hpp:31-47, exact |q-p|^2 <= R^2,
 // ascending index) is found among the points of the coarse pixels under the
 // fine window [fi-W, fi+W] x [fj-W, fj+W], W = floor(R/pitch)+1.  The
@@ -18,7 +19,8 @@
 // halving tree p[l] += p[l+o], o = 8..1.  The oracle uses the same order
 // (oracle/rt3d_oracle.c, lane_tree, APSS_LANES), so device and oracle agree
 // bit for bit.  The sphere fit and projection then run one thread per point
-// (apss_fit_kernel) from the moments staged in L2.
+// (apss_fit_kernel; apss_fit_split_kernel for single small frames) from the
+// moments staged in L2.
 #pragma once
 
 #include "rt3d_frame.cuh"
