@@ -43,7 +43,7 @@ StageFn stage_fn_g1(int st);
 #define BATCH_FRAME(FB) (FB).f[(FB).n == 1 ? 0u : (FB).first + blockIdx.x / (FB).bpf]
 
 #ifndef RT3D_APSS_MIN_BLOCKS
-#define RT3D_APSS_MIN_BLOCKS 4
+#define RT3D_APSS_MIN_BLOCKS 5
 #endif
 __global__ void __launch_bounds__(kNbrBlock, RT3D_APSS_MIN_BLOCKS) apss_kernel(const __grid_constant__ FrameBatch FB) {
     const Frame& F = BATCH_FRAME(FB);

@@ -63,7 +63,10 @@ struct RowTab {
 
 // APSS: two points per warp, 16 lanes each (see apss_moment_warps)
 constexpr int kApssGW = kApssLanes;
-constexpr int kApssCap = 256;  // ball members kept per point for the dense passes
+// ball members kept per point for the dense passes (larger balls take
+// chunk-by-chunk rescans): 208 keeps the warp's scratch at 10.9 KB, so five
+// 4-warp blocks share an SM (the balls of B and E hold <= ~206)
+constexpr int kApssCap = 208;
 struct ApssList {
     double z[kApssCap], w[kApssCap];  // member depth, d^2 then weight
     uint32_t fij[kApssCap];           // member fine cell, fi << 16 | fj

@@ -457,3 +457,25 @@ def test_fft_lowpass_sizes(gpu, rows, cols):
                 assert np.max(np.abs(got - img)) <= 1e-12 * np.max(np.abs(img))
             half = gpu.fft_lowpass(0.5 * img, cutoff, clamp=clamp)
             assert np.max(np.abs(2.0 * half - got)) <= 1e-12 * np.max(np.abs(img))
+
+
+def test_apss_ball_overflow_matches_oracle(gpu):
+    """Balls larger than the APSS member list (kApssCap, 208 per point): a dense
+    two-surface scene with a radius of 12 fine pixels (~450 members per point)
+    takes the chunk-by-chunk rescans (pass A and pass B) for most points, on
+    both lane groups and through the shared pair scans; bit-identical to the
+    oracle."""
+    from paper_1905_06700_b200.abi import Config
+    from scenegen.scene import SceneSpec, SurfaceSpec, simulate
+    spec = SceneSpec(rows=32, cols=32, bins=300, bin_resolution_m=0.01, pixel_pitch_m=0.01,
+                     target_ppp=20.0, target_sbr=5.0,
+                     surfaces=[SurfaceSpec(depth_m=1.5), SurfaceSpec(depth_m=1.2, region=(8, 8, 24, 24))])
+    cfg = Config(max_iters=3, stop_tol=0.0, apss_radius=0.12, knn_k=7, r_min=0.2,
+                 init_max_returns=2, init_min_separation=6)
+    sc = simulate(spec, 5)
+    gpu.set_scene(sc)
+    rep = gpu.reconstruct(cfg)
+    ref = O.reconstruct(sc, cfg, "oracle")
+    assert rep["iterations"] == ref["iterations"]
+    assert np.array_equal(rep["points"], ref["points"])
+    np.testing.assert_array_equal(rep["trace"], ref["trace"])
