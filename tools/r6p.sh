@@ -1,0 +1,1 @@
+BATCHES=1,16 KT=1 timeout 600 python tools/batch_probe.py B C 2>&1 | grep "kernel_ms\|ms_per_batch" | cut -c1-200; timeout 300 python tools/profile_e.py 2 2>&1 | tail -1 | cut -c1-250
