@@ -389,6 +389,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--e2e-groups", type=int, default=1, choices=[1, 2],
+                    help="e2e session groups: 1 = full-size grids, copies between batches; "
+                         "2 = two groups with grids sized for two, copies overlapping kernels")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
     ap.add_argument("--batch", type=int, default=16,
@@ -490,13 +493,15 @@ def main():
             for _ in range(NB)]
     import ctypes as C
     from paper_1905_06700_b200 import rt3d as R
-    group_b = [Session(local) for _ in range(NB)]
+    two = args.e2e_groups == 2
+    group_b = [Session(local) for _ in range(NB)] if two else []
     for s, c in zip(group_b, cubes):
         s.set_scene(c)
-    groups = [sessions, group_b]
-    for g in groups:
-        for s in g:
-            s.set_sharing(2)
+    groups = [sessions, group_b] if two else [sessions, sessions]
+    if two:
+        for g in groups:
+            for s in g:
+                s.set_sharing(2)
 
     def upload_launch(g):
         for s, c in zip(g, pinned):
@@ -513,22 +518,29 @@ def main():
         return d2h
 
     upload_launch(groups[0])
-    upload_launch(groups[1])
     download(groups[0])
-    download(groups[1])
+    if two:
+        upload_launch(groups[1])
+        download(groups[1])
     barrier(world)
     t0 = time.perf_counter()
-    upload_launch(groups[0])
-    for k in range(n_e2e):
-        if k + 1 < n_e2e:
-            upload_launch(groups[(k + 1) % 2])  # runs while batch k finishes
-        d2h = download(groups[k % 2])
+    if two:
+        upload_launch(groups[0])
+        for k in range(n_e2e):
+            if k + 1 < n_e2e:
+                upload_launch(groups[(k + 1) % 2])  # runs while batch k finishes
+            d2h = download(groups[k % 2])
+    else:
+        for k in range(n_e2e):  # full grids; each step's copies around its batch
+            upload_launch(groups[0])
+            d2h = download(groups[0])
     e2e_s = time.perf_counter() - t0
     e2e_s = barrier_max(e2e_s, world, local)
     e2e_fps = world * n_e2e * NB / e2e_s
     h2d = sum(c.offsets.nbytes + c.events.nbytes for c in cubes)
-    for s in sessions:
-        s.set_sharing(1)
+    if two:
+        for s in sessions:
+            s.set_sharing(1)
     for s in group_b:
         s.close()
 
@@ -595,8 +607,11 @@ def main():
                     "d2h_bytes_per_step": int(d2h),
                     "mode": f"public API per step: rt3d_set_cube x{NB} from pinned host cubes, "
                             f"rt3d_reconstruct_batch, rt3d_state_copy x{NB} (cloud + background) "
-                            "into pinned host buffers; wall clock; two session groups alternate so "
-                            "one batch's copies overlap the other's kernels"},
+                            "into pinned host buffers; wall clock; "
+                            + ("two session groups alternate so one batch's copies overlap the "
+                               "other's kernels" if args.e2e_groups == 2 else
+                               "one session group with full-size grids, each step's copies "
+                               "around its batch")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic_per_launch(dom),
                          "kernel": KERNEL_NAMES[dom],
