@@ -100,10 +100,11 @@ __device__ __forceinline__ double apss_weight(double radius, double dist) {
 
 // a / d from dinv = 1.0 / d (the IEEE quotient) with one fused correction:
 // the correctly rounded quotient for normal operands (Markstein; see
-// apss_weight_d2), for a shared divisor
+// apss_weight_d2), for a shared divisor.  A zero dividend keeps its sign
+// (the correction would turn -0 into +0).
 __device__ __forceinline__ double div_rcp(double a, double d, double dinv) {
     const double q0 = a * dinv;
-    return __fma_rn(__fma_rn(-q0, d, a), dinv, q0);
+    return a == 0.0 ? q0 : __fma_rn(__fma_rn(-q0, d, a), dinv, q0);
 }
 
 // apss_weight(radius, sqrt(d2)) for d2 >= 0, rinv = 1.0 / radius (the IEEE
