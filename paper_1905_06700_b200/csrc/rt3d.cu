@@ -80,8 +80,30 @@ __global__ void __launch_bounds__(kNbrBlock, 7) knn_kernel(const __grid_constant
     // pairs by ticket on large clouds only: on small ones the one counter
     // per frame is contended (B, C: kNN +25-50 %)
     const uint32_t P = ld_cg(&F.ctl->pown);
-    knn_warps(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), P, ld_cg(&F.ctl->tc),
-              ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc), P >= (1u << 20));
+    knn_warps<1>(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), P, ld_cg(&F.ctl->tc),
+                 ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc), P >= (1u << 20));
+}
+
+// every point to its final window in one kernel (superres frames: their
+// first windows are small, and most points need the wider one)
+__global__ void __launch_bounds__(kNbrBlock, 7) knn_full_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
+    stamp(F, PH_LAUNCH);
+    const uint32_t P = ld_cg(&F.ctl->pown);
+    knn_warps<0>(F, reinterpret_cast<KnnWarpSm*>(smem_raw), ld_cg(&F.ctl->pbase), P, ld_cg(&F.ctl->tc),
+                 ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc), P >= (1u << 20));
+}
+
+// the points knn_kernel left for a wider window, over the full ball
+__global__ void __launch_bounds__(kNbrBlock, 7) knn_rescan_kernel(const __grid_constant__ FrameBatch FB) {
+    const Frame& F = BATCH_FRAME(FB);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (ld_cg(&F.ctl->stop) || ld_cg(&F.ctl->abort)) return;
+    if (ld_cg(&F.ctl->knn_nres) == 0u) return;
+    knn_warps<2>(F, reinterpret_cast<KnnWarpSm*>(smem_raw), 0u, 0u, ld_cg(&F.ctl->tc),
+                 ld_cg(&F.ctl->rc), ld_cg(&F.ctl->sc));
 }
 
 // Depth intervals of the blocks of F.zbs consecutive points of each pixel
@@ -615,7 +637,7 @@ struct rt3d_session {
     DevBuf t[2], r[2], b[2], pix[2], fi[2], fj[2], fl[2], bo[2];
     size_t pcap = 0;
     DevBuf gt, ct, gr, cr, gb, cb, oog, lam, blk, bmax, cnt, btot, part, mig[2];
-    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom, zb;
+    DevBuf pk_t, pk_resp, pk_mass, pk_int, npk, nval, fft_re, fft_im, amom, zb, knn_list;
     DevBuf ctl, diag, trace, outpts, misc, prof, tblk, tbmax;
     bool profile = false;
     Ctl* h_ctl = nullptr;  // pinned staging
@@ -821,6 +843,8 @@ rt3d_status build_frame(rt3d_session* s, Frame& F, const Cfg& cfg, int max_iters
             F.zbs = bs;
         }
     }
+    CUDA_TRY(s->knn_list.ensure(std::max<size_t>(s->pcap, 1) * 4));
+    F.knn_list = s->knn_list.as<uint32_t>();
     F.ctl = s->ctl.as<Ctl>();
     F.dbg = s->d_dbg;
     F.prof = nullptr;
@@ -1113,9 +1137,21 @@ rt3d_status launch_frames_direct(rt3d_session* s, const Frame* Fs, int n, int fi
             if ((st = stage(ST_INTENSITY, it))) return st;
             if ((st = halo(2))) return st;  // t after APSS, r after the intensity step
             st = timed_launch(s, RT3D_KC_KNN, [&]() -> rt3d_status {
-                knn_kernel<<<s->grid_knn * count, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
-                             s->stream>>>(fb_knn);
-                CUDA_TRY(cudaGetLastError());
+                // first windows then the deferred wider ones (no superres:
+                // B kNN -11 %, E -7 %); superres frames in one kernel (C: the
+                // split is +18 %)
+                if (F.s > 1) {
+                    knn_full_kernel<<<s->grid_knn * count, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
+                                      s->stream>>>(fb_knn);
+                    CUDA_TRY(cudaGetLastError());
+                } else {
+                    knn_kernel<<<s->grid_knn * count, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
+                                 s->stream>>>(fb_knn);
+                    CUDA_TRY(cudaGetLastError());
+                    knn_rescan_kernel<<<s->grid_knn * count, kNbrBlock, sizeof(KnnWarpSm) * kNbrWarps,
+                                        s->stream>>>(fb_knn);
+                    CUDA_TRY(cudaGetLastError());
+                }
                 return RT3D_OK;
             });
             if (st) return st;
@@ -1374,6 +1410,10 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
         CUDA_TRY(cudaFuncSetAttribute(apss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(ApssWarpSm) * kNbrWarps)));
         CUDA_TRY(cudaFuncSetAttribute(knn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(KnnWarpSm) * kNbrWarps)));
+        CUDA_TRY(cudaFuncSetAttribute(knn_rescan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(sizeof(KnnWarpSm) * kNbrWarps)));
+        CUDA_TRY(cudaFuncSetAttribute(knn_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(sizeof(KnnWarpSm) * kNbrWarps)));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, apss_kernel, kNbrBlock,
                                                                sizeof(ApssWarpSm) * kNbrWarps));

@@ -102,7 +102,8 @@ struct Ctl {
     // blocktree sweeps: block nodes handed out by ticket (by sweep parity);
     // the last block to leave a sweep resets them
     unsigned int wq_ticket[2], wq_done[2];
-    unsigned int knn_next, pad2_;  // kNN: the next pair of points by ticket (reset by every stage kernel)
+    unsigned int knn_next;  // kNN: the next pair of points by ticket (reset by every stage kernel)
+    unsigned int knn_nres;  // kNN: points deferred to the rescan kernel (reset likewise)
 };
 constexpr unsigned long long kBarrierTimeoutNs = 2000000000ull;
 #ifndef RT3D_BARRIER_SLEEP_NS
@@ -203,6 +204,7 @@ struct Frame {
     // before each APSS launch; empty blocks (+inf, -inf)); nullptr: off
     double2* zb;
     uint32_t zkb, zbs;
+    uint32_t* knn_list;  // points the kNN's first windows left to the rescan kernel
     double* fft_re;   // 2*npix complex scratch (fft background mode)
     double* fft_im;
     // launch geometry: this frame's blocks are blk0 .. blk0 + nblk - 1 of the

@@ -1075,6 +1075,12 @@ __device__ __forceinline__ int knn_select(KnnList& L, unsigned int cnt, int k, b
 // final; otherwise the window grows to the first ring whose bound exceeds
 // the k-th key (at most W, the full ball).  The two groups grow their
 // windows independently; the warp rescans until both are final.
+// MODE 0: every point to its final window (one kernel).  MODE 1 (knn_kernel):
+// every point's first window; a point that needs a wider one is appended to
+// F.knn_list (its result left to MODE 2).  MODE 2 (knn_rescan_kernel): the
+// listed points over the full ball W, which holds every candidate of any
+// window the growth could stop at, so the selection is the same.
+template <int MODE = 0>
 static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, uint32_t P, int tc,
                                  int rc, int sc, bool dyn = false) {
     using G = Grp<kKnnGW>;
@@ -1125,6 +1131,10 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             dtq = F.t[tc][pb + nl];
         }
     };
+    if (MODE == 2) {  // the listed points
+        P = ld_cg(&F.ctl->knn_nres);
+        dyn = false;
+    }
     if (dyn) {
         unsigned int t0 = 0;
         if (lane == 0) t0 = atomicAdd(tkt, 1u);
@@ -1137,21 +1147,29 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
         if (2u * pair >= P) break;  // (warp-uniform)
         unsigned int nxt = 0;
         if (dyn && lane == 0) nxt = atomicAdd(tkt, 1u);
-        int fi, fj;
-        double tq;
-        if (dyn) {
+        int fi = 0, fj = 0;
+        double tq = 0.0;
+        const uint32_t nl = 2u * pair + (uint32_t)grp;
+        const bool act = nl < P;
+        uint32_t n = pb + nl;
+        if (MODE == 2) {
+            n = act ? F.knn_list[nl] : 0u;
+            if (act) {
+                fi = F.fi[sc][n];
+                fj = F.fj[sc][n];
+                tq = F.t[tc][n];
+            }
+        } else if (dyn) {
             fi = dfi;
             fj = dfj;
             tq = dtq;
         } else {
             point(j, fi, fj, tq);
         }
-        const uint32_t nl = 2u * pair + (uint32_t)grp;
-        const bool act = nl < P;
-        const uint32_t n = pb + nl;
         RT3D_CHECK(!act || n < F.pcap);
         const Pos q{(fi + 0.5) * pitch, (fj + 0.5) * pitch, tq * F.bres};
-        int w = w0;
+        int w = MODE == 2 ? Wfull : w0;
+        bool deferred = false;
         int taken = 0;
         unsigned int cnt = 0;
         bool done = !act, over = false;
@@ -1191,7 +1209,12 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
                     else w = wn;
                 }
             }
+            if (MODE == 1 && !done) {  // a wider window: the rescan kernel's
+                deferred = true;
+                done = true;
+            }
         }
+        if (MODE == 1 && deferred && gl == 0) F.knn_list[atomicAdd(&F.ctl->knn_nres, 1u)] = n;
         if (dyn) {  // the next pair's positions load during the selection's tail
             const uint32_t np = __shfl_sync(0xffffffffu, nxt, 0);
             load_pos(np);
@@ -1239,9 +1262,9 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
         // loads in parallel, the sum in rank order
         {
             double acc = 0.0;
-            const int tm = (int)G::wmax((uint32_t)(over ? 0 : taken));
+            const int tm = (int)G::wmax((uint32_t)(over || deferred ? 0 : taken));
             for (int t0 = 0; t0 < tm; t0 += kKnnGW) {
-                const double v = !over && t0 + gl < taken ? rr[L.sel[t0 + gl]] : 0.0;
+                const double v = !over && !deferred && t0 + gl < taken ? rr[L.sel[t0 + gl]] : 0.0;
                 const int nb = tm - t0 < kKnnGW ? tm - t0 : kKnnGW;  // (warp-uniform)
                 for (int t = 0; t < nb; ++t) {
                     const double x = __shfl_sync(0xffffffffu, v, t, kKnnGW);
@@ -1250,7 +1273,7 @@ static __device__ void knn_warps(const Frame& F, KnnWarpSm* wsm, uint32_t pb, ui
             }
             if (act && !over) result = taken == 0 ? rr[n] : acc / (double)taken;
         }
-        if (act && gl == 0) {
+        if (act && !deferred && gl == 0) {
             F.r[rc ^ 1][n] = result;
             kept += (result >= F.cfg.r_min) ? 1u : 0u;  // prune's test (denoise.hpp:246)
         }

@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kBlock, StageOcc<G>::kBlocks)
         c->cmax = sm.c.cmax;
         c->keep = 0;  // the next kNN pass counts from zero
         c->knn_next = 0;
+        c->knn_nres = 0;
         c->P = global_P(F);  // (row bands: all bands' points, from barc)
         F.ctl->tc = tc;
         F.ctl->rc = rc;
