@@ -238,7 +238,9 @@ rt3d_status rt3d_graph_counts(rt3d_session* s, uint64_t* captures, uint64_t* lau
 
 /* Upload the sensor (IRF tables, gain, dead mask) and the photon cube.  They
  * stay resident until replaced.  Validation follows SensorModel's ctor
- * (sensor.hpp:138-148) and PhotonCube::validate (cube.hpp:84-112). */
+ * (sensor.hpp:138-148) and PhotonCube::validate (cube.hpp:84-112); the cube's
+ * per-pixel checks run on the device after the upload, so a cube rejected
+ * there (RT3D_ERR_FORMAT "... at pixel p") leaves the session without one. */
 rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* sensor);
 rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* cube);
 /* decode_cube / read_cube (io.hpp:116-150) from an SPCB byte buffer straight

@@ -9,6 +9,7 @@
 // palm_step) through the program switch.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -23,6 +24,18 @@
 #include "rt3d_nbr.cuh"
 #include "rt3d_stage.cuh"
 #include "rt3d_sim.cuh"
+
+namespace {
+// NVTX range over a public entry point (header-only NVTX v3: a no-op unless a
+// profiler injects itself), so an nsys/ncu timeline shows the API calls around
+// the kernels and the graph replays.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace rt3d;
 
@@ -395,6 +408,36 @@ __global__ void spcb_gather_kernel(const uint32_t* words, const uint32_t* off, u
             ev[e0 + k] = make_uint2(bin, count);
         }
         if (kind) atomicMin(err, ((unsigned long long)p << 2) | kind);
+    }
+}
+
+// rt3d_set_cube's checks on the device (PhotonCube::validate, cube.hpp:94-106,
+// after the host checked the dimensions and the offsets' two ends): pixel p's
+// offset range and events, the first error in pixel order (and, within a
+// pixel, in event order) kept as (pixel << 3 | kind) in *err, kind 1 negative
+// range, 2 bin out of range, 3 zero count, 4 bins not increasing; the 64-bit
+// offsets narrowed into the device CSR's 32-bit table on the way.
+__global__ void cube_check_kernel(const unsigned long long* off64, uint32_t npix,
+                                  unsigned long long n_events, uint32_t n_bins, const uint2* ev,
+                                  uint32_t* off32, unsigned long long* err) {
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += gridDim.x * blockDim.x) {
+        const unsigned long long e0 = off64[p], e1 = off64[p + 1];
+        off32[p] = (uint32_t)e0;
+        if (p == 0) off32[npix] = (uint32_t)off64[npix];
+        unsigned kind = 0;
+        if (e0 > e1) {
+            kind = 1;
+        } else if (e1 <= n_events) {  // (else a later pixel's range is negative)
+            uint32_t prev = 0;
+            for (unsigned long long k = e0; k < e1 && !kind; ++k) {
+                const uint2 e = ev[k];
+                if (e.x >= n_bins) kind = 2;
+                else if (e.y < 1) kind = 3;
+                else if (k > e0 && e.x <= prev) kind = 4;
+                prev = e.x;
+            }
+        }
+        if (kind) atomicMin(err, ((unsigned long long)p << 3) | kind);
     }
 }
 
@@ -1589,6 +1632,7 @@ static rt3d_status irf_check(const rt3d_irf& f) {
 }
 
 rt3d_status rt3d_set_sensor(rt3d_session* s, const rt3d_sensor* v) {
+    NvtxRange nvtx_("rt3d_set_sensor");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!v) return fail(RT3D_ERR_INVALID_ARGUMENT, "null sensor");
@@ -1697,23 +1741,46 @@ static rt3d_status validate_cube(const rt3d_cube* c, uint32_t* off32) {
 }
 
 rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
+    NvtxRange nvtx_("rt3d_set_cube");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!c) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube");
     if (c->n_rows <= 0 || c->n_cols <= 0 || c->n_bins <= 0)
         return fail(RT3D_ERR_FORMAT, "cube: non-positive dimensions");
     const size_t npix = (size_t)c->n_rows * c->n_cols;
-    std::vector<uint32_t> off32(npix + 1);
-    if ((st = validate_cube(c, off32.data()))) return st;
+    if (!c->offsets || c->offsets[0] != 0 || c->offsets[npix] != c->n_events)
+        return fail(RT3D_ERR_FORMAT, "cube: bad offset table");
+    if (c->n_events >= (1ull << 32)) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: >= 2^32 events");
+    if (npix >= (1ull << 32) - 1) return fail(RT3D_ERR_UNSUPPORTED, "rt3d: too many pixels");
     // the device may still read the other slot's / this slot's buffers
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     s->cube_slot = 0;
+    s->have_cube = false;
     CUDA_TRY(s->off.ensure((npix + 1) * 4));
     CUDA_TRY(s->ev.ensure(std::max<uint64_t>(c->n_events, 1) * 8));
-    CUDA_TRY(cudaMemcpyAsync(s->off.p, off32.data(), (npix + 1) * 4, cudaMemcpyHostToDevice, s->stream));
+    const size_t eo = (npix + 1) * 8;  // the error word after the 64-bit offsets
+    CUDA_TRY(s->misc.ensure(eo + 8));
+    unsigned long long* err = reinterpret_cast<unsigned long long*>(static_cast<char*>(s->misc.p) + eo);
+    CUDA_TRY(cudaMemcpyAsync(s->misc.p, c->offsets, eo, cudaMemcpyHostToDevice, s->stream));
     if (c->n_events)
         CUDA_TRY(cudaMemcpyAsync(s->ev.p, c->events, c->n_events * 8, cudaMemcpyHostToDevice, s->stream));
+    CUDA_TRY(cudaMemsetAsync(err, 0xff, 8, s->stream));
+    cube_check_kernel<<<s->nsm * 8, 256, 0, s->stream>>>(
+        s->misc.as<unsigned long long>(), (uint32_t)npix, c->n_events, (uint32_t)c->n_bins,
+        s->ev.as<uint2>(), s->off.as<uint32_t>(), err);
+    CUDA_TRY(cudaGetLastError());
+    unsigned long long herr = 0;
+    CUDA_TRY(cudaMemcpyAsync(&herr, err, 8, cudaMemcpyDeviceToHost, s->stream));
     CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (herr != ~0ull) {
+        const unsigned long long p = herr >> 3;
+        const unsigned kind = (unsigned)(herr & 7u);
+        return fail(RT3D_ERR_FORMAT, kind == 1   ? "cube: negative event range at pixel %llu"
+                                     : kind == 2 ? "cube: bin out of range at pixel %llu"
+                                     : kind == 3 ? "cube: zero count at pixel %llu"
+                                                 : "cube: bins not strictly increasing at pixel %llu",
+                    p);
+    }
     s->have_cube = true;
     s->c_rows = c->n_rows;
     s->c_cols = c->n_cols;
@@ -1726,6 +1793,7 @@ rt3d_status rt3d_set_cube(rt3d_session* s, const rt3d_cube* c) {
 // host walks the per-pixel record headers only (O(pixels)); the events are
 // copied once as raw bytes and gathered + validated on the device.
 rt3d_status rt3d_set_cube_spcb(rt3d_session* s, const void* bytes, uint64_t n_bytes) {
+    NvtxRange nvtx_("rt3d_set_cube_spcb");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!bytes) return fail(RT3D_ERR_INVALID_ARGUMENT, "null SPCB buffer");
@@ -1889,6 +1957,7 @@ static rt3d_status resolve_state(rt3d_session* s) {
 }
 
 rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
+    NvtxRange nvtx_("rt3d_reconstruct");
     return run_init_like(s, cfg, PROG_RECON);
 }
 
@@ -1911,6 +1980,7 @@ rt3d_status rt3d_reconstruct(rt3d_session* s, const rt3d_recon_config* cfg) {
 // devices run one coupled launch sequence per device.  The result is
 // identical to rt3d_reconstruct for any n.
 rt3d_status rt3d_reconstruct_bands(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
+    NvtxRange nvtx_("rt3d_reconstruct_bands");
     if (!ss || n < 1 || n > kMaxBatch || (n & (n - 1)))
         return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: row bands: a power of two up to 16");
     for (int k = 0; k < n; ++k) {
@@ -2090,6 +2160,7 @@ rt3d_status rt3d_band_pixels(rt3d_session* s, uint32_t* pix0, uint32_t* pix1) {
 }
 
 rt3d_status rt3d_reconstruct_batch(rt3d_session* const* ss, int n, const rt3d_recon_config* cfg) {
+    NvtxRange nvtx_("rt3d_reconstruct_batch");
     if (!ss || n < 1 || n > kMaxBatch)
         return fail(RT3D_ERR_INVALID_ARGUMENT, "rt3d: batch of 1..%d sessions", kMaxBatch);
     for (int k = 0; k < n; ++k) {
@@ -2140,6 +2211,7 @@ static rt3d_status pipeline_init(rt3d_session* s) {
 
 rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* c, const rt3d_recon_config* cfg,
                               uint64_t* ticket) {
+    NvtxRange nvtx_("rt3d_frame_submit");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!c || !ticket) return fail(RT3D_ERR_INVALID_ARGUMENT, "null cube / ticket");
@@ -2199,6 +2271,7 @@ rt3d_status rt3d_frame_submit(rt3d_session* s, const rt3d_cube* c, const rt3d_re
 
 rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* pts, uint64_t cap,
                                uint64_t* n_points, double* background, rt3d_report* info) {
+    NvtxRange nvtx_("rt3d_frame_collect");
     rt3d_status st = require_device(s);
     if (st) return st;
     const int slot = (int)(ticket & 1u);
@@ -2243,6 +2316,7 @@ rt3d_status rt3d_frame_collect(rt3d_session* s, uint64_t ticket, rt3d_point* pts
 }
 
 rt3d_status rt3d_init_matched_filter(rt3d_session* s, const rt3d_init_params* p) {
+    NvtxRange nvtx_("rt3d_init_matched_filter");
     if (!p) return fail(RT3D_ERR_INVALID_ARGUMENT, "null params");
     rt3d_recon_config c;
     std::memset(&c, 0, sizeof c);
@@ -2312,6 +2386,7 @@ rt3d_status rt3d_state_size(rt3d_session* s, uint64_t* n) {
 }
 
 rt3d_status rt3d_state_copy(rt3d_session* s, rt3d_point* pts, double* background) {
+    NvtxRange nvtx_("rt3d_state_copy");
     rt3d_status st = require_device(s);
     if (st) return st;
     if ((st = resolve_state(s))) return st;
@@ -2345,6 +2420,7 @@ rt3d_status rt3d_state_copy(rt3d_session* s, rt3d_point* pts, double* background
 }
 
 rt3d_status rt3d_state_upload(rt3d_session* s, const rt3d_state_view* v) {
+    NvtxRange nvtx_("rt3d_state_upload");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!v) return fail(RT3D_ERR_INVALID_ARGUMENT, "null state");
@@ -2433,6 +2509,7 @@ static rt3d_status run_sweeps(rt3d_session* s, int program) {
 }
 
 rt3d_status rt3d_nll(rt3d_session* s, double* out) {
+    NvtxRange nvtx_("rt3d_nll");
     rt3d_status st = run_sweeps(s, PROG_NLL);
     if (st) return st;
     if ((st = read_ctl(s))) return st;
@@ -2443,6 +2520,7 @@ rt3d_status rt3d_nll(rt3d_session* s, double* out) {
 static rt3d_status run_grads(rt3d_session* s) { return run_sweeps(s, PROG_GRADS); }
 
 rt3d_status rt3d_grad_depth(rt3d_session* s, double* value, uint8_t* oog) {
+    NvtxRange nvtx_("rt3d_grad_depth");
     rt3d_status st = run_grads(s);
     if (st) return st;
     if ((st = copy_per_point(s, value, s->gt.p))) return st;
@@ -2450,12 +2528,14 @@ rt3d_status rt3d_grad_depth(rt3d_session* s, double* value, uint8_t* oog) {
 }
 
 rt3d_status rt3d_grad_intensity(rt3d_session* s, double* out) {
+    NvtxRange nvtx_("rt3d_grad_intensity");
     rt3d_status st = run_grads(s);
     if (st) return st;
     return copy_per_point(s, out, s->gr.p);
 }
 
 rt3d_status rt3d_grad_background(rt3d_session* s, double* out) {
+    NvtxRange nvtx_("rt3d_grad_background");
     rt3d_status st = run_grads(s);
     if (st) return st;
     if (out) {
@@ -2468,6 +2548,7 @@ rt3d_status rt3d_grad_background(rt3d_session* s, double* out) {
 
 rt3d_status rt3d_block_curvatures(rt3d_session* s, double* depth, double* intensity,
                                   double* background) {
+    NvtxRange nvtx_("rt3d_block_curvatures");
     rt3d_status st = run_grads(s);
     if (st) return st;
     if ((st = copy_per_point(s, depth, s->ct.p))) return st;
@@ -2481,6 +2562,7 @@ rt3d_status rt3d_block_curvatures(rt3d_session* s, double* depth, double* intens
 }
 
 rt3d_status rt3d_palm_step(rt3d_session* s, const rt3d_recon_config* cfg, rt3d_step_diag* diag) {
+    NvtxRange nvtx_("rt3d_palm_step");
     rt3d_status st = require_device(s);
     if (st) return st;
     if ((st = validate_cfg(cfg))) return st;
@@ -2516,6 +2598,7 @@ rt3d_status rt3d_matched_filter_peaks(rt3d_session* s, const rt3d_event* events,
                                       const rt3d_irf* irf, int32_t n_bins, int32_t k,
                                       double threshold, int32_t min_sep, rt3d_peak* out,
                                       int32_t* n_out) {
+    NvtxRange nvtx_("rt3d_matched_filter_peaks");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!irf || !out || !n_out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null argument");
@@ -2646,6 +2729,7 @@ static rt3d_status upload_points(rt3d_session* s, const rt3d_point* cloud, uint6
 rt3d_status rt3d_apss_project(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
                               const rt3d_apss_params* prm, const rt3d_point* index_cloud,
                               uint64_t n_index, double cell, rt3d_point* out) {
+    NvtxRange nvtx_("rt3d_apss_project");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!prm) return fail(RT3D_ERR_INVALID_ARGUMENT, "null params");
@@ -2680,6 +2764,7 @@ rt3d_status rt3d_apss_project(rt3d_session* s, const rt3d_point* cloud, uint64_t
 rt3d_status rt3d_knn_intensity_filter(rt3d_session* s, const rt3d_point* cloud, uint64_t n,
                                       int32_t k, const rt3d_point* index_cloud, uint64_t n_index,
                                       double cell, double radius, rt3d_point* out) {
+    NvtxRange nvtx_("rt3d_knn_intensity_filter");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (k < 1) return fail(RT3D_ERR_INVALID_ARGUMENT, "knn_intensity_filter: k must be >= 1");
@@ -2708,6 +2793,7 @@ rt3d_status rt3d_knn_intensity_filter(rt3d_session* s, const rt3d_point* cloud, 
 
 rt3d_status rt3d_prune(rt3d_session* s, const rt3d_point* cloud, uint64_t n, double r_min,
                        rt3d_point* out, uint64_t* n_out) {
+    NvtxRange nvtx_("rt3d_prune");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (r_min < 0.0) return fail(RT3D_ERR_INVALID_ARGUMENT, "prune: r_min must be >= 0");
@@ -2745,6 +2831,7 @@ rt3d_status rt3d_prune(rt3d_session* s, const rt3d_point* cloud, uint64_t n, dou
 
 rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t rows, int32_t cols,
                                     double cutoff, int32_t clamp_nonneg, double* out) {
+    NvtxRange nvtx_("rt3d_fft_lowpass_filter");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (cutoff <= 0.0 || cutoff > 1.0)
@@ -2772,6 +2859,7 @@ rt3d_status rt3d_fft_lowpass_filter(rt3d_session* s, const double* img, int32_t 
 rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est,
                           const rt3d_point* truth, uint64_t n_truth, double tau, double pitch,
                           rt3d_eval* out) {
+    NvtxRange nvtx_("rt3d_evaluate");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!out) return fail(RT3D_ERR_INVALID_ARGUMENT, "null result");
@@ -2852,6 +2940,7 @@ rt3d_status rt3d_evaluate(rt3d_session* s, const rt3d_point* est, uint64_t n_est
 rt3d_status rt3d_simulate_cube(rt3d_session* s, const rt3d_point* truth, uint64_t n_truth,
                                const double* background, uint64_t seed, uint64_t* n_events,
                                uint64_t* photons) {
+    NvtxRange nvtx_("rt3d_simulate_cube");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!s->have_sensor) return fail(RT3D_ERR_INVALID_ARGUMENT, "simulate: no sensor set");
@@ -2934,6 +3023,7 @@ rt3d_status rt3d_simulate_cube(rt3d_session* s, const rt3d_point* truth, uint64_
 
 // The session's resident cube back to the host (PhotonCube CSR, cube.hpp:24-40).
 rt3d_status rt3d_cube_copy(rt3d_session* s, uint64_t* offsets, rt3d_event* events) {
+    NvtxRange nvtx_("rt3d_cube_copy");
     rt3d_status st = require_device(s);
     if (st) return st;
     if (!s->have_cube) return fail(RT3D_ERR_INVALID_ARGUMENT, "no cube set");

@@ -142,6 +142,13 @@ def test_set_cube_validation_errors(gpu):
             lambda b: b.events.__setitem__(k + 1, (b.n_bins, 1))),
         "cube: zero count at pixel": bad(lambda b: b.events.__setitem__(k, (b.events[k]["bin"], 0))),
     }
+    # a negative range at the first pixel q whose range starts at event >= 2
+    q = int(np.argmax(sc.offsets[:-1] >= 2))
+    neg = bad(lambda b: b.offsets.__setitem__(q + 1, b.offsets[q] - 1))
+    with pytest.raises(Rt3dError) as ei:
+        gpu.set_cube(neg)
+    assert ei.value.status == 2
+    assert str(ei.value).rstrip().endswith(f"cube: negative event range at pixel {q}"), str(ei.value)
     for msg, b in cases.items():
         with pytest.raises(Rt3dError) as ei:
             gpu.set_cube(b)
