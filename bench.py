@@ -389,9 +389,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--e2e-groups", type=int, default=1, choices=[1, 2],
-                    help="e2e session groups: 1 = full-size grids, copies between batches; "
-                         "2 = two groups with grids sized for two, copies overlapping kernels")
+    ap.add_argument("--e2e-groups", type=int, default=2, choices=[1, 2],
+                    help="e2e session groups: 1 = one group, copies between batches; "
+                         "2 = two groups alternating batches (rt3d_session_after orders the "
+                         "batches on the device), one group's copies overlapping the other's "
+                         "frames")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
     ap.add_argument("--batch", type=int, default=16,
@@ -473,8 +475,9 @@ def main():
     # its NB cubes (rt3d_set_cube), reconstructs them as one batch
     # (rt3d_reconstruct_batch) and downloads every cloud and background
     # (rt3d_state_copy), all inside the timed region.  Two groups of sessions
-    # (cooperative grids sized for two, rt3d_session_set_sharing) alternate,
-    # so one batch's copies overlap the other batch's kernels.
+    # (full-size grids) alternate: rt3d_session_after queues each batch behind
+    # the other group's previous batch on the device, so the frames run one
+    # after another while one group's copies overlap the other's frames.
     import copy
     n_e2e = args.e2e_steps or max(K // 2, 6)
     pinned = []
@@ -498,14 +501,12 @@ def main():
     for s, c in zip(group_b, cubes):
         s.set_scene(c)
     groups = [sessions, group_b] if two else [sessions, sessions]
-    if two:
-        for g in groups:
-            for s in g:
-                s.set_sharing(2)
 
     def upload_launch(g):
         for s, c in zip(g, pinned):
             s.set_cube(c)
+        if two:
+            g[0].after(groups[1][0] if g is groups[0] else groups[0][0])
         Session.reconstruct_batch_async(g, cfg)
 
     def download(g):
@@ -608,8 +609,9 @@ def main():
                     "mode": f"public API per step: rt3d_set_cube x{NB} from pinned host cubes, "
                             f"rt3d_reconstruct_batch, rt3d_state_copy x{NB} (cloud + background) "
                             "into pinned host buffers; wall clock; "
-                            + ("two session groups alternate so one batch's copies overlap the "
-                               "other's kernels" if args.e2e_groups == 2 else
+                            + ("two session groups with full-size grids alternate batches "
+                               "(rt3d_session_after orders them on the device), so one batch's "
+                               "copies overlap the other's frames" if args.e2e_groups == 2 else
                                "one session group with full-size grids, each step's copies "
                                "around its batch")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -200,6 +200,12 @@ rt3d_status rt3d_session_synchronize(rt3d_session* s);
  * frames concurrently on the device (one per stream, e.g. alternate frames
  * of a video): each gets 1/n of the co-resident stage blocks.  Default 1. */
 rt3d_status rt3d_session_set_sharing(rt3d_session* s, int n_sessions);
+/* Device-side ordering, no host wait: the work queued on s from now on starts
+ * after the work queued so far on prior (an event on prior's stream).  With
+ * two groups of full-grid sessions alternating batches, one group's uploads
+ * and downloads overlap the other group's frames while the frames themselves
+ * run one after another. */
+rt3d_status rt3d_session_after(rt3d_session* s, rt3d_session* prior);
 /* The session's CUDA stream (a cudaStream_t), for callers that time the
  * stream-ordered entry points with their own CUDA events. */
 void* rt3d_session_stream(rt3d_session* s);

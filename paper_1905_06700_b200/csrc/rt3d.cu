@@ -701,6 +701,7 @@ struct rt3d_session {
     int report_iters_cap = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t xev = nullptr;  // cross-stream ordering of batched frames
+    cudaEvent_t oev = nullptr;  // rt3d_session_after's marker
     unsigned long long* h_dbg = nullptr;  // RT3D_DEBUG records (pinned copy)
     unsigned long long* d_dbg = nullptr;
     cudaStream_t side = nullptr;
@@ -1398,6 +1399,17 @@ static void set_frame_grids(rt3d_session* s) {
     }
 }
 
+rt3d_status rt3d_session_after(rt3d_session* s, rt3d_session* prior) {
+    rt3d_status st = require_device(s);
+    if (st) return st;
+    if (!prior) return fail(RT3D_ERR_INVALID_ARGUMENT, "null prior session");
+    if (prior == s) return RT3D_OK;
+    // (recorded and waited on at once: the event can be re-recorded later)
+    CUDA_TRY(cudaEventRecord(prior->oev, prior->stream));
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, prior->oev, 0));
+    return RT3D_OK;
+}
+
 rt3d_status rt3d_session_set_sharing(rt3d_session* s, int n_sessions) {
     rt3d_status st = require_device(s);
     if (st) return st;
@@ -1497,6 +1509,7 @@ rt3d_status rt3d_session_create(int device, rt3d_session** out) {
     CUDA_TRY(cudaEventCreate(&s->ev0));
     CUDA_TRY(cudaEventCreate(&s->ev1));
     CUDA_TRY(cudaEventCreateWithFlags(&s->xev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->oev, cudaEventDisableTiming));
     *out = s;
     return RT3D_OK;
 }
@@ -1528,6 +1541,7 @@ rt3d_status rt3d_session_destroy(rt3d_session* s) {
     if (s->ev0) cudaEventDestroy(s->ev0);
     if (s->ev1) cudaEventDestroy(s->ev1);
     if (s->xev) cudaEventDestroy(s->xev);
+    if (s->oev) cudaEventDestroy(s->oev);
     if (s->stream) cudaStreamDestroy(s->stream);
     delete s;  // DevBuf members free their device memory
     return RT3D_OK;

@@ -55,6 +55,7 @@ def lib() -> C.CDLL:
     _bind(L, "rt3d_session_destroy", _st, [SS])
     _bind(L, "rt3d_session_synchronize", _st, [SS])
     _bind(L, "rt3d_session_set_sharing", _st, [SS, C.c_int])
+    _bind(L, "rt3d_session_after", _st, [SS, SS])
     _bind(L, "rt3d_session_stream", C.c_void_p, [SS])
     _bind(L, "rt3d_session_profile", _st, [SS, C.c_int])
     _bind(L, "rt3d_profile_copy", _st, [SS, P(_u64), C.c_uint32, P(C.c_uint32)])
@@ -112,7 +113,7 @@ def _check(status: int):
 
 EXPORTED = [
     "rt3d_abi_version", "rt3d_last_error", "rt3d_device_count", "rt3d_session_create",
-    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
+    "rt3d_session_destroy", "rt3d_session_synchronize", "rt3d_session_set_sharing", "rt3d_session_after", "rt3d_session_stream", "rt3d_session_profile", "rt3d_profile_copy",
     "rt3d_session_time_kernels", "rt3d_kernel_times", "rt3d_graph_counts", "rt3d_debug_buffer",
     "rt3d_set_sensor", "rt3d_set_cube", "rt3d_set_cube_spcb",
     "rt3d_reconstruct", "rt3d_reconstruct_batch", "rt3d_reconstruct_bands", "rt3d_band_pixels",
@@ -319,6 +320,11 @@ class Session:
         v = _dbl()
         _check(lib().rt3d_measure_fp64_peak(self.h, C.byref(v)))
         return v.value
+
+    def after(self, prior: "Session"):
+        """rt3d_session_after: this session's next work starts after the work
+        queued so far on prior's stream (device-side, no host wait)."""
+        _check(lib().rt3d_session_after(self.h, prior.h))
 
     def set_sharing(self, n_sessions: int):
         """Size the cooperative grids so n sessions can run frames concurrently."""

@@ -93,3 +93,41 @@ def test_batch_errors(gpu):
     finally:
         s1.close()
         s2.close()
+
+
+def test_alternating_groups_pipeline(gpu):
+    """bench.py's e2e pipeline: two groups of sessions alternate batches,
+    each batch queued behind the other group's with rt3d_session_after, the
+    next group's uploads issued before this group's downloads; every frame is
+    what rt3d_reconstruct gives on its cube."""
+    n, steps = 4, 4
+    cubes = [simulate(SPEC, 70 + k) for k in range(n * steps)]
+    singles = []
+    for c in cubes:
+        gpu.set_scene(c)
+        singles.append(gpu.reconstruct(CFG))
+    groups = [[Session(0) for _ in range(n)] for _ in range(2)]
+    try:
+        for g in groups:
+            for s in g:
+                s.set_scene(cubes[0])
+
+        def launch(k):
+            g = groups[k % 2]
+            for s, c in zip(g, cubes[k * n:(k + 1) * n]):
+                s.set_cube(c)
+            g[0].after(groups[(k + 1) % 2][0])
+            Session.reconstruct_batch_async(g, CFG)
+
+        launch(0)
+        for k in range(steps):
+            if k + 1 < steps:
+                launch(k + 1)
+            for j, s in enumerate(groups[k % 2]):
+                r = s.report()
+                r["points"], r["background"] = s.state()
+                _same(r, singles[k * n + j])
+    finally:
+        for g in groups:
+            for s in g:
+                s.close()
