@@ -397,7 +397,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
     ap.add_argument("--batch", type=int, default=16,
-                    help="frames per step (rt3d_reconstruct_batch), 1..16")
+                    help="frames per step (rt3d_reconstruct_batch), 1..32")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_init()
