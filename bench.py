@@ -396,7 +396,7 @@ def main():
                          "frames")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the config-E leg")
-    ap.add_argument("--batch", type=int, default=16,
+    ap.add_argument("--batch", type=int, default=20,
                     help="frames per step (rt3d_reconstruct_batch), 1..32")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

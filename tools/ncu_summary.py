@@ -82,7 +82,7 @@ def full(path):
                    for c, v in traffic.items()}
 
 
-CMD = "python tools/profile_batch.py B 16 (one batch of 16 config-B frames, the bench step)"
+CMD = "python tools/profile_batch.py B 20 (one batch of 20 config-B frames, the bench step)"
 FULL_ARGS = "--profile-from-start off -c 6"
 
 
